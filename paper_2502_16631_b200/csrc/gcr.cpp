@@ -1,0 +1,1172 @@
+// gcr.cpp -- libgcr host runtime and C-ABI (include/gcr.h).
+//
+// Registry + phase machine (§3.1.1 lock/checkpoint/restore/unlock,
+// P:157-173), A1 page table, the chunked checkpoint pipeline
+// (K1 scan -> K2 compaction -> K4 pack -> pinned D2H on copy streams,
+// overlapped with K1 of the next chunk), the pagemap (K3), the
+// restore pipeline (H2D -> K6 scatter, K7 zero fill, K8 verify; §3.4), the
+// pinned-host pool and the image model.
+#include <algorithm>
+#include <chrono>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gcr.h"
+#include "gcr_internal.h"
+
+using namespace gcr;
+
+static_assert(sizeof(gcr_image_hdr) == 96, "header is 96 bytes");
+static_assert(offsetof(gcr_image_hdr, page_size) == 12 && offsetof(gcr_image_hdr, generation) == 16 &&
+                  offsetof(gcr_image_hdr, n_allocs) == 32 && offsetof(gcr_image_hdr, n_pages) == 40 &&
+                  offsetof(gcr_image_hdr, image_bytes) == 80 && offsetof(gcr_image_hdr, meta_crc32c) == 88,
+              "header offsets fixed by the format contract");
+static_assert(sizeof(gcr_alloc_rec) == 24 && sizeof(gcr_pagemap_entry) == 16, "record sizes");
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+uint64_t ns_since(Clock::time_point t0) {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
+}
+
+constexpr uint64_t kMaxChunk = 2ull << 30;
+constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity
+const char kMagic[8] = {'G', 'C', 'R', 'I', 'M', 'G', 0x00, 0x01};
+
+// ---------------------------------------------------------------------------
+// Pinned host pool: slabs from cudaHostAlloc, first-fit free lists with
+// coalescing.  gcr_reserve_host pre-pins slabs so the locked window never
+// pays for pinning.
+struct Slab {
+    uint8_t *base = nullptr;
+    uint64_t size = 0;
+    std::map<uint64_t, uint64_t> free_;  // offset -> length
+};
+
+struct PinnedPool {
+    std::vector<Slab *> slabs;
+    uint64_t pin_ns = 0;
+
+    ~PinnedPool() {
+        for (Slab *s : slabs) {
+            cudaFreeHost(s->base);
+            delete s;
+        }
+    }
+    static uint64_t round(uint64_t b) { return (b + 4095) & ~4095ull; }
+
+    bool add_slab(uint64_t bytes) {
+        auto t0 = Clock::now();
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        pin_ns += ns_since(t0);
+        Slab *s = new Slab;
+        s->base = static_cast<uint8_t *>(p);
+        s->size = bytes;
+        s->free_[0] = bytes;
+        slabs.push_back(s);
+        return true;
+    }
+    void *try_alloc(uint64_t bytes) {
+        for (Slab *s : slabs)
+            for (auto it = s->free_.begin(); it != s->free_.end(); ++it)
+                if (it->second >= bytes) {
+                    uint64_t off = it->first, len = it->second;
+                    s->free_.erase(it);
+                    if (len > bytes) s->free_[off + bytes] = len - bytes;
+                    return s->base + off;
+                }
+        return nullptr;
+    }
+    void *alloc(uint64_t bytes) {
+        bytes = round(std::max<uint64_t>(bytes, 1));
+        void *p = try_alloc(bytes);
+        if (p) return p;
+        if (!add_slab(std::max<uint64_t>(bytes, 256ull << 20))) return nullptr;
+        return try_alloc(bytes);
+    }
+    Slab *owner(void *p) {
+        for (Slab *s : slabs)
+            if ((uint8_t *)p >= s->base && (uint8_t *)p < s->base + s->size) return s;
+        return nullptr;
+    }
+    void release(void *p, uint64_t bytes) {
+        if (!p) return;
+        bytes = round(std::max<uint64_t>(bytes, 1));
+        Slab *s = owner(p);
+        if (!s) return;
+        uint64_t off = (uint8_t *)p - s->base;
+        auto it = s->free_.emplace(off, bytes).first;
+        auto nx = std::next(it);
+        if (nx != s->free_.end() && it->first + it->second == nx->first) {
+            it->second += nx->second;
+            s->free_.erase(nx);
+        }
+        if (it != s->free_.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second == it->first) {
+                pv->second += it->second;
+                s->free_.erase(it);
+            }
+        }
+    }
+    // keep the first new_bytes of an allocation of old_bytes
+    void shrink(void *p, uint64_t old_bytes, uint64_t new_bytes) {
+        uint64_t o = round(std::max<uint64_t>(old_bytes, 1)), n = round(std::max<uint64_t>(new_bytes, 1));
+        if (n < o) release((uint8_t *)p + n, o - n);
+    }
+    uint64_t free_bytes() const {
+        uint64_t f = 0;
+        for (Slab *s : slabs)
+            for (auto &kv : s->free_) f += kv.second;
+        return f;
+    }
+};
+
+struct RegEntry {
+    uint32_t id;
+    uint64_t dptr, bytes;
+};
+
+struct Chunk {
+    uint64_t tile_begin, tile_end, page_begin, page_end;
+};
+
+}  // namespace
+
+struct gcr_image {
+    gcr_ctx *ctx = nullptr;
+    gcr_image_hdr hdr{};
+    std::vector<gcr_alloc_rec> allocs;
+    gcr_pagemap_entry *pagemap = nullptr;
+    uint64_t pagemap_cap = 0;
+    uint32_t *digests = nullptr;
+    uint64_t digests_cap = 0;
+    uint8_t *data = nullptr;
+    uint64_t data_cap = 0;
+};
+
+struct gcr_ctx {
+    int device = 0;
+    int n_sms = 148;
+    gcr_config cfg{};
+    gcr_phase phase = GCR_RUNNING;
+    std::string err;
+    gcr_stats stats{};
+
+    std::vector<RegEntry> reg;
+    uint32_t next_id = 1;
+    std::vector<cudaStream_t> watched;
+
+    cudaStream_t compute = nullptr;
+    std::vector<cudaStream_t> copy;
+    std::vector<uint8_t *> slots;
+    CrcTables *tables_d = nullptr;
+    PinnedPool pool;
+    std::vector<gcr_image *> images;
+
+    // layout (A1), rebuilt when the registry changes
+    bool layout_valid = false;
+    uint32_t P = 0, lg = 0;
+    uint64_t n_pages = 0, n_tiles = 0;
+    std::vector<AllocDev> allocs_h;
+    std::vector<Chunk> chunks;
+    AllocDev *allocs_d = nullptr;
+    uint32_t *page_alloc = nullptr, *tile_alloc = nullptr;
+    uint32_t *D[2] = {nullptr, nullptr};
+    uint8_t *cls = nullptr;
+    TileInfo *tile_info = nullptr;
+    uint32_t *tile_off = nullptr;
+    uint32_t *slice_raw = nullptr;
+    uint8_t *slice_nz = nullptr;
+    uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
+    void *entries_d = nullptr;
+    ChunkTotals *totals_d = nullptr, *totals_h = nullptr;
+    unsigned long long *misc_d = nullptr, *misc_h = nullptr;  // [0] n_entries, [1] verify count, [2] first bad
+    uint32_t z_page = 0;
+
+    // restore descriptor buffers (grow on demand)
+    uint8_t *desc_d = nullptr, *desc_h = nullptr;
+    uint64_t desc_cap = 0;
+
+    // incremental parent state (R-8)
+    bool have_parent = false;
+    int parent_idx = 0;
+    uint64_t parent_gen = 0;
+    uint64_t next_gen = 1;
+
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t ev() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+};
+
+namespace {
+
+gcr_status fail(gcr_ctx *c, gcr_status s, const std::string &msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+#define CUDA_TRY(ctx, call)                                                                            \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) {                                                                       \
+            cudaGetLastError();                                                                        \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? GCR_E_NOMEM : GCR_E_CUDA,               \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                           \
+        }                                                                                              \
+    } while (0)
+
+#define LAUNCH_TRY(ctx, call)                                                                          \
+    do {                                                                                               \
+        int n_ = (call);                                                                               \
+        if (n_ < 0) {                                                                                  \
+            cudaError_t e_ = cudaGetLastError();                                                       \
+            return fail(ctx, GCR_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));         \
+        }                                                                                              \
+        ctx->stats.kernel_launches += (uint64_t)n_;                                                   \
+    } while (0)
+
+uint32_t log2u(uint64_t v) {
+    uint32_t r = 0;
+    while ((1ull << r) < v) r++;
+    return r;
+}
+
+bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P - 1u)) == 0; }
+
+void free_layout(gcr_ctx *c) {
+    void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
+                    c->tile_off, c->slice_raw, c->slice_nz, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
+                    c->entries_d, c->totals_d, c->misc_d};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (c->totals_h) cudaFreeHost(c->totals_h);
+    if (c->misc_h) cudaFreeHost(c->misc_h);
+    c->allocs_d = nullptr;
+    c->page_alloc = c->tile_alloc = c->D[0] = c->D[1] = nullptr;
+    c->cls = nullptr;
+    c->tile_info = nullptr;
+    c->tile_off = c->slice_raw = nullptr;
+    c->slice_nz = nullptr;
+    c->pm_blk_cnt = c->pm_blk_off = c->run_start = nullptr;
+    c->entries_d = nullptr;
+    c->totals_d = c->totals_h = nullptr;
+    c->misc_d = c->misc_h = nullptr;
+    c->layout_valid = false;
+    c->have_parent = false;
+}
+
+// A1: per-allocation page/tile bases, chunk plan, device buffers, K0.
+gcr_status build_layout(gcr_ctx *c) {
+    if (c->layout_valid) return GCR_OK;
+    free_layout(c);
+    const uint32_t P = c->cfg.page_size, lg = log2u(P);
+    c->P = P;
+    c->lg = lg;
+    c->allocs_h.clear();
+    uint64_t g = 0, t = 0;
+    for (const RegEntry &r : c->reg) {
+        AllocDev a{};
+        a.base = r.dptr;
+        a.bytes = r.bytes;
+        a.page0 = g;
+        a.tile0 = t;
+        a.n_pages = (uint32_t)((r.bytes + P - 1) / P);
+        a.n_tiles = P <= kTileBytes ? (uint32_t)((a.n_pages + (kTileBytes / P) - 1) / (kTileBytes / P))
+                                    : a.n_pages * (P / kTileBytes);
+        a.tail_len = (uint32_t)(r.bytes - (uint64_t)(a.n_pages - 1) * P);
+        a.z_tail = zero_digest(a.tail_len);
+        g += a.n_pages;
+        t += a.n_tiles;
+        c->allocs_h.push_back(a);
+    }
+    c->n_pages = g;
+    c->n_tiles = t;
+    c->z_page = zero_digest(P);
+    // chunk plan: uniform tile ranges; page ranges from the allocation walk
+    const uint64_t ct = c->cfg.chunk_bytes / kTileBytes;
+    c->chunks.clear();
+    for (uint64_t tb = 0; tb < t; tb += ct) {
+        Chunk ch{tb, std::min(t, tb + ct), 0, 0};
+        c->chunks.push_back(ch);
+    }
+    auto page_of_tile = [&](uint64_t tile) -> uint64_t {
+        if (tile >= t) return g;
+        // allocation containing tile (linear walk is fine: done once per layout)
+        size_t lo = 0, hi = c->allocs_h.size();
+        while (hi - lo > 1) {
+            size_t mid = (lo + hi) / 2;
+            if (c->allocs_h[mid].tile0 <= tile) lo = mid; else hi = mid;
+        }
+        const AllocDev &a = c->allocs_h[lo];
+        const uint64_t lt = tile - a.tile0;
+        return a.page0 + (P <= kTileBytes ? lt * (kTileBytes / P) : lt / (P / kTileBytes));
+    };
+    for (Chunk &ch : c->chunks) {
+        ch.page_begin = page_of_tile(ch.tile_begin);
+        ch.page_end = page_of_tile(ch.tile_end);
+    }
+    const uint64_t na = c->allocs_h.size(), nblk = (g + 4095) / 4096, nch = c->chunks.size();
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaMalloc(&c->allocs_d, sizeof(AllocDev) * na));
+    CUDA_TRY(c, cudaMalloc(&c->page_alloc, 4 * g));
+    CUDA_TRY(c, cudaMalloc(&c->tile_alloc, 4 * t));
+    CUDA_TRY(c, cudaMalloc(&c->D[0], 4 * g));
+    CUDA_TRY(c, cudaMalloc(&c->D[1], 4 * g));
+    CUDA_TRY(c, cudaMalloc(&c->cls, g));
+    CUDA_TRY(c, cudaMalloc(&c->tile_info, sizeof(TileInfo) * t));
+    CUDA_TRY(c, cudaMalloc(&c->tile_off, 4 * t));
+    if (P > kTileBytes) {
+        CUDA_TRY(c, cudaMalloc(&c->slice_raw, 4 * t));
+        CUDA_TRY(c, cudaMalloc(&c->slice_nz, t));
+    }
+    CUDA_TRY(c, cudaMalloc(&c->pm_blk_cnt, 4 * nblk));
+    CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
+    CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
+    CUDA_TRY(c, cudaMalloc(&c->entries_d, sizeof(gcr_pagemap_entry) * g));
+    CUDA_TRY(c, cudaMalloc(&c->totals_d, sizeof(ChunkTotals) * nch));
+    CUDA_TRY(c, cudaHostAlloc(&c->totals_h, sizeof(ChunkTotals) * nch, cudaHostAllocDefault));
+    CUDA_TRY(c, cudaMalloc(&c->misc_d, 8 * 4));
+    CUDA_TRY(c, cudaHostAlloc(&c->misc_h, 8 * 4, cudaHostAllocDefault));
+    CUDA_TRY(c, cudaMemcpyAsync(c->allocs_d, c->allocs_h.data(), sizeof(AllocDev) * na, cudaMemcpyHostToDevice,
+                                c->compute));
+    LAUNCH_TRY(c, launch_build_page_table(c->allocs_d, (uint32_t)na, c->page_alloc, c->tile_alloc,
+                                          P > kTileBytes ? P / kTileBytes : 1, P <= kTileBytes ? kTileBytes / P : 1,
+                                          c->compute));
+    CUDA_TRY(c, cudaStreamSynchronize(c->compute));
+    c->layout_valid = true;
+    c->have_parent = false;
+    return GCR_OK;
+}
+
+void sync_all(gcr_ctx *c) {
+    cudaStreamSynchronize(c->compute);
+    for (cudaStream_t s : c->copy) cudaStreamSynchronize(s);
+    cudaGetLastError();
+}
+
+void image_free_buffers(gcr_image *img) {
+    if (!img || !img->ctx) return;
+    PinnedPool &p = img->ctx->pool;
+    p.release(img->pagemap, img->pagemap_cap);
+    p.release(img->digests, img->digests_cap);
+    p.release(img->data, img->data_cap);
+    img->pagemap = nullptr;
+    img->digests = nullptr;
+    img->data = nullptr;
+}
+
+void destroy_image(gcr_ctx *c, gcr_image *img) {
+    image_free_buffers(img);
+    auto it = std::find(c->images.begin(), c->images.end(), img);
+    if (it != c->images.end()) c->images.erase(it);
+    delete img;
+}
+
+uint32_t meta_crc(const gcr_image *img) {
+    gcr_image_hdr h = img->hdr;
+    h.meta_crc32c = 0;
+    uint32_t s = host_crc32c_update(0xFFFFFFFFu, &h, sizeof h);
+    s = host_crc32c_update(s, img->allocs.data(), sizeof(gcr_alloc_rec) * img->allocs.size());
+    s = host_crc32c_update(s, img->pagemap, sizeof(gcr_pagemap_entry) * img->hdr.n_entries);
+    s = host_crc32c_update(s, img->digests, 4ull * img->hdr.n_pages);
+    return s ^ 0xFFFFFFFFu;
+}
+
+uint64_t pages_of(uint64_t bytes, uint32_t P) { return (bytes + P - 1) / P; }
+uint64_t page_len(uint64_t bytes, uint32_t P, uint64_t p) {
+    uint64_t rest = bytes - p * (uint64_t)P;
+    return rest < P ? rest : P;
+}
+
+// Structural check of an image against its own alloc table (CORRUPT on failure).
+gcr_status check_pagemap(gcr_ctx *c, const gcr_image *img) {
+    const gcr_image_hdr &h = img->hdr;
+    const uint32_t P = h.page_size;
+    if (!valid_page_size(P)) return fail(c, GCR_E_CORRUPT, "image page size invalid");
+    uint64_t e = 0, np = 0, nz = 0, npa = 0, pb = 0, tot = 0;
+    for (uint32_t a = 0; a < h.n_allocs; a++) {
+        const gcr_alloc_rec &r = img->allocs[a];
+        if (r.bytes == 0) return fail(c, GCR_E_CORRUPT, "image alloc of 0 bytes");
+        const uint64_t m = pages_of(r.bytes, P);
+        tot += m;
+        uint64_t p = 0;
+        while (p < m) {
+            if (e >= h.n_entries) return fail(c, GCR_E_CORRUPT, "pagemap too short");
+            const gcr_pagemap_entry &pe = img->pagemap[e];
+            if (pe.vaddr != r.vaddr + p * P || pe.nr_pages == 0 || p + pe.nr_pages > m)
+                return fail(c, GCR_E_CORRUPT, "pagemap entry inconsistent with alloc table");
+            if (pe.flags == GCR_PE_PRESENT) {
+                np += pe.nr_pages;
+                uint64_t last = p + pe.nr_pages;
+                pb += (last == m) ? (uint64_t)(pe.nr_pages - 1) * P + page_len(r.bytes, P, m - 1)
+                                  : (uint64_t)pe.nr_pages * P;
+            } else if (pe.flags == GCR_PE_ZERO) {
+                nz += pe.nr_pages;
+            } else if (pe.flags == GCR_PE_PARENT) {
+                npa += pe.nr_pages;
+            } else {
+                return fail(c, GCR_E_CORRUPT, "pagemap flags invalid");
+            }
+            p += pe.nr_pages;
+            e++;
+        }
+    }
+    if (e != h.n_entries || tot != h.n_pages || np != h.n_present || nz != h.n_zero || npa != h.n_parent ||
+        pb != h.image_bytes)
+        return fail(c, GCR_E_CORRUPT, "pagemap counts inconsistent with header");
+    return GCR_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+gcr_status gcr_config_default(gcr_config *out) {
+    if (!out) return GCR_E_INVAL;
+    out->page_size = 65536;
+    out->n_copy_streams = 2;
+    out->chunk_bytes = 256ull << 20;
+    out->n_staging_slots = 0;
+    out->verify = 1;
+    out->lock_timeout_ms = 10000;
+    return GCR_OK;
+}
+
+gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) {
+    if (!out) return GCR_E_INVAL;
+    *out = nullptr;
+    gcr_config cfg;
+    gcr_config_default(&cfg);
+    if (cfg_in) cfg = *cfg_in;
+    if (!valid_page_size(cfg.page_size) || cfg.n_copy_streams < 1 || cfg.n_copy_streams > 8 ||
+        cfg.chunk_bytes == 0 || cfg.chunk_bytes % cfg.page_size != 0 || cfg.chunk_bytes % kTileBytes != 0 ||
+        cfg.chunk_bytes > kMaxChunk || (cfg.n_staging_slots != 0 && cfg.n_staging_slots != cfg.n_copy_streams))
+        return GCR_E_INVAL;
+    if (!crc_self_test()) return GCR_E_INVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) {
+        cudaGetLastError();
+        return GCR_E_CUDA;
+    }
+    gcr_ctx *c = new (std::nothrow) gcr_ctx;
+    if (!c) return GCR_E_NOMEM;
+    c->device = cuda_device;
+    c->cfg = cfg;
+    c->stats.first_bad_page = UINT64_MAX;
+    auto bail = [&](gcr_status s) {
+        gcr_destroy(c);
+        return s;
+    };
+    if (cudaSetDevice(cuda_device) != cudaSuccess) return bail(GCR_E_CUDA);
+    cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
+    for (uint32_t i = 0; i < cfg.n_copy_streams; i++) {
+        cudaStream_t s;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
+        c->copy.push_back(s);
+        void *slot = nullptr;
+        if (cudaMalloc(&slot, cfg.chunk_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return bail(GCR_E_NOMEM);
+        }
+        c->slots.push_back(static_cast<uint8_t *>(slot));
+    }
+    CrcTables *th = new CrcTables;
+    build_tables(th);
+    if (cudaMalloc(&c->tables_d, sizeof(CrcTables)) != cudaSuccess ||
+        cudaMemcpy(c->tables_d, th, sizeof(CrcTables), cudaMemcpyHostToDevice) != cudaSuccess) {
+        delete th;
+        cudaGetLastError();
+        return bail(GCR_E_NOMEM);
+    }
+    delete th;
+    *out = c;
+    return GCR_OK;
+}
+
+gcr_status gcr_destroy(gcr_ctx *c) {
+    if (!c) return GCR_E_INVAL;
+    cudaSetDevice(c->device);
+    sync_all(c);
+    while (!c->images.empty()) destroy_image(c, c->images.back());
+    free_layout(c);
+    for (uint8_t *s : c->slots) cudaFree(s);
+    for (cudaStream_t s : c->copy) cudaStreamDestroy(s);
+    if (c->compute) cudaStreamDestroy(c->compute);
+    if (c->tables_d) cudaFree(c->tables_d);
+    if (c->desc_d) cudaFree(c->desc_d);
+    if (c->desc_h) cudaFreeHost(c->desc_h);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    cudaGetLastError();
+    delete c;
+    return GCR_OK;
+}
+
+gcr_status gcr_register(gcr_ctx *c, uint64_t dptr, uint64_t bytes, uint32_t *id_out) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "register: not RUNNING");
+    if (!id_out || dptr == 0 || bytes == 0 || dptr % 16 || bytes % 16)
+        return fail(c, GCR_E_INVAL, "register: null, empty or not 16-byte aligned (R-2)");
+    if (dptr + bytes < dptr) return fail(c, GCR_E_INVAL, "register: range overflows");
+    for (const RegEntry &r : c->reg)
+        if (dptr < r.dptr + r.bytes && r.dptr < dptr + bytes)
+            return fail(c, GCR_E_INVAL, "register: overlaps a registered allocation");
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, reinterpret_cast<void *>(dptr)) != cudaSuccess ||
+        at.type != cudaMemoryTypeDevice || at.device != c->device) {
+        cudaGetLastError();
+        return fail(c, GCR_E_INVAL, "register: not device memory of this ctx's device");
+    }
+    cudaPointerAttributes at2{};
+    if (cudaPointerGetAttributes(&at2, reinterpret_cast<void *>(dptr + bytes - 1)) != cudaSuccess ||
+        at2.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        return fail(c, GCR_E_INVAL, "register: range end is not device memory");
+    }
+    c->reg.push_back(RegEntry{c->next_id, dptr, bytes});
+    *id_out = c->next_id++;
+    c->layout_valid = false;
+    c->have_parent = false;
+    return GCR_OK;
+}
+
+gcr_status gcr_unregister(gcr_ctx *c, uint32_t id) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "unregister: not RUNNING");
+    for (size_t i = 0; i < c->reg.size(); i++)
+        if (c->reg[i].id == id) {
+            c->reg.erase(c->reg.begin() + i);
+            c->layout_valid = false;
+            c->have_parent = false;
+            return GCR_OK;
+        }
+    return fail(c, GCR_E_INVAL, "unregister: unknown alloc_id");
+}
+
+gcr_status gcr_watch_stream(gcr_ctx *c, void *stream) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "watch_stream: not RUNNING");
+    c->watched.push_back(static_cast<cudaStream_t>(stream));
+    return GCR_OK;
+}
+
+gcr_status gcr_reserve_host(gcr_ctx *c, uint64_t bytes) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "reserve_host: not RUNNING");
+    if (bytes == 0) return GCR_OK;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    if (!c->pool.add_slab(PinnedPool::round(bytes))) return fail(c, GCR_E_NOMEM, "reserve_host: cudaHostAlloc failed");
+    c->stats.pinned_alloc_ns = c->pool.pin_ns;
+    return GCR_OK;
+}
+
+gcr_status gcr_lock(gcr_ctx *c) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "lock: not RUNNING");
+    auto t0 = Clock::now();
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    // "waiting for active operations ... to complete" with a timeout
+    std::vector<cudaStream_t> ws = c->watched;
+    if (ws.empty()) ws.push_back(nullptr);
+    const uint64_t limit = c->cfg.lock_timeout_ms * 1000000ull;
+    for (;;) {
+        bool idle = true;
+        for (cudaStream_t s : ws) {
+            cudaError_t e = cudaStreamQuery(s);
+            if (e == cudaErrorNotReady) {
+                idle = false;
+                break;
+            }
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(c, GCR_E_CUDA, std::string("lock: cudaStreamQuery: ") + cudaGetErrorString(e));
+            }
+        }
+        if (idle) break;
+        if (ns_since(t0) >= limit) {
+            c->stats.lock_ns = ns_since(t0);
+            return fail(c, GCR_E_TIMEOUT, "lock: watched streams not idle within lock_timeout_ms (rolled back)");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    gcr_status s = build_layout(c);
+    if (s != GCR_OK) {
+        free_layout(c);
+        return s;
+    }
+    c->phase = GCR_LOCKED;
+    c->stats.lock_ns = ns_since(t0);
+    return GCR_OK;
+}
+
+gcr_status gcr_unlock(gcr_ctx *c) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "unlock: not locked");
+    auto t0 = Clock::now();
+    c->phase = GCR_RUNNING;
+    c->stats.unlock_ns = ns_since(t0);
+    return GCR_OK;
+}
+
+static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
+    const uint32_t P = c->P;
+    const int cur = c->have_parent ? 1 - c->parent_idx : 0;
+    uint32_t *Dnew = c->D[cur];
+    const uint32_t *Dref = mode == GCR_INCREMENTAL ? c->D[c->parent_idx] : nullptr;
+    gcr_stats &st = c->stats;
+    c->ev_used = 0;
+
+    uint64_t R = 0;
+    for (const RegEntry &r : c->reg) R += r.bytes;
+    img->data_cap = R;
+    img->data = static_cast<uint8_t *>(c->pool.alloc(R));
+    img->digests_cap = 4 * c->n_pages;
+    img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
+    st.pinned_alloc_ns = c->pool.pin_ns;
+    if (!img->data || !img->digests) return fail(c, GCR_E_NOMEM, "checkpoint: pinned host allocation failed");
+
+    ScanParams sp{};
+    sp.allocs = c->allocs_d;
+    sp.tile_alloc = c->tile_alloc;
+    sp.page_size = P;
+    sp.log2_page = c->lg;
+    sp.z_page = c->z_page;
+    sp.mode = mode == GCR_INCREMENTAL ? kScanIncremental : kScanFull;
+    sp.d_ref = Dref;
+    sp.d_out = Dnew;
+    sp.cls = c->cls;
+    sp.tile_info = c->tile_info;
+    sp.slice_raw = c->slice_raw;
+    sp.slice_nz = c->slice_nz;
+    sp.tables = c->tables_d;
+
+    const size_t nch = c->chunks.size();
+    std::vector<cudaEvent_t> k1s(nch), k1e(nch), tot(nch), pks(nch), pke(nch);
+    // Enqueue every chunk's scan + compaction on the compute stream up front.
+    for (size_t i = 0; i < nch; i++) {
+        const Chunk &ch = c->chunks[i];
+        sp.tile_begin = ch.tile_begin;
+        sp.tile_end = ch.tile_end;
+        k1s[i] = c->ev();
+        k1e[i] = c->ev();
+        tot[i] = c->ev();
+        CUDA_TRY(c, cudaEventRecord(k1s[i], c->compute));
+        LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
+        CUDA_TRY(c, cudaEventRecord(k1e[i], c->compute));
+        LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off, c->totals_d + i,
+                                       c->compute));
+        CUDA_TRY(c, cudaMemcpyAsync(c->totals_h + i, c->totals_d + i, sizeof(ChunkTotals), cudaMemcpyDeviceToHost,
+                                    c->compute));
+        CUDA_TRY(c, cudaEventRecord(tot[i], c->compute));
+    }
+    // Drain: as each chunk's totals land, pack it into its slot and copy out.
+    uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0;
+    Clock::time_point drain0;
+    const size_t S = c->copy.size();
+    for (size_t i = 0; i < nch; i++) {
+        const Chunk &ch = c->chunks[i];
+        CUDA_TRY(c, cudaEventSynchronize(tot[i]));
+        const ChunkTotals T = c->totals_h[i];
+        n_present += T.n_present;
+        n_zero += T.n_zero;
+        n_parent += T.n_parent;
+        cudaStream_t cs = c->copy[i % S];
+        if (i == 0) drain0 = Clock::now();
+        CUDA_TRY(c, cudaStreamWaitEvent(cs, tot[i], 0));
+        pks[i] = c->ev();
+        pke[i] = c->ev();
+        CUDA_TRY(c, cudaEventRecord(pks[i], cs));
+        if (T.image_bytes) {
+            LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, c->tile_off, ch.tile_begin, ch.tile_end, P,
+                                      c->lg, c->slots[i % S], c->n_sms, cs));
+        }
+        CUDA_TRY(c, cudaEventRecord(pke[i], cs));
+        if (base + T.image_bytes > R) return fail(c, GCR_E_CUDA, "checkpoint: image larger than registry");
+        if (T.image_bytes)
+            CUDA_TRY(c, cudaMemcpyAsync(img->data + base, c->slots[i % S], T.image_bytes, cudaMemcpyDeviceToHost, cs));
+        if (ch.page_end > ch.page_begin)
+            CUDA_TRY(c, cudaMemcpyAsync(img->digests + ch.page_begin, Dnew + ch.page_begin,
+                                        4 * (ch.page_end - ch.page_begin), cudaMemcpyDeviceToHost, cs));
+        base += T.image_bytes;
+    }
+    // K3 pagemap over all pages (maximal runs, independent of chunking).
+    auto pm0 = c->ev(), pm1 = c->ev();
+    CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
+    LAUNCH_TRY(c, launch_pagemap_count(c->cls, c->n_pages, c->pm_blk_cnt, c->pm_blk_off, c->misc_d, c->compute));
+    CUDA_TRY(c, cudaMemcpyAsync(c->misc_h, c->misc_d, 8, cudaMemcpyDeviceToHost, c->compute));
+    CUDA_TRY(c, cudaStreamSynchronize(c->compute));
+    const uint64_t ne = c->misc_h[0];
+    img->pagemap_cap = sizeof(gcr_pagemap_entry) * ne;
+    img->pagemap = static_cast<gcr_pagemap_entry *>(c->pool.alloc(img->pagemap_cap));
+    if (!img->pagemap) return fail(c, GCR_E_NOMEM, "checkpoint: pinned pagemap allocation failed");
+    LAUNCH_TRY(c, launch_pagemap_write(c->allocs_d, c->page_alloc, c->cls, c->n_pages, c->lg, c->pm_blk_off,
+                                       c->run_start, ne, c->entries_d, c->compute));
+    CUDA_TRY(c, cudaEventRecord(pm1, c->compute));
+    if (ne) CUDA_TRY(c, cudaMemcpyAsync(img->pagemap, c->entries_d, img->pagemap_cap, cudaMemcpyDeviceToHost, c->compute));
+    for (size_t s = 0; s < S; s++) {
+        cudaEvent_t e = c->ev();
+        CUDA_TRY(c, cudaEventRecord(e, c->copy[s]));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->compute));
+    st.drain_ns = ns_since(drain0);
+
+    // stats from the events
+    float ms;
+    st.scan_dev_ns = 0;
+    st.pack_dev_ns = 0;
+    for (size_t i = 0; i < nch; i++) {
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s[i], k1e[i]));
+        st.scan_dev_ns += (uint64_t)(ms * 1e6);
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, pks[i], pke[i]));
+        st.pack_dev_ns += (uint64_t)(ms * 1e6);
+    }
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, pm0, pm1));
+    st.compact_dev_ns = (uint64_t)(ms * 1e6);
+    st.scan_launches = nch;
+    st.scan_bytes = R;
+    st.pages_scanned = c->n_pages;
+    st.pages_zero = n_zero;
+    st.pages_parent = n_parent;
+    st.pages_written = n_present;
+    st.image_bytes = base;
+    st.n_entries = ne;
+
+    // image model
+    c->pool.shrink(img->data, img->data_cap, base);
+    img->data_cap = base;
+    gcr_image_hdr &h = img->hdr;
+    std::memcpy(h.magic, kMagic, 8);
+    h.version = 1;
+    h.page_size = P;
+    h.generation = c->next_gen;
+    h.parent_generation = mode == GCR_INCREMENTAL ? c->parent_gen : 0;
+    h.n_allocs = (uint32_t)c->reg.size();
+    h.flags = mode == GCR_INCREMENTAL ? 1u : 0u;
+    h.n_pages = c->n_pages;
+    h.n_present = n_present;
+    h.n_zero = n_zero;
+    h.n_parent = n_parent;
+    h.n_entries = ne;
+    h.image_bytes = base;
+    h.reserved = 0;
+    img->allocs.clear();
+    for (const RegEntry &r : c->reg) img->allocs.push_back(gcr_alloc_rec{r.dptr, r.bytes, r.id, 0});
+    h.meta_crc32c = meta_crc(img);
+    if (n_present + n_zero + n_parent != c->n_pages)
+        return fail(c, GCR_E_CUDA, "checkpoint: class counts do not cover every page");
+    c->next_gen++;
+    c->parent_idx = cur;
+    c->parent_gen = h.generation;
+    c->have_parent = true;
+    return GCR_OK;
+}
+
+gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
+    if (!c) return GCR_E_INVAL;
+    if (!out) return fail(c, GCR_E_INVAL, "checkpoint: out is NULL");
+    *out = nullptr;
+    if (c->phase != GCR_LOCKED) return fail(c, GCR_E_STATE, "checkpoint: not LOCKED");
+    if (mode != GCR_FULL && mode != GCR_INCREMENTAL) return fail(c, GCR_E_INVAL, "checkpoint: bad mode");
+    if (c->reg.empty()) return fail(c, GCR_E_INVAL, "checkpoint: no registered allocation");
+    if (mode == GCR_INCREMENTAL && !c->have_parent)
+        return fail(c, GCR_E_CHAIN, "checkpoint: INCREMENTAL without a parent digest state (R-8)");
+    auto t0 = Clock::now();
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    gcr_status s = build_layout(c);
+    if (s != GCR_OK) return s;
+    gcr_image *img = new (std::nothrow) gcr_image;
+    if (!img) return fail(c, GCR_E_NOMEM, "checkpoint: out of host memory");
+    img->ctx = c;
+    const bool had_parent = c->have_parent;
+    const int pidx = c->parent_idx;
+    const uint64_t pgen = c->parent_gen;
+    s = checkpoint_impl(c, mode, img);
+    if (s != GCR_OK) {
+        sync_all(c);
+        image_free_buffers(img);
+        delete img;
+        c->have_parent = had_parent;  // failure atomicity
+        c->parent_idx = pidx;
+        c->parent_gen = pgen;
+        return s;
+    }
+    c->images.push_back(img);
+    c->phase = GCR_CHECKPOINTED;
+    c->stats.checkpoint_ns = ns_since(t0);
+    *out = img;
+    return GCR_OK;
+}
+
+static gcr_status ensure_desc(gcr_ctx *c, uint64_t bytes) {
+    if (bytes <= c->desc_cap) return GCR_OK;
+    uint64_t cap = std::max<uint64_t>(bytes, 1ull << 20);
+    if (c->desc_d) cudaFree(c->desc_d);
+    if (c->desc_h) cudaFreeHost(c->desc_h);
+    c->desc_d = nullptr;
+    c->desc_h = nullptr;
+    c->desc_cap = 0;
+    CUDA_TRY(c, cudaMalloc(&c->desc_d, cap));
+    CUDA_TRY(c, cudaHostAlloc(&c->desc_h, cap, cudaHostAllocDefault));
+    c->desc_cap = cap;
+    return GCR_OK;
+}
+
+gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "restore: not locked");
+    if (!chain || n == 0) return fail(c, GCR_E_INVAL, "restore: empty chain");
+    for (uint32_t k = 0; k < n; k++)
+        if (!chain[k] || chain[k]->ctx != c) return fail(c, GCR_E_INVAL, "restore: image of another ctx or NULL");
+    auto t0 = Clock::now();
+    gcr_stats &st = c->stats;
+    // ---- validation, in order: meta CRC, version, layout, chain (c.2 step 1)
+    for (uint32_t k = 0; k < n; k++) {
+        const gcr_image *im = chain[k];
+        if (std::memcmp(im->hdr.magic, kMagic, 8) != 0 || meta_crc(im) != im->hdr.meta_crc32c)
+            return fail(c, GCR_E_CORRUPT, "restore: meta_crc32c mismatch");
+        if (im->hdr.version != 1) return fail(c, GCR_E_VERSION, "restore: unknown image version");
+        gcr_status s = check_pagemap(c, im);
+        if (s != GCR_OK) return s;
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        const gcr_image *im = chain[k];
+        if (im->hdr.page_size != c->cfg.page_size || im->hdr.n_allocs != c->reg.size())
+            return fail(c, GCR_E_LAYOUT, "restore: page size or allocation count differs from the registry");
+        for (uint32_t a = 0; a < im->hdr.n_allocs; a++)
+            if (im->allocs[a].bytes != c->reg[a].bytes)
+                return fail(c, GCR_E_LAYOUT, "restore: allocation sizes differ from the registry");
+    }
+    for (uint32_t k = 0; k < n; k++) {
+        const gcr_image_hdr &h = chain[k]->hdr;
+        if (k == 0 && ((h.flags & 1u) || h.parent_generation != 0 || h.n_parent != 0))
+            return fail(c, GCR_E_CHAIN, "restore: chain must start with a full image");
+        if (k > 0 && (!(h.flags & 1u) || h.parent_generation != chain[k - 1]->hdr.generation))
+            return fail(c, GCR_E_CHAIN, "restore: parent_generation link broken");
+    }
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    gcr_status s = build_layout(c);
+    if (s != GCR_OK) return s;
+    c->ev_used = 0;
+    const uint32_t P = c->P;
+    const uint64_t slot = c->cfg.chunk_bytes;
+    const size_t S = c->copy.size();
+
+    // ---- descriptors for every image (host walk of the pagemaps) ----------
+    struct ImgPlan {
+        uint64_t sc_begin, sc_end, z_begin, z_end;
+        std::vector<uint64_t> chunk_desc;  // scatter desc index where chunk j starts (size nchunks+1)
+    };
+    std::vector<ImgPlan> plans(n);
+    std::vector<ScatterDesc> sdesc;
+    std::vector<ZeroDesc> zdesc;
+    uint64_t h2d_bytes = 0;
+    for (uint32_t k = 0; k < n; k++) {
+        const gcr_image *im = chain[k];
+        ImgPlan &pl = plans[k];
+        pl.sc_begin = sdesc.size();
+        pl.z_begin = zdesc.size();
+        const uint64_t nchunks = (im->hdr.image_bytes + slot - 1) / slot;
+        pl.chunk_desc.assign(nchunks + 1, 0);
+        uint64_t cursor = 0, e = 0, next_chunk = 0;
+        for (uint32_t a = 0; a < im->hdr.n_allocs; a++) {
+            const uint64_t m = pages_of(c->reg[a].bytes, P);
+            uint64_t p = 0;
+            while (p < m) {
+                const gcr_pagemap_entry &pe = im->pagemap[e++];
+                const uint64_t last = p + pe.nr_pages;
+                uint64_t bytes = (last == m) ? (uint64_t)(pe.nr_pages - 1) * P + page_len(c->reg[a].bytes, P, m - 1)
+                                             : (uint64_t)pe.nr_pages * P;
+                uint64_t dst = c->reg[a].dptr + p * P;  // remapped by allocation index (R-14)
+                if (pe.flags == GCR_PE_PRESENT) {
+                    while (bytes) {
+                        const uint64_t j = cursor / slot;
+                        while (next_chunk <= j) pl.chunk_desc[next_chunk++] = sdesc.size();
+                        const uint64_t room = (j + 1) * slot - cursor;
+                        const uint64_t piece = std::min(std::min(bytes, room), kPieceBytes);
+                        sdesc.push_back(ScatterDesc{dst, cursor - j * slot, piece});
+                        dst += piece;
+                        cursor += piece;
+                        bytes -= piece;
+                    }
+                } else if (pe.flags == GCR_PE_ZERO) {
+                    while (bytes) {
+                        const uint64_t piece = std::min(bytes, kPieceBytes);
+                        zdesc.push_back(ZeroDesc{dst, piece});
+                        dst += piece;
+                        bytes -= piece;
+                    }
+                }
+                p = last;
+            }
+        }
+        while (next_chunk <= nchunks) pl.chunk_desc[next_chunk++] = sdesc.size();
+        pl.sc_end = sdesc.size();
+        pl.z_end = zdesc.size();
+        h2d_bytes += im->hdr.image_bytes;
+    }
+    const uint64_t sbytes = sizeof(ScatterDesc) * sdesc.size(), zbytes = sizeof(ZeroDesc) * zdesc.size();
+    s = ensure_desc(c, sbytes + zbytes + 16);
+    if (s != GCR_OK) return s;
+    std::memcpy(c->desc_h, sdesc.data(), sbytes);
+    std::memcpy(c->desc_h + sbytes, zdesc.data(), zbytes);
+    const ScatterDesc *sd = reinterpret_cast<const ScatterDesc *>(c->desc_d);
+    const ZeroDesc *zd = reinterpret_cast<const ZeroDesc *>(c->desc_d + sbytes);
+    CUDA_TRY(c, cudaMemcpyAsync(c->desc_d, c->desc_h, sbytes + zbytes, cudaMemcpyHostToDevice, c->compute));
+
+    // ---- apply the chain ----------------------------------------------------
+    std::vector<cudaEvent_t> sc0, sc1;
+    auto h2d0 = Clock::now();
+    for (uint32_t k = 0; k < n; k++) {
+        const gcr_image *im = chain[k];
+        const ImgPlan &pl = plans[k];
+        cudaEvent_t start = c->ev();
+        CUDA_TRY(c, cudaEventRecord(start, c->compute));
+        for (size_t i = 0; i < S; i++) CUDA_TRY(c, cudaStreamWaitEvent(c->copy[i], start, 0));
+        const uint64_t nchunks = pl.chunk_desc.size() - 1;
+        for (uint64_t j = 0; j < nchunks; j++) {
+            cudaStream_t cs = c->copy[j % S];
+            const uint64_t lo = j * slot, hi = std::min(im->hdr.image_bytes, lo + slot);
+            CUDA_TRY(c, cudaMemcpyAsync(c->slots[j % S], im->data + lo, hi - lo, cudaMemcpyHostToDevice, cs));
+            cudaEvent_t a = c->ev(), b = c->ev();
+            CUDA_TRY(c, cudaEventRecord(a, cs));
+            LAUNCH_TRY(c, launch_scatter(sd + pl.chunk_desc[j], pl.chunk_desc[j + 1] - pl.chunk_desc[j],
+                                         c->slots[j % S], c->n_sms, cs));
+            CUDA_TRY(c, cudaEventRecord(b, cs));
+            sc0.push_back(a);
+            sc1.push_back(b);
+        }
+        if (pl.z_end > pl.z_begin) {
+            cudaEvent_t a = c->ev(), b = c->ev();
+            CUDA_TRY(c, cudaEventRecord(a, c->copy[0]));
+            LAUNCH_TRY(c, launch_zero_fill(zd + pl.z_begin, pl.z_end - pl.z_begin, c->n_sms, c->copy[0]));
+            CUDA_TRY(c, cudaEventRecord(b, c->copy[0]));
+            sc0.push_back(a);
+            sc1.push_back(b);
+        }
+        for (size_t i = 0; i < S; i++) {
+            cudaEvent_t e = c->ev();
+            CUDA_TRY(c, cudaEventRecord(e, c->copy[i]));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
+        }
+    }
+    // ---- verify: recompute every digest and compare with D_k (R-11) ---------
+    const gcr_image *last = chain[n - 1];
+    const int scratch = c->have_parent ? 1 - c->parent_idx : 0;
+    CUDA_TRY(c, cudaMemcpyAsync(c->D[scratch], last->digests, 4 * c->n_pages, cudaMemcpyHostToDevice, c->compute));
+    cudaEvent_t v0 = c->ev(), v1 = c->ev();
+    uint64_t verify_launches = 0;
+    if (c->cfg.verify) {
+        CUDA_TRY(c, cudaMemsetAsync(c->misc_d + 1, 0, 8, c->compute));
+        CUDA_TRY(c, cudaMemsetAsync(c->misc_d + 2, 0xFF, 8, c->compute));
+        ScanParams sp{};
+        sp.allocs = c->allocs_d;
+        sp.tile_alloc = c->tile_alloc;
+        sp.tile_begin = 0;
+        sp.tile_end = c->n_tiles;
+        sp.page_size = P;
+        sp.log2_page = c->lg;
+        sp.z_page = c->z_page;
+        sp.mode = kScanVerify;
+        sp.d_ref = c->D[scratch];
+        sp.slice_raw = c->slice_raw;
+        sp.slice_nz = c->slice_nz;
+        sp.verify_count = c->misc_d + 1;
+        sp.first_bad = c->misc_d + 2;
+        sp.tables = c->tables_d;
+        CUDA_TRY(c, cudaEventRecord(v0, c->compute));
+        LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
+        CUDA_TRY(c, cudaEventRecord(v1, c->compute));
+        CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));
+        verify_launches = 1;
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(c->compute));
+    st.restore_h2d_ns = ns_since(h2d0);
+    float ms;
+    st.scatter_dev_ns = 0;
+    for (size_t i = 0; i < sc0.size(); i++) {
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, sc0[i], sc1[i]));
+        st.scatter_dev_ns += (uint64_t)(ms * 1e6);
+    }
+    st.verify_dev_ns = 0;
+    st.verify_failures = 0;
+    st.first_bad_page = UINT64_MAX;
+    if (c->cfg.verify) {
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, v0, v1));
+        st.verify_dev_ns = (uint64_t)(ms * 1e6);
+        st.verify_failures = c->misc_h[1];
+        st.first_bad_page = c->misc_h[2];
+    }
+    st.verify_launches = verify_launches;
+    st.restore_h2d_bytes = h2d_bytes;
+    c->phase = GCR_LOCKED;
+    st.restore_ns = ns_since(t0);
+    if (st.verify_failures) {
+        c->have_parent = false;
+        return fail(c, GCR_E_VERIFY, "restore: " + std::to_string(st.verify_failures) + " page digest(s) differ");
+    }
+    // the next incremental diffs against the restored state (c.2 step 4)
+    c->parent_idx = scratch;
+    c->parent_gen = last->hdr.generation;
+    c->have_parent = true;
+    c->next_gen = std::max(c->next_gen, last->hdr.generation + 1);
+    return GCR_OK;
+}
+
+gcr_status gcr_get_phase(const gcr_ctx *c, gcr_phase *out) {
+    if (!c || !out) return GCR_E_INVAL;
+    *out = c->phase;
+    return GCR_OK;
+}
+
+gcr_status gcr_get_stats(const gcr_ctx *c, gcr_stats *out) {
+    if (!c || !out) return GCR_E_INVAL;
+    *out = c->stats;
+    return GCR_OK;
+}
+
+gcr_status gcr_ctx_stream(const gcr_ctx *c, void **out) {
+    if (!c || !out) return GCR_E_INVAL;
+    *out = c->compute;
+    return GCR_OK;
+}
+
+const char *gcr_last_error(const gcr_ctx *c) { return c ? c->err.c_str() : "null ctx"; }
+
+gcr_status gcr_image_header(const gcr_image *img, gcr_image_hdr *out) {
+    if (!img || !out) return GCR_E_INVAL;
+    *out = img->hdr;
+    return GCR_OK;
+}
+
+gcr_status gcr_image_allocs(const gcr_image *img, const gcr_alloc_rec **p, uint32_t *n) {
+    if (!img || !p || !n) return GCR_E_INVAL;
+    *p = img->allocs.data();
+    *n = (uint32_t)img->allocs.size();
+    return GCR_OK;
+}
+
+gcr_status gcr_image_pagemap(const gcr_image *img, const gcr_pagemap_entry **p, uint64_t *n) {
+    if (!img || !p || !n) return GCR_E_INVAL;
+    *p = img->pagemap;
+    *n = img->hdr.n_entries;
+    return GCR_OK;
+}
+
+gcr_status gcr_image_digests(const gcr_image *img, const uint32_t **p, uint64_t *n) {
+    if (!img || !p || !n) return GCR_E_INVAL;
+    *p = img->digests;
+    *n = img->hdr.n_pages;
+    return GCR_OK;
+}
+
+gcr_status gcr_image_data(const gcr_image *img, const uint8_t **p, uint64_t *bytes) {
+    if (!img || !p || !bytes) return GCR_E_INVAL;
+    *p = img->data;
+    *bytes = img->hdr.image_bytes;
+    return GCR_OK;
+}
+
+gcr_status gcr_image_free(gcr_image *img) {
+    if (!img || !img->ctx) return GCR_E_INVAL;
+    gcr_ctx *c = img->ctx;
+    cudaSetDevice(c->device);
+    sync_all(c);
+    destroy_image(c, img);
+    return GCR_OK;
+}
+
+gcr_status gcr_image_stream_size(const gcr_image *img, uint64_t *bytes) {
+    if (!img || !bytes) return GCR_E_INVAL;
+    const gcr_image_hdr &h = img->hdr;
+    *bytes = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages + h.image_bytes;
+    return GCR_OK;
+}
+
+gcr_status gcr_image_serialize(const gcr_image *img, void *dst, uint64_t cap) {
+    uint64_t need;
+    if (!dst || gcr_image_stream_size(img, &need) != GCR_OK || cap < need) return GCR_E_INVAL;
+    const gcr_image_hdr &h = img->hdr;
+    uint8_t *o = static_cast<uint8_t *>(dst);
+    std::memcpy(o, &h, 96);
+    o += 96;
+    std::memcpy(o, img->allocs.data(), 24ull * h.n_allocs);
+    o += 24ull * h.n_allocs;
+    if (h.n_entries) std::memcpy(o, img->pagemap, 16ull * h.n_entries);
+    o += 16ull * h.n_entries;
+    std::memcpy(o, img->digests, 4ull * h.n_pages);
+    o += 4ull * h.n_pages;
+    if (h.image_bytes) std::memcpy(o, img->data, h.image_bytes);
+    return GCR_OK;
+}
+
+gcr_status gcr_image_import(gcr_ctx *c, const void *stream, uint64_t bytes, gcr_image **out) {
+    if (!c) return GCR_E_INVAL;
+    if (!stream || !out) return fail(c, GCR_E_INVAL, "import: null argument");
+    *out = nullptr;
+    const uint8_t *s = static_cast<const uint8_t *>(stream);
+    if (bytes < 96) return fail(c, GCR_E_CORRUPT, "import: shorter than a header");
+    gcr_image_hdr h;
+    std::memcpy(&h, s, 96);
+    if (std::memcmp(h.magic, kMagic, 8) != 0) return fail(c, GCR_E_CORRUPT, "import: bad magic");
+    if (h.n_pages > bytes / 4 || h.n_entries > bytes / 16 || h.n_allocs > bytes / 24)
+        return fail(c, GCR_E_CORRUPT, "import: section sizes exceed the stream");
+    const uint64_t meta = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages;
+    if (meta > bytes || bytes - meta != h.image_bytes) return fail(c, GCR_E_CORRUPT, "import: framing mismatch");
+    gcr_image_hdr h0 = h;
+    h0.meta_crc32c = 0;
+    uint32_t st = host_crc32c_update(0xFFFFFFFFu, &h0, 96);
+    st = host_crc32c_update(st, s + 96, meta - 96) ^ 0xFFFFFFFFu;
+    if (st != h.meta_crc32c) return fail(c, GCR_E_CORRUPT, "import: meta_crc32c mismatch");
+    if (h.version != 1) return fail(c, GCR_E_VERSION, "import: unknown version");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    gcr_image *img = new (std::nothrow) gcr_image;
+    if (!img) return fail(c, GCR_E_NOMEM, "import: out of host memory");
+    img->ctx = c;
+    img->hdr = h;
+    img->allocs.resize(h.n_allocs);
+    std::memcpy(img->allocs.data(), s + 96, 24ull * h.n_allocs);
+    img->pagemap_cap = 16ull * h.n_entries;
+    img->digests_cap = 4ull * h.n_pages;
+    img->data_cap = h.image_bytes;
+    img->pagemap = static_cast<gcr_pagemap_entry *>(c->pool.alloc(img->pagemap_cap));
+    img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
+    img->data = static_cast<uint8_t *>(c->pool.alloc(img->data_cap));
+    c->stats.pinned_alloc_ns = c->pool.pin_ns;
+    if (!img->pagemap || !img->digests || !img->data) {
+        image_free_buffers(img);
+        delete img;
+        return fail(c, GCR_E_NOMEM, "import: pinned allocation failed");
+    }
+    const uint8_t *o = s + 96 + 24ull * h.n_allocs;
+    std::memcpy(img->pagemap, o, 16ull * h.n_entries);
+    o += 16ull * h.n_entries;
+    std::memcpy(img->digests, o, 4ull * h.n_pages);
+    o += 4ull * h.n_pages;
+    std::memcpy(img->data, o, h.image_bytes);
+    c->images.push_back(img);
+    *out = img;
+    return GCR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// gcr_internal.h -- internal types shared by the libgcr host runtime
+// (gcr.cpp, crc_host.cpp, pinned_pool.cpp) and the sm_100a kernels
+// (kernels.cu).  Not part of the C-ABI (include/gcr.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gcr {
+
+// ---------------------------------------------------------------------------
+// Work geometry.  A TILE is 64 KiB of virtual page space
+// scanned by one warp; a warp is 4 lane GROUPS of 8 lanes; a group owns a
+// 16 KiB SEGMENT of the tile and streams it as 128-byte rows (8 lanes x 16 B).
+constexpr uint32_t kTileBytes = 65536;
+constexpr uint32_t kGroupBytes = 16384;
+constexpr uint32_t kRowBytes = 128;
+constexpr uint32_t kLog2Tile = 16;
+
+// Page classes (c.1 step 5).  cls[] bytes also carry kClsAllocStart on the
+// first page of each allocation (runs never cross allocations, c.1 step 7).
+constexpr uint8_t kClsPresent = 0, kClsZero = 1, kClsParent = 2;
+constexpr uint8_t kClsAllocStart = 0x80;
+
+enum ScanMode : int { kScanFull = 0, kScanIncremental = 1, kScanVerify = 2 };
+
+// Per-allocation descriptor in device memory (A1 page table).
+struct AllocDev {
+    uint64_t base;      // device address of the allocation
+    uint64_t bytes;     // registered length (multiple of 16)
+    uint64_t page0;     // global index of its first page
+    uint64_t tile0;     // global index of its first tile
+    uint32_t n_pages;
+    uint32_t n_tiles;
+    uint32_t tail_len;  // length of its last page (== page_size if none is short)
+    uint32_t z_tail;    // Z(tail_len) = CRC32C of tail_len zero bytes
+};
+
+// Per-tile result of the scan used by compaction (K2) and pack (K4).
+struct TileInfo {
+    uint32_t present_bytes;  // PRESENT bytes whose image offset is anchored at this tile
+    uint32_t counts;         // n_present | n_zero << 10 | n_parent << 20 (pages anchored here)
+};
+
+struct ChunkTotals {
+    unsigned long long image_bytes;
+    unsigned long long n_present, n_zero, n_parent;
+};
+
+// CRC32C tables in device global memory; kernels stage them in shared memory.
+// Every table maps a 32-bit register v to adv_d(v) = v * x^(8d) mod P as the
+// XOR of 4 byte-indexed entries: tab[k][e] = adv_d(e << 8k).
+struct CrcTables {
+    uint32_t braid[4][256];  // d = 128 (one row of 8 lanes x 16 B)
+    uint32_t t4[4][256];     // d = 4   (word step for the lane raw16)
+    uint32_t a16[4][256];    // d = 16  (lane tree, level 0)
+    uint32_t a32[4][256];    // d = 32  (level 1)
+    uint32_t a64[4][256];    // d = 64  (level 2)
+    uint32_t a16k[4][256];   // d = 16 KiB (group combine, level 0)
+    uint32_t a32k[4][256];   // d = 32 KiB (group combine, level 1)
+    uint32_t a64k[4][256];   // d = 64 KiB (slice fold, pages > 64 KiB)
+};
+
+struct ScanParams {
+    const AllocDev *allocs;
+    const uint32_t *tile_alloc;
+    uint64_t tile_begin, tile_end;
+    uint32_t page_size, log2_page;
+    uint32_t z_page;
+    int mode;
+    const uint32_t *d_ref;     // D_prev (incremental) or D_k (verify)
+    uint32_t *d_out;           // D_new (full / incremental)
+    uint8_t *cls;              // class per page (full / incremental)
+    TileInfo *tile_info;       // per tile (full / incremental)
+    uint32_t *slice_raw;       // per tile, pages > 64 KiB
+    uint8_t *slice_nz;         // per tile, pages > 64 KiB
+    unsigned long long *verify_count;
+    unsigned long long *first_bad;
+    const CrcTables *tables;
+};
+
+struct ScatterDesc {
+    uint64_t dst;      // device address
+    uint64_t src_off;  // offset in the staging slot
+    uint64_t bytes;    // multiple of 16
+};
+
+struct ZeroDesc {
+    uint64_t dst;
+    uint64_t bytes;
+};
+
+// ---- kernel launchers (kernels.cu); all asynchronous on `st` -------------
+// Each returns the number of kernels it launched (for stats) or -1 on a
+// launch error (cudaGetLastError holds it).
+int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t *page_alloc,
+                            uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
+                            cudaStream_t st);
+int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);
+int launch_tile_scan(const TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end,
+                     uint32_t *tile_off, ChunkTotals *totals, cudaStream_t st);
+int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
+                const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
+                uint32_t page_size, uint32_t log2_page, uint8_t *slot, int n_sms, cudaStream_t st);
+// Pagemap over all pages: phase 1 counts run starts per block and scans them,
+// writing the entry count to *n_entries_dev; phase 2 writes the entries.
+int launch_pagemap_count(const uint8_t *cls, uint64_t n_pages, uint32_t *blk_cnt, uint32_t *blk_off,
+                         unsigned long long *n_entries_dev, cudaStream_t st);
+int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls,
+                         uint64_t n_pages, uint32_t log2_page, const uint32_t *blk_off,
+                         uint32_t *run_start, uint64_t n_entries, void *entries_dev, cudaStream_t st);
+int launch_scatter(const ScatterDesc *desc, uint64_t n_desc, const uint8_t *slot, int n_sms,
+                   cudaStream_t st);
+int launch_zero_fill(const ZeroDesc *desc, uint64_t n_desc, int n_sms, cudaStream_t st);
+size_t scan_smem_bytes();
+
+// ---- host CRC32C math (crc_host.cpp), independent of oracle/ --------------
+void build_tables(CrcTables *out);
+uint32_t zero_digest(uint64_t n);                 // Z(n)
+uint32_t host_crc32c_update(uint32_t state, const void *p, uint64_t n);  // raw register update
+bool crc_self_test();                            // "123456789" -> 0xE3069283 through the tables
+
+}  // namespace gcr
