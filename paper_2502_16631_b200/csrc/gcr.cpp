@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -169,6 +170,7 @@ struct gcr_ctx {
     std::vector<cudaStream_t> watched;
 
     cudaStream_t compute = nullptr;
+    cudaStream_t post = nullptr;  // K2 compaction + totals, off the scan's critical path
     std::vector<cudaStream_t> copy;
     std::vector<uint8_t *> slots;
     CrcTables *tables_d = nullptr;
@@ -191,8 +193,10 @@ struct gcr_ctx {
     uint8_t *slice_nz = nullptr;
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
-    ChunkTotals *totals_d = nullptr, *totals_h = nullptr;
+    ChunkTotals *totals_d = nullptr, *totals_h = nullptr, *totals_map = nullptr;  // totals_h: mapped pinned
+    unsigned *done_d = nullptr;                               // per-chunk CTA tickets
     unsigned long long *misc_d = nullptr, *misc_h = nullptr;  // [0] n_entries, [1] verify count, [2] first bad
+    unsigned long long *nent_h = nullptr, *nent_map = nullptr;  // mapped pinned n_entries
     uint32_t z_page = 0;
 
     // restore descriptor buffers (grow on demand)
@@ -255,11 +259,15 @@ bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P
 void free_layout(gcr_ctx *c) {
     void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
                     c->tile_off, c->slice_raw, c->slice_nz, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
-                    c->entries_d, c->totals_d, c->misc_d};
+                    c->entries_d, c->totals_d, c->misc_d, c->done_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->totals_h) cudaFreeHost(c->totals_h);
     if (c->misc_h) cudaFreeHost(c->misc_h);
+    if (c->nent_h) cudaFreeHost(c->nent_h);
+    c->nent_h = c->nent_map = nullptr;
+    c->done_d = nullptr;
+    c->totals_map = nullptr;
     c->allocs_d = nullptr;
     c->page_alloc = c->tile_alloc = c->D[0] = c->D[1] = nullptr;
     c->cls = nullptr;
@@ -343,7 +351,12 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
     CUDA_TRY(c, cudaMalloc(&c->entries_d, sizeof(gcr_pagemap_entry) * g));
     CUDA_TRY(c, cudaMalloc(&c->totals_d, sizeof(ChunkTotals) * nch));
-    CUDA_TRY(c, cudaHostAlloc(&c->totals_h, sizeof(ChunkTotals) * nch, cudaHostAllocDefault));
+    CUDA_TRY(c, cudaHostAlloc(&c->totals_h, sizeof(ChunkTotals) * nch, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->totals_map), c->totals_h, 0));
+    CUDA_TRY(c, cudaMalloc(&c->done_d, sizeof(unsigned) * nch));
+    CUDA_TRY(c, cudaMemset(c->done_d, 0, sizeof(unsigned) * nch));
+    CUDA_TRY(c, cudaHostAlloc(&c->nent_h, 64, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->nent_map), c->nent_h, 0));
     CUDA_TRY(c, cudaMalloc(&c->misc_d, 8 * 4));
     CUDA_TRY(c, cudaHostAlloc(&c->misc_h, 8 * 4, cudaHostAllocDefault));
     CUDA_TRY(c, cudaMemcpyAsync(c->allocs_d, c->allocs_h.data(), sizeof(AllocDev) * na, cudaMemcpyHostToDevice,
@@ -359,6 +372,7 @@ gcr_status build_layout(gcr_ctx *c) {
 
 void sync_all(gcr_ctx *c) {
     cudaStreamSynchronize(c->compute);
+    if (c->post) cudaStreamSynchronize(c->post);
     for (cudaStream_t s : c->copy) cudaStreamSynchronize(s);
     cudaGetLastError();
 }
@@ -480,6 +494,7 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     if (cudaSetDevice(cuda_device) != cudaSuccess) return bail(GCR_E_CUDA);
     cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
+    if (cudaStreamCreateWithFlags(&c->post, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     for (uint32_t i = 0; i < cfg.n_copy_streams; i++) {
         cudaStream_t s;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
@@ -513,6 +528,7 @@ gcr_status gcr_destroy(gcr_ctx *c) {
     for (uint8_t *s : c->slots) cudaFree(s);
     for (cudaStream_t s : c->copy) cudaStreamDestroy(s);
     if (c->compute) cudaStreamDestroy(c->compute);
+    if (c->post) cudaStreamDestroy(c->post);
     if (c->tables_d) cudaFree(c->tables_d);
     if (c->desc_d) cudaFree(c->desc_d);
     if (c->desc_h) cudaFreeHost(c->desc_h);
@@ -659,25 +675,30 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.slice_raw = c->slice_raw;
     sp.slice_nz = c->slice_nz;
     sp.tables = c->tables_d;
+    sp.done = c->done_d;
+    sp.tile_off = c->tile_off;
 
     const size_t nch = c->chunks.size();
-    std::vector<cudaEvent_t> k1s(nch), k1e(nch), tot(nch), pks(nch), pke(nch);
+    std::vector<cudaEvent_t> k1s(nch), k1e(nch), tot(nch), pks(nch), pke(nch), dde(nch);
+    static const bool trace = std::getenv("GCR_TRACE") != nullptr;
+    cudaEvent_t t0 = c->ev();
+    CUDA_TRY(c, cudaEventRecord(t0, c->compute));
     // Enqueue every chunk's scan + compaction on the compute stream up front.
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         sp.tile_begin = ch.tile_begin;
         sp.tile_end = ch.tile_end;
+        sp.chunk_idx = (uint32_t)i;
+        sp.totals_dev = c->totals_d + i;
+        sp.totals_host = c->totals_map + i;
         k1s[i] = c->ev();
         k1e[i] = c->ev();
-        tot[i] = c->ev();
         CUDA_TRY(c, cudaEventRecord(k1s[i], c->compute));
+        // K1 (+K1b) -- its last CTA runs the chunk compaction K2 and stores the
+        // totals into mapped pinned memory: no DMA on the drain's copy engines.
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
         CUDA_TRY(c, cudaEventRecord(k1e[i], c->compute));
-        LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off, c->totals_d + i,
-                                       c->compute));
-        CUDA_TRY(c, cudaMemcpyAsync(c->totals_h + i, c->totals_d + i, sizeof(ChunkTotals), cudaMemcpyDeviceToHost,
-                                    c->compute));
-        CUDA_TRY(c, cudaEventRecord(tot[i], c->compute));
+        tot[i] = k1e[i];
     }
     // Drain: as each chunk's totals land, pack it into its slot and copy out.
     uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0;
@@ -686,7 +707,11 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         CUDA_TRY(c, cudaEventSynchronize(tot[i]));
-        const ChunkTotals T = c->totals_h[i];
+        ChunkTotals T;
+        {
+            const volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(c->totals_h + i);
+            T = ChunkTotals{h[0], h[1], h[2], h[3]};
+        }
         n_present += T.n_present;
         n_zero += T.n_zero;
         n_parent += T.n_parent;
@@ -707,15 +732,18 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         if (ch.page_end > ch.page_begin)
             CUDA_TRY(c, cudaMemcpyAsync(img->digests + ch.page_begin, Dnew + ch.page_begin,
                                         4 * (ch.page_end - ch.page_begin), cudaMemcpyDeviceToHost, cs));
+        dde[i] = c->ev();
+        CUDA_TRY(c, cudaEventRecord(dde[i], cs));
         base += T.image_bytes;
     }
     // K3 pagemap over all pages (maximal runs, independent of chunking).
     auto pm0 = c->ev(), pm1 = c->ev();
     CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
-    LAUNCH_TRY(c, launch_pagemap_count(c->cls, c->n_pages, c->pm_blk_cnt, c->pm_blk_off, c->misc_d, c->compute));
-    CUDA_TRY(c, cudaMemcpyAsync(c->misc_h, c->misc_d, 8, cudaMemcpyDeviceToHost, c->compute));
-    CUDA_TRY(c, cudaStreamSynchronize(c->compute));
-    const uint64_t ne = c->misc_h[0];
+    LAUNCH_TRY(c, launch_pagemap_count(c->cls, c->n_pages, c->pm_blk_cnt, c->pm_blk_off, c->nent_map, c->compute));
+    cudaEvent_t pmc = c->ev();
+    CUDA_TRY(c, cudaEventRecord(pmc, c->compute));
+    CUDA_TRY(c, cudaEventSynchronize(pmc));
+    const uint64_t ne = *reinterpret_cast<volatile unsigned long long *>(c->nent_h);
     img->pagemap_cap = sizeof(gcr_pagemap_entry) * ne;
     img->pagemap = static_cast<gcr_pagemap_entry *>(c->pool.alloc(img->pagemap_cap));
     if (!img->pagemap) return fail(c, GCR_E_NOMEM, "checkpoint: pinned pagemap allocation failed");
@@ -743,6 +771,19 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     }
     CUDA_TRY(c, cudaEventElapsedTime(&ms, pm0, pm1));
     st.compact_dev_ns = (uint64_t)(ms * 1e6);
+    if (trace) {  // GCR_TRACE=1: per-chunk timeline (ms from the checkpoint's first event) on stderr
+        auto rel = [&](cudaEvent_t e) {
+            float m = 0;
+            cudaEventElapsedTime(&m, t0, e);
+            return m;
+        };
+        std::fprintf(stderr, "{\"gcr_trace\": \"checkpoint\", \"chunks\": [");
+        for (size_t i = 0; i < nch; i++)
+            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k1s[i]), rel(k1e[i]),
+                         rel(tot[i]), rel(pks[i]), rel(pke[i]), rel(dde[i]));
+        std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": \"k1_start k1_end totals pack_start pack_end d2h_end\"}\n",
+                     rel(pm0), rel(pm1));
+    }
     st.scan_launches = nch;
     st.scan_bytes = R;
     st.pages_scanned = c->n_pages;

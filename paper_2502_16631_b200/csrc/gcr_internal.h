@@ -76,6 +76,12 @@ struct ScanParams {
     unsigned long long *verify_count;
     unsigned long long *first_bad;
     const CrcTables *tables;
+    // chunk compaction by the last CTA (full / incremental)
+    unsigned *done;              // per-chunk CTA tickets, zero between launches
+    uint32_t chunk_idx;
+    uint32_t *tile_off;
+    ChunkTotals *totals_dev;
+    ChunkTotals *totals_host;    // mapped pinned
 };
 
 struct ScatterDesc {
@@ -96,8 +102,6 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
                             uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
                             cudaStream_t st);
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);
-int launch_tile_scan(const TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end,
-                     uint32_t *tile_off, ChunkTotals *totals, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
                 const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, int n_sms, cudaStream_t st);

@@ -5,7 +5,7 @@
 //  K1 scan               A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
 //                        all-zero test, dirty diff, class; tile summaries
 //  K1b fold_slices       pages > 64 KiB: fold the 64 KiB slice registers
-//  K2 tile_scan          A5: chunk-local exclusive scan of PRESENT bytes
+//  K2 chunk_scan         A5: chunk-local exclusive scan of PRESENT bytes (last CTA of K1)
 //  K3 pagemap_*          A5: maximal runs -> CRIU-style pagemap entries
 //  K4 pack               A6: stream-compaction of PRESENT pages into staging
 //  K6 scatter            A8: staged image pieces -> allocation pages
@@ -39,8 +39,14 @@ namespace {
 constexpr uint32_t kBraidSmem = 4u * 256u * 32u * 4u;  // 128 KiB
 constexpr uint32_t kSmallTables = 6;                   // t4 a16 a32 a64 a16k a32k
 constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u;
-constexpr int kScanThreads = 512;
-constexpr int kScanUnroll = 8;
+#ifndef GCR_SCAN_THREADS
+#define GCR_SCAN_THREADS 640
+#endif
+constexpr int kScanThreads = GCR_SCAN_THREADS;
+#ifndef GCR_SCAN_UNROLL
+#define GCR_SCAN_UNROLL 5
+#endif
+constexpr int kScanUnroll = GCR_SCAN_UNROLL;
 
 enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3, kA16K = 4, kA32K = 5 };
 
@@ -92,34 +98,71 @@ __device__ __forceinline__ void row_step(const char *smb, uint32_t lane4, uint32
 // row 0 (gp + r*128 is its 16 bytes of row r); first_ok masks lanes of row r0
 // that lie in the virtual zero padding of a short page.
 template <int U>
-__device__ __forceinline__ void seg_stream(const char *smb, uint32_t lane4, const char *gp, int r0,
-                                           int R, bool first_ok, uint32_t (&x)[4], uint32_t &acc) {
-    const int nrows = R - r0;
-    uint4 w[U];
+__device__ __forceinline__ void load_block(uint4 (&w)[U], const char *gp, int r, bool mask_first, bool first_ok) {
+    const char *p = gp + (size_t)r * kRowBytes;
+#pragma unroll
+    for (int u = 0; u < U; u++)
+        w[u] = (u > 0 || !mask_first || first_ok) ? ldg_stream(p + u * kRowBytes) : make_uint4(0, 0, 0, 0);
+}
+
+template <int U, bool kFirst>
+__device__ __forceinline__ void proc_block(const char *smb, uint32_t lane4, uint32_t (&x)[4], uint32_t &acc,
+                                           const uint4 (&w)[U]) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
-        const bool ok = (u < nrows) && (u > 0 || first_ok);
-        w[u] = ok ? ldg_stream(gp + (size_t)(r0 + u) * kRowBytes) : make_uint4(0, 0, 0, 0);
+        if (kFirst && u == 0) {  // x = 0 before the first row: adv_128(0) ^ w == w
+            x[0] = w[0].x;
+            x[1] = w[0].y;
+            x[2] = w[0].z;
+            x[3] = w[0].w;
+            acc = w[0].x | w[0].y | w[0].z | w[0].w;
+        } else {
+            row_step(smb, lane4, x, acc, w[u]);
+        }
     }
-    x[0] = w[0].x;
-    x[1] = w[0].y;
-    x[2] = w[0].z;
-    x[3] = w[0].w;
-    acc = w[0].x | w[0].y | w[0].z | w[0].w;
-#pragma unroll
-    for (int u = 1; u < U; u++)
-        if (u < nrows) row_step(smb, lane4, x, acc, w[u]);
-    int r = r0 + U;
-    for (; r + U <= R; r += U) {
-        const char *p = gp + (size_t)r * kRowBytes;
-#pragma unroll
-        for (int u = 0; u < U; u++) w[u] = ldg_stream(p + u * kRowBytes);
-#pragma unroll
-        for (int u = 0; u < U; u++) row_step(smb, lane4, x, acc, w[u]);
+}
+
+// Rows are consumed in blocks of U with the next block's loads in flight
+// (register double buffering): the scan is bound by bytes in flight per SM.
+template <int U>
+__device__ __forceinline__ void seg_stream(const char *smb, uint32_t lane4, const char *gp, int r0,
+                                           int R, bool first_ok, uint32_t (&x)[4], uint32_t &acc) {
+    const int nblk = (R - r0) / U;
+    int r = r0;
+    bool started = false;
+    if (nblk > 0) {
+        uint4 wa[U], wb[U];
+        load_block<U>(wa, gp, r, true, first_ok);
+        if (nblk > 1) load_block<U>(wb, gp, r + U, false, true);
+        proc_block<U, true>(smb, lane4, x, acc, wa);
+        r += U;
+        int b = 1;
+        for (; b + 1 < nblk; b += 2) {
+            load_block<U>(wa, gp, r + U, false, true);
+            proc_block<U, false>(smb, lane4, x, acc, wb);
+            r += U;
+            if (b + 2 < nblk) load_block<U>(wb, gp, r + U, false, true);
+            proc_block<U, false>(smb, lane4, x, acc, wa);
+            r += U;
+        }
+        if (b < nblk) {
+            proc_block<U, false>(smb, lane4, x, acc, wb);
+            r += U;
+        }
+        started = true;
     }
-    for (; r < R; r++) {
-        const uint4 v = ldg_stream(gp + (size_t)r * kRowBytes);
-        row_step(smb, lane4, x, acc, v);
+    for (; r < R; r++) {  // rows left over by a short (padded) page
+        const bool ok = started || r > r0 || first_ok;
+        const uint4 v = ok ? ldg_stream(gp + (size_t)r * kRowBytes) : make_uint4(0, 0, 0, 0);
+        if (!started && r == r0) {
+            x[0] = v.x;
+            x[1] = v.y;
+            x[2] = v.z;
+            x[3] = v.w;
+            acc = v.x | v.y | v.z | v.w;
+        } else {
+            row_step(smb, lane4, x, acc, v);
+        }
     }
 }
 
@@ -173,22 +216,133 @@ __device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, b
     p.cls[g] = c | (alloc_start ? kClsAllocStart : 0);
 }
 
+// Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
+__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
+                                                                   unsigned long long *total) {
+    __shared__ unsigned long long warp_sums[32];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= (uint32_t)d) inc += o;
+    }
+    if (lane == 31) warp_sums[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        unsigned long long s = lane < nw ? warp_sums[lane] : 0ull;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(0xFFFFFFFFu, s, d);
+            if (lane >= (uint32_t)d) s += o;
+        }
+        if (lane < nw) warp_sums[lane] = s;  // inclusive
+    }
+    __syncthreads();
+    const unsigned long long before = warp == 0 ? 0ull : warp_sums[warp - 1];
+    const unsigned long long res = before + inc - v;
+    if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return res;
+}
+
+// K2 (run by the LAST CTA of the chunk's scan): chunk-local exclusive scan of
+// PRESENT bytes over tiles -> tile_off, and the chunk totals, stored both to
+// device memory and straight into mapped pinned host memory so the host learns
+// the chunk's image size without a DMA queued behind the drain.
+__device__ void chunk_scan(const TileInfo *ti, uint64_t tb, uint64_t te, uint32_t *tile_off,
+                           ChunkTotals *tot_dev, ChunkTotals *tot_host) {
+    const uint64_t n = te - tb;
+    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint64_t lo = tb + per * threadIdx.x;
+    const uint64_t hi = min(te, lo + per);
+    unsigned long long s = 0, np = 0, nzr = 0, npa = 0;
+    for (uint64_t t = lo; t < hi; t++) {
+        const uint2 v = __ldcg(reinterpret_cast<const uint2 *>(ti) + t);
+        const TileInfo x{v.x, v.y};
+        s += x.present_bytes;
+        np += x.counts & 1023u;
+        nzr += (x.counts >> 10) & 1023u;
+        npa += (x.counts >> 20) & 1023u;
+    }
+    unsigned long long total;
+    unsigned long long off = block_exclusive_scan(s, &total);
+    for (uint64_t t = lo; t < hi; t++) {
+        tile_off[t] = (uint32_t)off;
+        off += __ldcg(reinterpret_cast<const unsigned *>(ti) + 2 * t);
+    }
+    unsigned long long tp, tz, tpa;
+    block_exclusive_scan(np, &tp);
+    block_exclusive_scan(nzr, &tz);
+    block_exclusive_scan(npa, &tpa);
+    if (threadIdx.x == 0) {
+        const ChunkTotals T{total, tp, tz, tpa};
+        *tot_dev = T;
+        volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(tot_host);
+        h[0] = T.image_bytes;
+        h[1] = T.n_present;
+        h[2] = T.n_zero;
+        h[3] = T.n_parent;
+        __threadfence_system();
+    }
+}
+
+// Last-CTA-done: every CTA fences its tile_info writes, takes a ticket, and the
+// CTA holding the last ticket runs chunk_scan (then re-arms the counter).
+__device__ __forceinline__ void last_cta_chunk_scan(const ScanParams &p) {
+    __shared__ bool am_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) am_last = atomicAdd(p.done + p.chunk_idx, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!am_last) return;
+    __threadfence();
+    chunk_scan(p.tile_info, p.tile_begin, p.tile_end, p.tile_off, p.totals_dev, p.totals_host);
+    if (threadIdx.x == 0) p.done[p.chunk_idx] = 0u;
+}
+
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const char *smb = reinterpret_cast<const char *>(sm);
     const uint32_t *small = sm + kBraidSmem / 4;
 
-    // Stage the tables: braid lane-private (word (k>>1)*16384 + e*64 +
-    // (k&1)*32 + l), the small ones as-is.
+    // Stage the tables.  Each thread loads a few table words once (all loads
+    // issued before any store) and writes the braid words to all 32 lane-private
+    // replicas: word (k>>1)*16384 + e*64 + (k&1)*32 + l.
     {
         const uint32_t *gb = &p.tables->braid[0][0];
-        for (uint32_t i = threadIdx.x; i < 4u * 256u * 32u; i += blockDim.x) {
-            const uint32_t l = i & 31u, ke = i >> 5, k = ke >> 8, e = ke & 255u;
-            sm[(k >> 1) * 16384u + e * 64u + (k & 1u) * 32u + l] = __ldg(gb + ke);
-        }
         const uint32_t *gs = &p.tables->t4[0][0];  // t4..a32k are contiguous
+        constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
+        constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
+        uint32_t bv[kPer], sv[kPerS];
+#pragma unroll
+        for (uint32_t j = 0; j < kPer; j++) {
+            const uint32_t ke = threadIdx.x + j * kScanThreads;
+            bv[j] = ke < 1024u ? __ldg(gb + ke) : 0u;
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < kPerS; j++) {
+            const uint32_t i = threadIdx.x + j * kScanThreads;
+            sv[j] = i < kSmallTables * 1024u ? __ldg(gs + i) : 0u;
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < kPer; j++) {
+            const uint32_t ke = threadIdx.x + j * kScanThreads;
+            if (ke < 1024u) {
+                const uint32_t k = ke >> 8, e = ke & 255u;
+                uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
+                const uint4 v4 = make_uint4(bv[j], bv[j], bv[j], bv[j]);
+#pragma unroll
+                for (int l = 0; l < 8; l++) dst[l] = v4;
+            }
+        }
         uint32_t *ss = sm + kBraidSmem / 4;
-        for (uint32_t i = threadIdx.x; i < kSmallTables * 1024u; i += blockDim.x) ss[i] = __ldg(gs + i);
+#pragma unroll
+        for (uint32_t j = 0; j < kPerS; j++) {
+            const uint32_t i = threadIdx.x + j * kScanThreads;
+            if (i < kSmallTables * 1024u) ss[i] = sv[j];
+        }
     }
     __syncthreads();
 
@@ -289,6 +443,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             if (lane == 0) p.tile_info[t] = TileInfo{pb, cn};
         }
     }
+    if (p.mode != kScanVerify && P <= kTileBytes) last_cta_chunk_scan(p);
 }
 
 // K1b: pages > 64 KiB.  One thread per tile; the thread owning slice 0 of a
@@ -322,6 +477,7 @@ __global__ void __launch_bounds__(256) k_fold_slices(const ScanParams p) {
                       nz, pa);
         if (p.mode != kScanVerify) p.tile_info[t] = TileInfo{pa.present_bytes, pa.counts};
     }
+    if (p.mode != kScanVerify) last_cta_chunk_scan(p);
 }
 
 // K0: page -> allocation and tile -> allocation (A1).  One CTA per allocation.
@@ -331,65 +487,6 @@ __global__ void k_build_page_table(const AllocDev *allocs, uint32_t *page_alloc,
     const uint32_t np = allocs[a].n_pages, nt = allocs[a].n_tiles;
     for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) page_alloc[page0 + i] = a;
     for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) tile_alloc[tile0 + i] = a;
-}
-
-// Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
-__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
-                                                                   unsigned long long *total) {
-    __shared__ unsigned long long warp_sums[32];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    unsigned long long inc = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-        if (lane >= (uint32_t)d) inc += o;
-    }
-    if (lane == 31) warp_sums[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t nw = blockDim.x >> 5;
-        unsigned long long s = lane < nw ? warp_sums[lane] : 0ull;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long o = __shfl_up_sync(0xFFFFFFFFu, s, d);
-            if (lane >= (uint32_t)d) s += o;
-        }
-        if (lane < nw) warp_sums[lane] = s;  // inclusive
-    }
-    __syncthreads();
-    const unsigned long long before = warp == 0 ? 0ull : warp_sums[warp - 1];
-    const unsigned long long res = before + inc - v;
-    if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
-    __syncthreads();
-    return res;
-}
-
-// K2: chunk-local exclusive scan of PRESENT bytes over tiles; chunk totals.
-__global__ void __launch_bounds__(1024) k_tile_scan(const TileInfo *ti, uint64_t tb, uint64_t te,
-                                                    uint32_t *tile_off, ChunkTotals *tot) {
-    const uint64_t n = te - tb;
-    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = tb + per * threadIdx.x;
-    const uint64_t hi = min(te, lo + per);
-    unsigned long long s = 0, np = 0, nzr = 0, npa = 0;
-    for (uint64_t t = lo; t < hi; t++) {
-        const TileInfo x = ti[t];
-        s += x.present_bytes;
-        np += x.counts & 1023u;
-        nzr += (x.counts >> 10) & 1023u;
-        npa += (x.counts >> 20) & 1023u;
-    }
-    unsigned long long total;
-    unsigned long long off = block_exclusive_scan(s, &total);
-    for (uint64_t t = lo; t < hi; t++) {
-        tile_off[t] = (uint32_t)off;
-        off += ti[t].present_bytes;
-    }
-    unsigned long long tp, tz, tpa;
-    block_exclusive_scan(np, &tp);
-    block_exclusive_scan(nzr, &tz);
-    block_exclusive_scan(npa, &tpa);
-    if (threadIdx.x == 0) *tot = ChunkTotals{total, tp, tz, tpa};
 }
 
 // Warp-cooperative 16-byte-vector copy of `bytes` (multiple of 16).
@@ -507,7 +604,10 @@ __global__ void __launch_bounds__(1024) k_pm_scan(const uint32_t *blk_cnt, uint3
         blk_off[b] = (uint32_t)off;
         off += blk_cnt[b];
     }
-    if (threadIdx.x == 0) *n_entries = total;
+    if (threadIdx.x == 0) {
+        *reinterpret_cast<volatile unsigned long long *>(n_entries) = total;  // mapped pinned
+        __threadfence_system();
+    }
 }
 
 __global__ void __launch_bounds__(1024) k_pm_starts(const uint8_t *cls, uint64_t n, const uint32_t *blk_off,
@@ -604,12 +704,6 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
         n++;
     }
     return launched(n);
-}
-
-int launch_tile_scan(const TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off,
-                     ChunkTotals *totals, cudaStream_t st) {
-    k_tile_scan<<<1, 1024, 0, st>>>(tile_info, tb, te, tile_off, totals);
-    return launched(1);
 }
 
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, const uint32_t *tile_off,

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgcr.so")
+LIB_PATH = os.environ.get("GCR_LIBRARY") or os.path.join(PKG, "libgcr.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
