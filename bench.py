@@ -171,6 +171,7 @@ def run_ours(args):
     import torch
     world, rank, local, pg = _dist()
     torch.cuda.set_device(local)
+    from paper_2502_16631_b200 import dist as gdist
     from paper_2502_16631_b200 import gcr, synth
 
     w = synth.make_workload(args.config, rank=rank, page_size=args.page_size, gib=args.gib)
@@ -191,7 +192,12 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         h0 = time.perf_counter()
         e0.record(stream)
-        ctx.lock()
+        if pg is not None:  # globally consistent cut: all-or-nothing lock vote over gloo (dist.py)
+            st = gdist.lock_all(ctx)
+            if st != 0:
+                raise RuntimeError(f"lock vote failed: {st}")
+        else:
+            ctx.lock()
         img = ctx.checkpoint(gcr.GCR_FULL)
         s_ck = ctx.stats()
         ctx.restore([img])
