@@ -83,9 +83,7 @@ void build_tables(CrcTables *t) {
     fill_table(t->a16, 16);
     fill_table(t->a32, 32);
     fill_table(t->a64, 64);
-    fill_table(t->a16k, 16384);
-    fill_table(t->a32k, 32768);
-    fill_table(t->a64k, 65536);
+    for (int j = 0; j < 14; j++) fill_table(t->fold[j], (uint64_t)kRowBytes << j);
 }
 
 uint32_t zero_digest(uint64_t n) { return mat_vec(adv_matrix(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu; }
@@ -138,8 +136,10 @@ bool crc_self_test() {
     // braid table consistency: adv_128 == (adv_4)^32 on a probe value
     uint32_t v = 0x12345678u, w = v;
     for (int k = 0; k < 32; k++) w = apply4(t->t4, w);
+    // fold tables: adv_{128*2} through fold[1] == braid applied twice
     bool ok = a == 0xE3069283u && b == 0xE3069283u && apply4(t->braid, v) == w &&
-              zero_digest(65536) == 0x72C0C4A4u;
+              zero_digest(65536) == 0x72C0C4A4u && apply4(t->fold[0], v) == w &&
+              apply4(t->fold[1], v) == apply4(t->braid, apply4(t->braid, v));
     delete t;
     return ok;
 }

@@ -140,7 +140,7 @@ struct RegEntry {
 };
 
 struct Chunk {
-    uint64_t tile_begin, tile_end, page_begin, page_end;
+    uint64_t tile_begin, tile_end, page_begin, page_end, row_begin, row_end;
 };
 
 }  // namespace
@@ -180,7 +180,7 @@ struct gcr_ctx {
     // layout (A1), rebuilt when the registry changes
     bool layout_valid = false;
     uint32_t P = 0, lg = 0;
-    uint64_t n_pages = 0, n_tiles = 0;
+    uint64_t n_pages = 0, n_tiles = 0, n_rows = 0;
     std::vector<AllocDev> allocs_h;
     std::vector<Chunk> chunks;
     AllocDev *allocs_d = nullptr;
@@ -189,8 +189,8 @@ struct gcr_ctx {
     uint8_t *cls = nullptr;
     TileInfo *tile_info = nullptr;
     uint32_t *tile_off = nullptr;
-    uint32_t *slice_raw = nullptr;
-    uint8_t *slice_nz = nullptr;
+    Piece *pieces = nullptr;  // 2 per K1 group
+    uint32_t *contrib = nullptr;
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
     ChunkTotals *totals_d = nullptr, *totals_h = nullptr, *totals_map = nullptr;  // totals_h: mapped pinned
@@ -258,7 +258,7 @@ bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P
 
 void free_layout(gcr_ctx *c) {
     void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
-                    c->tile_off, c->slice_raw, c->slice_nz, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
+                    c->tile_off, c->pieces, c->contrib, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
                     c->entries_d, c->totals_d, c->misc_d, c->done_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -272,8 +272,9 @@ void free_layout(gcr_ctx *c) {
     c->page_alloc = c->tile_alloc = c->D[0] = c->D[1] = nullptr;
     c->cls = nullptr;
     c->tile_info = nullptr;
-    c->tile_off = c->slice_raw = nullptr;
-    c->slice_nz = nullptr;
+    c->tile_off = nullptr;
+    c->pieces = nullptr;
+    c->contrib = nullptr;
     c->pm_blk_cnt = c->pm_blk_off = c->run_start = nullptr;
     c->entries_d = nullptr;
     c->totals_d = c->totals_h = nullptr;
@@ -290,7 +291,7 @@ gcr_status build_layout(gcr_ctx *c) {
     c->P = P;
     c->lg = lg;
     c->allocs_h.clear();
-    uint64_t g = 0, t = 0;
+    uint64_t g = 0, t = 0, rows = 0;
     for (const RegEntry &r : c->reg) {
         AllocDev a{};
         a.base = r.dptr;
@@ -302,6 +303,9 @@ gcr_status build_layout(gcr_ctx *c) {
                                     : a.n_pages * (P / kTileBytes);
         a.tail_len = (uint32_t)(r.bytes - (uint64_t)(a.n_pages - 1) * P);
         a.z_tail = zero_digest(a.tail_len);
+        a.row0 = rows;
+        a.n_rows = (uint64_t)(a.n_pages - 1) * (P / kRowBytes) + (a.tail_len + kRowBytes - 1) / kRowBytes;
+        rows += a.n_rows;
         g += a.n_pages;
         t += a.n_tiles;
         c->allocs_h.push_back(a);
@@ -328,10 +332,22 @@ gcr_status build_layout(gcr_ctx *c) {
         const uint64_t lt = tile - a.tile0;
         return a.page0 + (P <= kTileBytes ? lt * (kTileBytes / P) : lt / (P / kTileBytes));
     };
+    auto row_of_page = [&](uint64_t page) -> uint64_t {
+        if (page >= g) return rows;
+        size_t lo = 0, hi = c->allocs_h.size();
+        while (hi - lo > 1) {
+            size_t mid = (lo + hi) / 2;
+            if (c->allocs_h[mid].page0 <= page) lo = mid; else hi = mid;
+        }
+        return c->allocs_h[lo].row0 + (page - c->allocs_h[lo].page0) * (P / kRowBytes);
+    };
     for (Chunk &ch : c->chunks) {
         ch.page_begin = page_of_tile(ch.tile_begin);
         ch.page_end = page_of_tile(ch.tile_end);
+        ch.row_begin = row_of_page(ch.page_begin);
+        ch.row_end = row_of_page(ch.page_end);
     }
+    c->n_rows = rows;
     const uint64_t na = c->allocs_h.size(), nblk = (g + 4095) / 4096, nch = c->chunks.size();
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaMalloc(&c->allocs_d, sizeof(AllocDev) * na));
@@ -342,15 +358,15 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->cls, g));
     CUDA_TRY(c, cudaMalloc(&c->tile_info, sizeof(TileInfo) * t));
     CUDA_TRY(c, cudaMalloc(&c->tile_off, 4 * t));
-    if (P > kTileBytes) {
-        CUDA_TRY(c, cudaMalloc(&c->slice_raw, 4 * t));
-        CUDA_TRY(c, cudaMalloc(&c->slice_nz, t));
-    }
+    CUDA_TRY(c, cudaMemset(c->tile_info, 0, sizeof(TileInfo) * t));
+    CUDA_TRY(c, cudaMalloc(&c->pieces, sizeof(Piece) * 2 * scan_groups(~0ull >> 8, c->n_sms)));
+    CUDA_TRY(c, cudaMalloc(&c->contrib, sizeof(uint32_t) * 2 * scan_groups(~0ull >> 8, c->n_sms)));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_cnt, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
     CUDA_TRY(c, cudaMalloc(&c->entries_d, sizeof(gcr_pagemap_entry) * g));
     CUDA_TRY(c, cudaMalloc(&c->totals_d, sizeof(ChunkTotals) * nch));
+    CUDA_TRY(c, cudaMemset(c->totals_d, 0, sizeof(ChunkTotals) * nch));
     CUDA_TRY(c, cudaHostAlloc(&c->totals_h, sizeof(ChunkTotals) * nch, cudaHostAllocMapped));
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->totals_map), c->totals_h, 0));
     CUDA_TRY(c, cudaMalloc(&c->done_d, sizeof(unsigned) * nch));
@@ -663,7 +679,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
 
     ScanParams sp{};
     sp.allocs = c->allocs_d;
-    sp.tile_alloc = c->tile_alloc;
+    sp.n_allocs = (uint32_t)c->allocs_h.size();
+    sp.pieces = c->pieces;
+    sp.contrib = c->contrib;
     sp.page_size = P;
     sp.log2_page = c->lg;
     sp.z_page = c->z_page;
@@ -672,8 +690,6 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.d_out = Dnew;
     sp.cls = c->cls;
     sp.tile_info = c->tile_info;
-    sp.slice_raw = c->slice_raw;
-    sp.slice_nz = c->slice_nz;
     sp.tables = c->tables_d;
     sp.done = c->done_d;
     sp.tile_off = c->tile_off;
@@ -688,6 +704,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         const Chunk &ch = c->chunks[i];
         sp.tile_begin = ch.tile_begin;
         sp.tile_end = ch.tile_end;
+        sp.row_begin = ch.row_begin;
+        sp.row_end = ch.row_end;
+        sp.groups = scan_groups(ch.row_end - ch.row_begin, c->n_sms);
         sp.chunk_idx = (uint32_t)i;
         sp.totals_dev = c->totals_d + i;
         sp.totals_host = c->totals_map + i;
@@ -722,9 +741,12 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         pke[i] = c->ev();
         CUDA_TRY(c, cudaEventRecord(pks[i], cs));
         if (T.image_bytes) {
+            LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off, cs));
             LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, c->tile_off, ch.tile_begin, ch.tile_end, P,
                                       c->lg, c->slots[i % S], c->n_sms, cs));
         }
+        if (!T.image_bytes)  // nothing to pack, but the tile counters must be re-zeroed
+            LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off, cs));
         CUDA_TRY(c, cudaEventRecord(pke[i], cs));
         if (base + T.image_bytes > R) return fail(c, GCR_E_CUDA, "checkpoint: image larger than registry");
         if (T.image_bytes)
@@ -845,6 +867,11 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
     s = checkpoint_impl(c, mode, img);
     if (s != GCR_OK) {
         sync_all(c);
+        // re-arm the per-launch device state the kernels leave zeroed on success
+        cudaMemset(c->tile_info, 0, sizeof(TileInfo) * c->n_tiles);
+        cudaMemset(c->done_d, 0, sizeof(unsigned) * c->chunks.size());
+        cudaMemset(c->totals_d, 0, sizeof(ChunkTotals) * c->chunks.size());
+        cudaGetLastError();
         image_free_buffers(img);
         delete img;
         c->have_parent = had_parent;  // failure atomicity
@@ -1022,7 +1049,12 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         CUDA_TRY(c, cudaMemsetAsync(c->misc_d + 2, 0xFF, 8, c->compute));
         ScanParams sp{};
         sp.allocs = c->allocs_d;
-        sp.tile_alloc = c->tile_alloc;
+        sp.n_allocs = (uint32_t)c->allocs_h.size();
+        sp.pieces = c->pieces;
+        sp.contrib = c->contrib;
+        sp.row_begin = 0;
+        sp.row_end = c->n_rows;
+        sp.groups = scan_groups(c->n_rows, c->n_sms);
         sp.tile_begin = 0;
         sp.tile_end = c->n_tiles;
         sp.page_size = P;
@@ -1030,8 +1062,6 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.z_page = c->z_page;
         sp.mode = kScanVerify;
         sp.d_ref = c->D[scratch];
-        sp.slice_raw = c->slice_raw;
-        sp.slice_nz = c->slice_nz;
         sp.verify_count = c->misc_d + 1;
         sp.first_bad = c->misc_d + 2;
         sp.tables = c->tables_d;

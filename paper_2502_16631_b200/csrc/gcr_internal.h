@@ -33,6 +33,16 @@ struct AllocDev {
     uint32_t n_tiles;
     uint32_t tail_len;  // length of its last page (== page_size if none is short)
     uint32_t z_tail;    // Z(tail_len) = CRC32C of tail_len zero bytes
+    uint64_t row0;      // global index of its first REAL 128-byte row
+    uint64_t n_rows;    // (n_pages-1)*P/128 + ceil(tail_len/128)
+};
+
+// Partial raw register of a page cut by a K1 group boundary (folded by K1b).
+struct Piece {
+    unsigned long long page;  // global page index, ~0 = empty slot
+    uint32_t alloc;
+    uint32_t vr_begin, vr_end;  // virtual rows [vr_begin, vr_end) of the page
+    uint32_t raw, nz;
 };
 
 // Per-tile result of the scan used by compaction (K2) and pack (K4).
@@ -55,15 +65,17 @@ struct CrcTables {
     uint32_t a16[4][256];    // d = 16  (lane tree, level 0)
     uint32_t a32[4][256];    // d = 32  (level 1)
     uint32_t a64[4][256];    // d = 64  (level 2)
-    uint32_t a16k[4][256];   // d = 16 KiB (group combine, level 0)
-    uint32_t a32k[4][256];   // d = 32 KiB (group combine, level 1)
-    uint32_t a64k[4][256];   // d = 64 KiB (slice fold, pages > 64 KiB)
+    uint32_t fold[14][4][256];  // d = 128 * 2^j: arbitrary row-distance folds of K1b
 };
 
 struct ScanParams {
     const AllocDev *allocs;
-    const uint32_t *tile_alloc;
-    uint64_t tile_begin, tile_end;
+    uint32_t n_allocs;
+    uint64_t row_begin, row_end;   // chunk: global real rows (page aligned)
+    uint64_t groups;               // 8-lane groups sharing the rows equally
+    Piece *pieces;                 // 2 per group
+    uint32_t *contrib;             // 2 per group: piece contribution adv_{(Rp-vend)*128}(raw)
+    uint64_t tile_begin, tile_end; // chunk: tiles (compaction)
     uint32_t page_size, log2_page;
     uint32_t z_page;
     int mode;
@@ -71,8 +83,6 @@ struct ScanParams {
     uint32_t *d_out;           // D_new (full / incremental)
     uint8_t *cls;              // class per page (full / incremental)
     TileInfo *tile_info;       // per tile (full / incremental)
-    uint32_t *slice_raw;       // per tile, pages > 64 KiB
-    uint8_t *slice_nz;         // per tile, pages > 64 KiB
     unsigned long long *verify_count;
     unsigned long long *first_bad;
     const CrcTables *tables;
@@ -80,8 +90,8 @@ struct ScanParams {
     unsigned *done;              // per-chunk CTA tickets, zero between launches
     uint32_t chunk_idx;
     uint32_t *tile_off;
-    ChunkTotals *totals_dev;
-    ChunkTotals *totals_host;    // mapped pinned
+    ChunkTotals *totals_dev;     // device accumulator (zero between launches)
+    ChunkTotals *totals_host;    // mapped pinned, published by K1b's last CTA
 };
 
 struct ScatterDesc {
@@ -101,7 +111,10 @@ struct ZeroDesc {
 int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t *page_alloc,
                             uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
                             cudaStream_t st);
+uint64_t scan_groups(uint64_t rows, int n_sms);
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);
+int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, uint32_t *tile_off,
+                     cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
                 const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, int n_sms, cudaStream_t st);

@@ -5,7 +5,8 @@
 //  K1 scan               A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
 //                        all-zero test, dirty diff, class; tile summaries
 //  K1b fold_slices       pages > 64 KiB: fold the 64 KiB slice registers
-//  K2 chunk_scan         A5: chunk-local exclusive scan of PRESENT bytes (last CTA of K1)
+//  K2 tile_scan          A5: chunk-local exclusive scan of PRESENT bytes per tile (pack offsets);
+//                        chunk totals via CTA-aggregated atomics, published by K1b's last CTA
 //  K3 pagemap_*          A5: maximal runs -> CRIU-style pagemap entries
 //  K4 pack               A6: stream-compaction of PRESENT pages into staging
 //  K6 scatter            A8: staged image pieces -> allocation pages
@@ -37,8 +38,9 @@ namespace gcr {
 namespace {
 
 constexpr uint32_t kBraidSmem = 4u * 256u * 32u * 4u;  // 128 KiB
-constexpr uint32_t kSmallTables = 6;                   // t4 a16 a32 a64 a16k a32k
+constexpr uint32_t kSmallTables = 4;                   // t4 a16 a32 a64
 constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u;
+constexpr uint32_t kFoldTables = 14;  // adv_{128 * 2^j}, j < 14: row distances < 16384 (P <= 2 MiB)
 #ifndef GCR_SCAN_THREADS
 #define GCR_SCAN_THREADS 640
 #endif
@@ -48,7 +50,7 @@ constexpr int kScanThreads = GCR_SCAN_THREADS;
 #endif
 constexpr int kScanUnroll = GCR_SCAN_UNROLL;
 
-enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3, kA16K = 4, kA32K = 5 };
+enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
@@ -65,19 +67,30 @@ __device__ __forceinline__ uint4 ldg_stream(const void *p) {
     return r;
 }
 
-__device__ __forceinline__ uint32_t lds_at(const char *base, uint32_t off) {
-    return *reinterpret_cast<const uint32_t *>(base + off);
+template <int kOff>
+__device__ __forceinline__ uint32_t lds_imm(uint32_t saddr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(saddr), "n"(kOff));
+    return v;
 }
 
-// x -> adv_128(x) through the lane-private braid tables.
-__device__ __forceinline__ uint32_t braid(const char *smb, uint32_t x, uint32_t lane4) {
-    const uint32_t i0 = prmt(x, lane4, 0x5504u);
-    const uint32_t i1 = prmt(x, lane4, 0x5514u);
-    const uint32_t i2 = prmt(x, lane4, 0x5524u);
-    const uint32_t i3 = prmt(x, lane4, 0x5534u);
-    return lds_at(smb, i0) ^ lds_at(smb, i1 + 128u) ^ lds_at(smb, i2 + 65536u) ^
-           lds_at(smb, i3 + 65536u + 128u);
+// x -> adv_128(x) through the lane-private braid tables (shared address sb =
+// table base).  prmt(x, l*4, 0x55k4) = byte_k(x) << 8 | l*4 builds the scaled
+// index in one instruction; the table number lives in the ld.shared
+// immediate.  The base add runs on the FMA pipe (IMAD.IADD), which the
+// lookups leave idle.  (A 64 KiB-aligned table base would fold it into the
+// prmt but costs ~63 KiB of L1, which the streaming loads need in flight.)
+__device__ __forceinline__ uint32_t braid(uint32_t x, uint32_t lane4, uint32_t sb) {
+    const uint32_t i0 = prmt(x, lane4, 0x5504u) + sb;
+    const uint32_t i1 = prmt(x, lane4, 0x5514u) + sb;
+    const uint32_t i2 = prmt(x, lane4, 0x5524u) + sb;
+    const uint32_t i3 = prmt(x, lane4, 0x5534u) + sb;
+    return lds_imm<0>(i0) ^ lds_imm<128>(i1) ^ lds_imm<65536>(i2) ^ lds_imm<65536 + 128>(i3);
 }
+
+struct BraidCtx {
+    uint32_t lane4, sb;
+};
 
 // v -> adv_d(v) through an unreplicated 4x256 table (used once per segment).
 __device__ __forceinline__ uint32_t apply_tab(const uint32_t *tb, uint32_t v) {
@@ -85,13 +98,12 @@ __device__ __forceinline__ uint32_t apply_tab(const uint32_t *tb, uint32_t v) {
            tb[768u + (v >> 24)];
 }
 
-__device__ __forceinline__ void row_step(const char *smb, uint32_t lane4, uint32_t (&x)[4],
-                                         uint32_t &acc, const uint4 &w) {
+__device__ __forceinline__ void row_step(BraidCtx cl, uint32_t (&x)[4], uint32_t &acc, const uint4 &w) {
     acc |= w.x | w.y | w.z | w.w;
-    x[0] = braid(smb, x[0], lane4) ^ w.x;
-    x[1] = braid(smb, x[1], lane4) ^ w.y;
-    x[2] = braid(smb, x[2], lane4) ^ w.z;
-    x[3] = braid(smb, x[3], lane4) ^ w.w;
+    x[0] = braid(x[0], cl.lane4, cl.sb) ^ w.x;
+    x[1] = braid(x[1], cl.lane4, cl.sb) ^ w.y;
+    x[2] = braid(x[2], cl.lane4, cl.sb) ^ w.z;
+    x[3] = braid(x[3], cl.lane4, cl.sb) ^ w.w;
 }
 
 // Stream rows [r0, R) of one segment.  gp is this lane's pointer for virtual
@@ -106,8 +118,7 @@ __device__ __forceinline__ void load_block(uint4 (&w)[U], const char *gp, int r,
 }
 
 template <int U, bool kFirst>
-__device__ __forceinline__ void proc_block(const char *smb, uint32_t lane4, uint32_t (&x)[4], uint32_t &acc,
-                                           const uint4 (&w)[U]) {
+__device__ __forceinline__ void proc_block(BraidCtx cl, uint32_t (&x)[4], uint32_t &acc, const uint4 (&w)[U]) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
         if (kFirst && u == 0) {  // x = 0 before the first row: adv_128(0) ^ w == w
@@ -117,7 +128,7 @@ __device__ __forceinline__ void proc_block(const char *smb, uint32_t lane4, uint
             x[3] = w[0].w;
             acc = w[0].x | w[0].y | w[0].z | w[0].w;
         } else {
-            row_step(smb, lane4, x, acc, w[u]);
+            row_step(cl, x, acc, w[u]);
         }
     }
 }
@@ -125,8 +136,8 @@ __device__ __forceinline__ void proc_block(const char *smb, uint32_t lane4, uint
 // Rows are consumed in blocks of U with the next block's loads in flight
 // (register double buffering): the scan is bound by bytes in flight per SM.
 template <int U>
-__device__ __forceinline__ void seg_stream(const char *smb, uint32_t lane4, const char *gp, int r0,
-                                           int R, bool first_ok, uint32_t (&x)[4], uint32_t &acc) {
+__device__ __forceinline__ void seg_stream(BraidCtx cl, const char *gp, int r0, int R, bool first_ok,
+                                           uint32_t (&x)[4], uint32_t &acc) {
     const int nblk = (R - r0) / U;
     int r = r0;
     bool started = false;
@@ -134,19 +145,19 @@ __device__ __forceinline__ void seg_stream(const char *smb, uint32_t lane4, cons
         uint4 wa[U], wb[U];
         load_block<U>(wa, gp, r, true, first_ok);
         if (nblk > 1) load_block<U>(wb, gp, r + U, false, true);
-        proc_block<U, true>(smb, lane4, x, acc, wa);
+        proc_block<U, true>(cl, x, acc, wa);
         r += U;
         int b = 1;
         for (; b + 1 < nblk; b += 2) {
             load_block<U>(wa, gp, r + U, false, true);
-            proc_block<U, false>(smb, lane4, x, acc, wb);
+            proc_block<U, false>(cl, x, acc, wb);
             r += U;
             if (b + 2 < nblk) load_block<U>(wb, gp, r + U, false, true);
-            proc_block<U, false>(smb, lane4, x, acc, wa);
+            proc_block<U, false>(cl, x, acc, wa);
             r += U;
         }
         if (b < nblk) {
-            proc_block<U, false>(smb, lane4, x, acc, wb);
+            proc_block<U, false>(cl, x, acc, wb);
             r += U;
         }
         started = true;
@@ -161,7 +172,7 @@ __device__ __forceinline__ void seg_stream(const char *smb, uint32_t lane4, cons
             x[3] = v.w;
             acc = v.x | v.y | v.z | v.w;
         } else {
-            row_step(smb, lane4, x, acc, v);
+            row_step(cl, x, acc, v);
         }
     }
 }
@@ -183,15 +194,24 @@ __device__ __forceinline__ uint32_t group_raw(const uint32_t *small, const uint3
     return v;
 }
 
-struct PageAcc {
-    uint32_t present_bytes = 0, counts = 0;
+// Tile that anchors page pi of an allocation for compaction/pack: the tile
+// holding it (P <= 64 KiB) or its first 64 KiB slice (P > 64 KiB).
+__device__ __forceinline__ uint64_t tile_of_page(uint64_t tile0, uint64_t pi, uint32_t P, uint32_t lg) {
+    return P <= kTileBytes ? tile0 + (pi >> (kLog2Tile - lg)) : tile0 + (pi << (lg - kLog2Tile));
+}
+
+// Per-CTA accumulators of the chunk totals (flushed with one global atomic
+// per CTA per counter: no same-address atomic storm at L2).
+struct CtaTotals {
+    unsigned long long image_bytes, n_present, n_zero, n_parent;
 };
 
-// c.1 steps 3-5 for one page given its raw register and non-zero flag
-// (or the A9 verify comparison).  Executed by one lane.
-__device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, bool alloc_start,
-                                              uint32_t len, uint32_t zlen, uint32_t raw, bool nz,
-                                              PageAcc &acc) {
+// c.1 steps 3-5 for one page given its raw register and non-zero flag (or
+// the A9 verify comparison), plus the per-tile and per-CTA compaction
+// counters.  Executed by one lane.
+__device__ __forceinline__ void finalize_page(const ScanParams &p, CtaTotals *ct, uint64_t g, uint64_t tile,
+                                              bool alloc_start, uint32_t len, uint32_t zlen, uint32_t raw,
+                                              bool nz) {
     const uint32_t d = raw ^ zlen;
     if (p.mode == kScanVerify) {
         if (d != __ldg(p.d_ref + g)) {
@@ -201,19 +221,41 @@ __device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, b
         return;
     }
     uint8_t c;
+    uint32_t inc;
     if (!nz) {
         c = kClsZero;
-        acc.counts += 1u << 10;
+        inc = 1u << 10;
+        atomicAdd(&ct->n_zero, 1ull);
     } else if (p.mode == kScanIncremental && __ldg(p.d_ref + g) == d) {
         c = kClsParent;
-        acc.counts += 1u << 20;
+        inc = 1u << 20;
+        atomicAdd(&ct->n_parent, 1ull);
     } else {
         c = kClsPresent;
-        acc.counts += 1u;
-        acc.present_bytes += len;
+        inc = 1u;
+        atomicAdd(&p.tile_info[tile].present_bytes, len);
+        atomicAdd(&ct->n_present, 1ull);
+        atomicAdd(&ct->image_bytes, (unsigned long long)len);
     }
+    atomicAdd(&p.tile_info[tile].counts, inc);
     p.d_out[g] = d;
     p.cls[g] = c | (alloc_start ? kClsAllocStart : 0);
+}
+
+__device__ __forceinline__ void cta_totals_init(CtaTotals *ct) {
+    if (threadIdx.x == 0) *ct = CtaTotals{0ull, 0ull, 0ull, 0ull};
+}
+
+// Flush this CTA's totals into the chunk accumulator (device memory).
+__device__ __forceinline__ void cta_totals_flush(const ScanParams &p, CtaTotals *ct) {
+    __syncthreads();
+    if (threadIdx.x == 0 && p.mode != kScanVerify) {
+        unsigned long long *acc = reinterpret_cast<unsigned long long *>(p.totals_dev);
+        if (ct->image_bytes) atomicAdd(acc + 0, ct->image_bytes);
+        if (ct->n_present) atomicAdd(acc + 1, ct->n_present);
+        if (ct->n_zero) atomicAdd(acc + 2, ct->n_zero);
+        if (ct->n_parent) atomicAdd(acc + 3, ct->n_parent);
+    }
 }
 
 // Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
@@ -247,72 +289,91 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
     return res;
 }
 
-// K2 (run by the LAST CTA of the chunk's scan): chunk-local exclusive scan of
-// PRESENT bytes over tiles -> tile_off, and the chunk totals, stored both to
-// device memory and straight into mapped pinned host memory so the host learns
-// the chunk's image size without a DMA queued behind the drain.
-__device__ void chunk_scan(const TileInfo *ti, uint64_t tb, uint64_t te, uint32_t *tile_off,
-                           ChunkTotals *tot_dev, ChunkTotals *tot_host) {
-    const uint64_t n = te - tb;
-    const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
-    const uint64_t lo = tb + per * threadIdx.x;
-    const uint64_t hi = min(te, lo + per);
-    unsigned long long s = 0, np = 0, nzr = 0, npa = 0;
-    for (uint64_t t = lo; t < hi; t++) {
-        const uint2 v = __ldcg(reinterpret_cast<const uint2 *>(ti) + t);
-        const TileInfo x{v.x, v.y};
-        s += x.present_bytes;
-        np += x.counts & 1023u;
-        nzr += (x.counts >> 10) & 1023u;
-        npa += (x.counts >> 20) & 1023u;
-    }
-    unsigned long long total;
-    unsigned long long off = block_exclusive_scan(s, &total);
-    for (uint64_t t = lo; t < hi; t++) {
-        tile_off[t] = (uint32_t)off;
-        off += __ldcg(reinterpret_cast<const unsigned *>(ti) + 2 * t);
-    }
-    unsigned long long tp, tz, tpa;
-    block_exclusive_scan(np, &tp);
-    block_exclusive_scan(nzr, &tz);
-    block_exclusive_scan(npa, &tpa);
-    if (threadIdx.x == 0) {
-        const ChunkTotals T{total, tp, tz, tpa};
-        *tot_dev = T;
-        volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(tot_host);
-        h[0] = T.image_bytes;
-        h[1] = T.n_present;
-        h[2] = T.n_zero;
-        h[3] = T.n_parent;
-        __threadfence_system();
-    }
-}
-
-// Last-CTA-done: every CTA fences its tile_info writes, takes a ticket, and the
-// CTA holding the last ticket runs chunk_scan (then re-arms the counter).
-__device__ __forceinline__ void last_cta_chunk_scan(const ScanParams &p) {
+// Last-CTA-done of K1b: every CTA has flushed its totals; the CTA holding the
+// last ticket publishes the chunk totals straight into mapped pinned host
+// memory (no DMA queued behind the drain on the copy engines), re-zeroes the
+// device accumulator and re-arms the ticket counter.
+__device__ __forceinline__ void last_cta_publish(const ScanParams &p) {
     __shared__ bool am_last;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) am_last = atomicAdd(p.done + p.chunk_idx, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (!am_last) return;
+    if (!am_last || threadIdx.x != 0) return;
     __threadfence();
-    chunk_scan(p.tile_info, p.tile_begin, p.tile_end, p.tile_off, p.totals_dev, p.totals_host);
-    if (threadIdx.x == 0) p.done[p.chunk_idx] = 0u;
+    volatile unsigned long long *acc = reinterpret_cast<volatile unsigned long long *>(p.totals_dev);
+    volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(p.totals_host);
+    const unsigned long long a0 = acc[0], a1 = acc[1], a2 = acc[2], a3 = acc[3];
+    h[0] = a0;
+    h[1] = a1;
+    h[2] = a2;
+    h[3] = a3;
+    acc[0] = acc[1] = acc[2] = acc[3] = 0ull;
+    __threadfence_system();
+    p.done[p.chunk_idx] = 0u;
 }
 
+// K2: chunk-local exclusive scan of PRESENT bytes over the chunk's tiles ->
+// tile_off (the pack's destination offsets); re-zeroes the tile counters.
+// One CTA, coalesced rounds of blockDim tiles.  Runs on the copy stream right
+// before K4, off the scan's critical path.
+__global__ void __launch_bounds__(1024) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te, uint32_t *tile_off) {
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0ull;
+    __syncthreads();
+    for (uint64_t base = tb; base < te; base += blockDim.x) {
+        const uint64_t t = base + threadIdx.x;
+        unsigned v = 0;
+        if (t < te) {
+            v = ti[t].present_bytes;
+            ti[t] = TileInfo{0u, 0u};
+        }
+        unsigned long long tot;
+        const unsigned long long off = block_exclusive_scan(v, &tot) + carry;
+        if (t < te) tile_off[t] = (uint32_t)off;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+}
+
+// Allocation holding global real row r: 8-ary search by the 8 lanes of a
+// group (each round every lane probes one row0; one ballot narrows the range
+// 8x), so a group's start costs ~log8(n_allocs) dependent loads, not log2.
+__device__ __forceinline__ uint32_t alloc_of_row(const AllocDev *al, uint32_t n, uint64_t r, uint32_t q,
+                                                 uint32_t grp, unsigned gmask) {
+    uint32_t lo = 0, hi = n;  // al[lo].row0 <= r < al[hi].row0 (al[n] = +inf)
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 7) / 8;
+        const uint32_t probe = lo + q * step;
+        const bool le = probe < hi && __ldg(&al[probe].row0) <= r;
+        const unsigned b = (__ballot_sync(gmask, le) >> (8 * grp)) & 0xFFu;
+        const uint32_t qm = 31 - __clz(b);  // lane 0 (probe = lo) always qualifies
+        lo = lo + qm * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
+// K1.  The chunk's REAL rows (128-byte rows of page data; the virtual zero
+// padding in front of a short page is not counted) are split into equal
+// contiguous ranges, one per 8-lane group, so every group streams the same
+// number of bytes whatever the page size or the chunk size (no wave
+// quantization).  A group walks its range page by page: pages wholly inside
+// are finalized in place; a page cut by the range boundary yields a PIECE
+// (its raw register over the rows the group saw) that K1b folds.
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
-    const char *smb = reinterpret_cast<const char *>(sm);
-    const uint32_t *small = sm + kBraidSmem / 4;
+    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
+    uint32_t *tabp = sm;
+    const uint32_t *small = tabp + kBraidSmem / 4;
 
     // Stage the tables.  Each thread loads a few table words once (all loads
     // issued before any store) and writes the braid words to all 32 lane-private
     // replicas: word (k>>1)*16384 + e*64 + (k&1)*32 + l.
     {
         const uint32_t *gb = &p.tables->braid[0][0];
-        const uint32_t *gs = &p.tables->t4[0][0];  // t4..a32k are contiguous
+        const uint32_t *gs = &p.tables->t4[0][0];  // t4, a16, a32, a64 are contiguous
         constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
         constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
         uint32_t bv[kPer], sv[kPerS];
@@ -331,153 +392,135 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             const uint32_t ke = threadIdx.x + j * kScanThreads;
             if (ke < 1024u) {
                 const uint32_t k = ke >> 8, e = ke & 255u;
-                uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
+                uint4 *dst = reinterpret_cast<uint4 *>(tabp + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
                 const uint4 v4 = make_uint4(bv[j], bv[j], bv[j], bv[j]);
 #pragma unroll
                 for (int l = 0; l < 8; l++) dst[l] = v4;
             }
         }
-        uint32_t *ss = sm + kBraidSmem / 4;
+        uint32_t *ss = tabp + kBraidSmem / 4;
 #pragma unroll
         for (uint32_t j = 0; j < kPerS; j++) {
             const uint32_t i = threadIdx.x + j * kScanThreads;
             if (i < kSmallTables * 1024u) ss[i] = sv[j];
         }
     }
+    __shared__ CtaTotals ct;
+    cta_totals_init(&ct);
     __syncthreads();
 
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31u;
     const uint32_t grp = lane >> 3, q = lane & 7u;
-    const uint32_t lane4 = lane * 4u;
+    const BraidCtx cl{lane * 4u, tab};
     const unsigned gmask = 0xFFu << (8u * grp);
-    const uint32_t P = p.page_size, lg = p.log2_page;
-    const uint32_t seg = P < kGroupBytes ? P : kGroupBytes;
-    const int R = (int)(seg / kRowBytes);
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-
-    for (uint64_t t = p.tile_begin + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; t < p.tile_end;
-         t += nwarps) {
-        const uint32_t a = __ldg(p.tile_alloc + t);
-        const AllocDev *al = p.allocs + a;
-        const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), tile0 = __ldg(&al->tile0);
-        const uint32_t n_pages = __ldg(&al->n_pages), tail_len = __ldg(&al->tail_len),
-                       z_tail = __ldg(&al->z_tail);
-        const uint64_t lt = t - tile0;
-        PageAcc pa;
-
-        if (P <= kGroupBytes) {
-            // ---- pages <= 16 KiB: each group owns 16K/P whole pages ------------
-            const uint32_t ppg = kGroupBytes >> lg;          // pages per group
-            const uint64_t pi0 = lt * (kTileBytes >> lg) + (uint64_t)grp * ppg;
-            for (uint32_t i = 0; i < ppg; i++) {
-                const uint64_t pi = pi0 + i;
-                if (pi >= n_pages) break;                    // group-uniform
-                const bool tail = pi == (uint64_t)n_pages - 1;
-                const uint32_t len = tail ? tail_len : P;
-                const uint32_t pad = P - len;
-                const char *gp = reinterpret_cast<const char *>(base + (pi << lg)) - pad + q * 16u;
-                const int r0 = (int)(pad >> 7);
-                const bool first_ok = ((uint32_t)r0 * kRowBytes + q * 16u) >= pad;
-                uint32_t x[4], acc;
-                seg_stream<kScanUnroll>(smb, lane4, gp, r0, R, first_ok, x, acc);
-                const uint32_t raw = group_raw(small, x, gmask);
-                const bool nz = (__ballot_sync(gmask, acc != 0) & gmask) != 0;
-                if (q == 0)
-                    finalize_page(p, page0 + pi, pi == 0, len, tail ? z_tail : p.z_page, raw, nz, pa);
+    const uint64_t gid = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4u + grp;
+    if (gid < p.groups) {
+        const uint32_t P = p.page_size, lg = p.log2_page;
+        const int Rp = (int)(P >> 7);  // virtual rows per page
+        const uint64_t rows = p.row_end - p.row_begin;
+        uint64_t r = p.row_begin + rows * gid / p.groups;
+        const uint64_t rend = p.row_begin + rows * (gid + 1) / p.groups;
+        uint32_t a = alloc_of_row(p.allocs, p.n_allocs, r, q, grp, gmask);
+        int slot = 0;
+        Piece *pc = p.pieces + 2 * gid;
+        while (r < rend) {
+            const AllocDev *al = p.allocs + a;
+            const uint64_t row0 = __ldg(&al->row0), rows_a = __ldg(&al->n_rows);
+            if (r >= row0 + rows_a) {  // range continues in the next allocation
+                a++;
+                continue;
             }
-            __syncwarp();
-        } else {
-            // ---- pages >= 32 KiB: each group streams one 16 KiB segment --------
-            uint64_t pi;
-            uint32_t po;
-            if (P <= kTileBytes) {
-                pi = lt * (kTileBytes >> lg) + ((grp * kGroupBytes) >> lg);
-                po = (grp * kGroupBytes) & (P - 1u);
-            } else {
-                const uint32_t tpp = P >> kLog2Tile;
-                pi = lt / tpp;
-                po = (uint32_t)(lt % tpp) * kTileBytes + grp * kGroupBytes;
-            }
-            uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u;
-            const bool exists = pi < n_pages;
+            const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), tile0 = __ldg(&al->tile0);
+            const uint32_t n_pages = __ldg(&al->n_pages), tail_len = __ldg(&al->tail_len);
+            const uint64_t lr = r - row0;
+            uint64_t pi = lr >> (lg - 7);
+            if (pi >= n_pages) pi = n_pages - 1;
             const bool tail = pi == (uint64_t)n_pages - 1;
             const uint32_t len = tail ? tail_len : P;
-            if (exists) {
-                const uint32_t pad = P - len;
-                const uint32_t ds = pad > po ? pad - po : 0u;
-                if (ds < kGroupBytes) {
-                    const char *gp = reinterpret_cast<const char *>(base + (pi << lg)) + po - pad + q * 16u;
-                    const int r0 = (int)(ds >> 7);
-                    const bool first_ok = ((uint32_t)r0 * kRowBytes + q * 16u) >= ds;
-                    seg_stream<kScanUnroll>(smb, lane4, gp, r0, R, first_ok, x, acc);
+            const uint32_t pad = P - len;
+            const int r0 = (int)(pad >> 7);
+            const int vr = (int)(lr - (pi << (lg - 7))) + r0;
+            const uint64_t left = rend - r;
+            const int vend = (uint64_t)(Rp - vr) <= left ? Rp : vr + (int)left;
+            const char *gp = reinterpret_cast<const char *>(base + (pi << lg)) - pad + q * 16u;
+            const bool first_ok = vr > r0 || ((uint32_t)r0 * kRowBytes + q * 16u) >= pad;
+            uint32_t x[4], acc;
+            seg_stream<kScanUnroll>(cl, gp, vr, vend, first_ok, x, acc);
+            const uint32_t raw = group_raw(small, x, gmask);
+            const bool nz = (__ballot_sync(gmask, acc != 0) & gmask) != 0;
+            if (q == 0) {
+                if (vr == r0 && vend == Rp) {
+                    finalize_page(p, &ct, page0 + pi, tile_of_page(tile0, pi, P, lg), pi == 0, len,
+                                  tail ? __ldg(&al->z_tail) : p.z_page, raw, nz);
+                } else {
+                    pc[slot] = Piece{page0 + pi, a, (uint32_t)vr, (uint32_t)vend, raw, nz ? 1u : 0u};
+                    slot++;
                 }
             }
-            __syncwarp();
-            const uint32_t graw = group_raw(small, x, gmask);
-            const unsigned nzb = __ballot_sync(0xFFFFFFFFu, acc != 0);
-            // combine groups: (g0,g1) and (g2,g3) with adv_16K
-            uint32_t o = __shfl_down_sync(0xFFFFFFFFu, graw, 8);
-            const uint32_t c01 = apply_tab(small + kA16K * 1024u, graw) ^ o;
-            if (P == 2u * kGroupBytes) {
-                // two pages per tile: lanes 0 and 16 finalize
-                if ((lane & 15u) == 0 && exists) {
-                    const bool nz = ((nzb >> (lane & 16u)) & 0xFFFFu) != 0;
-                    finalize_page(p, page0 + pi, pi == 0, len, tail ? z_tail : p.z_page, c01, nz, pa);
-                }
-            } else {
-                o = __shfl_down_sync(0xFFFFFFFFu, c01, 16);
-                const uint32_t c = apply_tab(small + kA32K * 1024u, c01) ^ o;
-                if (lane == 0 && exists) {
-                    if (P == kTileBytes) {
-                        finalize_page(p, page0 + pi, pi == 0, len, tail ? z_tail : p.z_page, c, nzb != 0, pa);
-                    } else {
-                        p.slice_raw[t] = c;
-                        p.slice_nz[t] = nzb != 0;
-                    }
-                }
-            }
+            slot = __shfl_sync(gmask, slot, 0, 8);
+            r += (uint64_t)(vend - vr);
         }
-        if (p.mode != kScanVerify && P <= kTileBytes) {
-            const uint32_t pb = __reduce_add_sync(0xFFFFFFFFu, pa.present_bytes);
-            const uint32_t cn = __reduce_add_sync(0xFFFFFFFFu, pa.counts);
-            if (lane == 0) p.tile_info[t] = TileInfo{pb, cn};
-        }
+        if (q == 0)
+            for (; slot < 2; slot++) pc[slot] = Piece{~0ull, 0u, 0u, 0u, 0u, 0u};
     }
-    if (p.mode != kScanVerify && P <= kTileBytes) last_cta_chunk_scan(p);
+    cta_totals_flush(p, &ct);
 }
 
-// K1b: pages > 64 KiB.  One thread per tile; the thread owning slice 0 of a
-// page folds the page's slices: raw = fold_s adv_64K(raw) ^ slice_s.
-__global__ void __launch_bounds__(256) k_fold_slices(const ScanParams p) {
-    __shared__ uint32_t a64k[1024];
-    for (uint32_t i = threadIdx.x; i < 1024u; i += blockDim.x) a64k[i] = __ldg(&p.tables->a64k[0][0] + i);
+// K1b: fold the pieces of pages cut by group boundaries, in two launches.
+// (a) every piece, in parallel: its contribution to its page's register,
+//     adv_{(Rp - vend) * 128}(raw), by the binary expansion of the row
+//     distance through tables fold[j] = adv_{128 * 2^j} (d < 2^14 rows).
+__global__ void __launch_bounds__(256) k_fold_contrib(const ScanParams p) {
+    extern __shared__ uint32_t fsm[];  // kFoldTables x 1024 words
+    for (uint32_t i = threadIdx.x; i < kFoldTables * 1024u; i += blockDim.x) fsm[i] = __ldg(&p.tables->fold[0][0][0] + i);
     __syncthreads();
-    const uint32_t tpp = p.page_size >> kLog2Tile;
-    for (uint64_t t = p.tile_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < p.tile_end;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = __ldg(p.tile_alloc + t);
-        const AllocDev *al = p.allocs + a;
-        const uint64_t lt = t - __ldg(&al->tile0);
-        if (lt % tpp != 0) {
-            if (p.mode != kScanVerify) p.tile_info[t] = TileInfo{0u, 0u};
-            continue;
-        }
-        const uint64_t pi = lt / tpp;
-        uint32_t raw = 0;
-        bool nz = false;
-        for (uint32_t s = 0; s < tpp; s++) {
-            raw = apply_tab(a64k, raw) ^ p.slice_raw[t + s];
-            nz |= p.slice_nz[t + s] != 0;
-        }
-        const uint32_t n_pages = __ldg(&al->n_pages);
-        const bool tail = pi == (uint64_t)n_pages - 1;
-        const uint32_t len = tail ? __ldg(&al->tail_len) : p.page_size;
-        PageAcc pa;
-        finalize_page(p, __ldg(&al->page0) + pi, pi == 0, len, tail ? __ldg(&al->z_tail) : p.z_page, raw,
-                      nz, pa);
-        if (p.mode != kScanVerify) p.tile_info[t] = TileInfo{pa.present_bytes, pa.counts};
+    const uint32_t Rp = p.page_size >> 7;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * p.groups;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const Piece pc = p.pieces[i];
+        if (pc.page == ~0ull) continue;
+        uint32_t d = Rp - pc.vr_end, c = pc.raw;
+        for (uint32_t j = 0; d; j++, d >>= 1)
+            if (d & 1u) c = apply_tab(fsm + j * 1024u, c);
+        p.contrib[i] = c;
     }
-    if (p.mode != kScanVerify) last_cta_chunk_scan(p);
+}
+
+// (b) the group holding a page's FIRST piece owns it: XOR of the contributions
+//     of its piece and of the HEAD pieces of the following groups, then c.1
+//     steps 3-5.  Its last CTA publishes the chunk totals.
+__global__ void __launch_bounds__(256) k_fold_final(const ScanParams p) {
+    __shared__ CtaTotals ct;
+    cta_totals_init(&ct);
+    __syncthreads();
+    const uint32_t P = p.page_size, lg = p.log2_page;
+    const uint32_t Rp = P >> 7;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.groups;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        for (int s = 1; s >= 0; s--) {
+            const Piece pc = p.pieces[2 * j + s];
+            if (pc.page == ~0ull) continue;
+            const AllocDev *al = p.allocs + pc.alloc;
+            const uint64_t pi = pc.page - __ldg(&al->page0);
+            const uint32_t n_pages = __ldg(&al->n_pages);
+            const bool tail = pi == (uint64_t)n_pages - 1;
+            const uint32_t len = tail ? __ldg(&al->tail_len) : P;
+            const uint32_t r0 = (P - len) >> 7;
+            if (pc.vr_begin != r0) continue;  // not the page's first piece
+            uint32_t raw = p.contrib[2 * j + s];
+            bool nz = pc.nz != 0;
+            uint32_t end = pc.vr_end;
+            for (uint64_t k = j + 1; end < Rp && k < p.groups; k++) {
+                raw ^= p.contrib[2 * k];
+                nz |= p.pieces[2 * k].nz != 0;
+                end = p.pieces[2 * k].vr_end;
+            }
+            finalize_page(p, &ct, pc.page, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
+                          tail ? __ldg(&al->z_tail) : p.z_page, raw, nz);
+        }
+    }
+    cta_totals_flush(p, &ct);
+    if (p.mode != kScanVerify) last_cta_publish(p);
 }
 
 // K0: page -> allocation and tile -> allocation (A1).  One CTA per allocation.
@@ -682,28 +725,49 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
     return launched(1);
 }
 
+uint64_t scan_groups(uint64_t rows, int n_sms) {
+    // every group streams >= 32 rows (4 KiB); at most all groups of a full grid
+    const uint64_t full = (uint64_t)n_sms * (kScanThreads / 32) * 4;
+    uint64_t g = rows / 32;
+    if (g < 1) g = 1;
+    return g < full ? g : full;
+}
+
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) !=
-            cudaSuccess)
+    // once per device: setting a function attribute can serialise with work in
+    // flight, which would leave the GPU idle between pipelined chunk launches
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev]) {
+        if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess)
             return -1;
-        attr = true;
+        attr_done[dev] = true;
     }
-    const uint64_t tiles = p.tile_end - p.tile_begin;
-    if (tiles == 0) return 0;
-    const uint64_t wpb = kScanThreads / 32;
-    uint64_t grid = (tiles + wpb - 1) / wpb;
-    if (grid > (uint64_t)n_sms) grid = n_sms;
+    if (p.row_end == p.row_begin) return 0;
+    const uint64_t gpb = (kScanThreads / 32) * 4;
+    const uint64_t grid = (p.groups + gpb - 1) / gpb;
     k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
-    int n = 1;
-    if (p.page_size > kTileBytes) {
-        uint64_t g2 = (tiles + 255) / 256;
-        if (g2 > (uint64_t)n_sms * 8) g2 = n_sms * 8;
-        k_fold_slices<<<(unsigned)g2, 256, 0, st>>>(p);
-        n++;
+    static bool fold_attr[64] = {};
+    if (dev < 64 && !fold_attr[dev]) {
+        if (cudaFuncSetAttribute(k_fold_contrib, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kFoldTables * 4096u)) != cudaSuccess)
+            return -1;
+        fold_attr[dev] = true;
     }
-    return launched(n);
+    uint64_t gc = (2 * p.groups + 255) / 256;
+    if (gc > (uint64_t)n_sms) gc = n_sms;
+    k_fold_contrib<<<(unsigned)gc, 256, kFoldTables * 4096u, st>>>(p);
+    uint64_t g2 = (p.groups + 255) / 256;
+    if (g2 > (uint64_t)n_sms * 4) g2 = n_sms * 4;
+    k_fold_final<<<(unsigned)g2, 256, 0, st>>>(p);
+    return launched(3);
+}
+
+int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off, cudaStream_t st) {
+    if (te == tb) return 0;
+    k_tile_scan<<<1, 1024, 0, st>>>(tile_info, tb, te, tile_off);
+    return launched(1);
 }
 
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, const uint32_t *tile_off,
