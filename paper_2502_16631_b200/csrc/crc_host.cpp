@@ -83,7 +83,9 @@ void build_tables(CrcTables *t) {
     fill_table(t->a16, 16);
     fill_table(t->a32, 32);
     fill_table(t->a64, 64);
-    for (int j = 0; j < 14; j++) fill_table(t->fold[j], (uint64_t)kRowBytes << j);
+    fill_table(t->a128, 128);
+    fill_table(t->a256, 256);
+    for (int j = 0; j < 12; j++) fill_table(t->fold[j], (uint64_t)kRowBytes << j);
 }
 
 uint32_t zero_digest(uint64_t n) { return mat_vec(adv_matrix(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu; }
@@ -133,10 +135,10 @@ bool crc_self_test() {
     }
     uint32_t a = host_crc32c_update(st, s + i, 9 - i) ^ 0xFFFFFFFFu;
     uint32_t b = host_crc32c_update(0xFFFFFFFFu, s, 9) ^ 0xFFFFFFFFu;
-    // braid table consistency: adv_128 == (adv_4)^32 on a probe value
+    // braid table consistency: adv_512 == (adv_4)^128 on a probe value
     uint32_t v = 0x12345678u, w = v;
-    for (int k = 0; k < 32; k++) w = apply4(t->t4, w);
-    // fold tables: adv_{128*2} through fold[1] == braid applied twice
+    for (int k = 0; k < 128; k++) w = apply4(t->t4, w);
+    // fold tables: adv_{512*2} through fold[1] == braid applied twice
     bool ok = a == 0xE3069283u && b == 0xE3069283u && apply4(t->braid, v) == w &&
               zero_digest(65536) == 0x72C0C4A4u && apply4(t->fold[0], v) == w &&
               apply4(t->fold[1], v) == apply4(t->braid, apply4(t->braid, v));

@@ -359,8 +359,8 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->tile_info, sizeof(TileInfo) * t));
     CUDA_TRY(c, cudaMalloc(&c->tile_off, 4 * t));
     CUDA_TRY(c, cudaMemset(c->tile_info, 0, sizeof(TileInfo) * t));
-    CUDA_TRY(c, cudaMalloc(&c->pieces, sizeof(Piece) * 2 * scan_groups(~0ull >> 8, c->n_sms)));
-    CUDA_TRY(c, cudaMalloc(&c->contrib, sizeof(uint32_t) * 2 * scan_groups(~0ull >> 8, c->n_sms)));
+    CUDA_TRY(c, cudaMalloc(&c->pieces, sizeof(Piece) * 2 * scan_workers(~0ull >> 8, c->n_sms)));
+    CUDA_TRY(c, cudaMalloc(&c->contrib, sizeof(uint32_t) * 2 * scan_workers(~0ull >> 8, c->n_sms)));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_cnt, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
@@ -706,7 +706,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         sp.tile_end = ch.tile_end;
         sp.row_begin = ch.row_begin;
         sp.row_end = ch.row_end;
-        sp.groups = scan_groups(ch.row_end - ch.row_begin, c->n_sms);
+        sp.workers = scan_workers(ch.row_end - ch.row_begin, c->n_sms);
         sp.chunk_idx = (uint32_t)i;
         sp.totals_dev = c->totals_d + i;
         sp.totals_host = c->totals_map + i;
@@ -1054,7 +1054,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.contrib = c->contrib;
         sp.row_begin = 0;
         sp.row_end = c->n_rows;
-        sp.groups = scan_groups(c->n_rows, c->n_sms);
+        sp.workers = scan_workers(c->n_rows, c->n_sms);
         sp.tile_begin = 0;
         sp.tile_end = c->n_tiles;
         sp.page_size = P;

@@ -8,12 +8,10 @@
 namespace gcr {
 
 // ---------------------------------------------------------------------------
-// Work geometry.  A TILE is 64 KiB of virtual page space
-// scanned by one warp; a warp is 4 lane GROUPS of 8 lanes; a group owns a
-// 16 KiB SEGMENT of the tile and streams it as 128-byte rows (8 lanes x 16 B).
+// Work geometry.  K1 streams 512-byte ROWS (one per warp
+// instruction); a TILE is 64 KiB of page space, the unit of compaction/pack.
 constexpr uint32_t kTileBytes = 65536;
-constexpr uint32_t kGroupBytes = 16384;
-constexpr uint32_t kRowBytes = 128;
+constexpr uint32_t kRowBytes = 512;  // one warp row: 32 lanes x 16 B
 constexpr uint32_t kLog2Tile = 16;
 
 // Page classes (c.1 step 5).  cls[] bytes also carry kClsAllocStart on the
@@ -33,11 +31,11 @@ struct AllocDev {
     uint32_t n_tiles;
     uint32_t tail_len;  // length of its last page (== page_size if none is short)
     uint32_t z_tail;    // Z(tail_len) = CRC32C of tail_len zero bytes
-    uint64_t row0;      // global index of its first REAL 128-byte row
-    uint64_t n_rows;    // (n_pages-1)*P/128 + ceil(tail_len/128)
+    uint64_t row0;      // global index of its first REAL 512-byte row
+    uint64_t n_rows;    // (n_pages-1)*P/512 + ceil(tail_len/512)
 };
 
-// Partial raw register of a page cut by a K1 group boundary (folded by K1b).
+// Partial raw register of a page cut by a K1 warp-range boundary (folded by K1b).
 struct Piece {
     unsigned long long page;  // global page index, ~0 = empty slot
     uint32_t alloc;
@@ -60,21 +58,23 @@ struct ChunkTotals {
 // Every table maps a 32-bit register v to adv_d(v) = v * x^(8d) mod P as the
 // XOR of 4 byte-indexed entries: tab[k][e] = adv_d(e << 8k).
 struct CrcTables {
-    uint32_t braid[4][256];  // d = 128 (one row of 8 lanes x 16 B)
+    uint32_t braid[4][256];  // d = 512 (one row of 32 lanes x 16 B)
     uint32_t t4[4][256];     // d = 4   (word step for the lane raw16)
     uint32_t a16[4][256];    // d = 16  (lane tree, level 0)
     uint32_t a32[4][256];    // d = 32  (level 1)
     uint32_t a64[4][256];    // d = 64  (level 2)
-    uint32_t fold[14][4][256];  // d = 128 * 2^j: arbitrary row-distance folds of K1b
+    uint32_t a128[4][256];   // d = 128 (level 3)
+    uint32_t a256[4][256];   // d = 256 (level 4)
+    uint32_t fold[12][4][256];  // d = 512 * 2^j: arbitrary row-distance folds of K1b
 };
 
 struct ScanParams {
     const AllocDev *allocs;
     uint32_t n_allocs;
     uint64_t row_begin, row_end;   // chunk: global real rows (page aligned)
-    uint64_t groups;               // 8-lane groups sharing the rows equally
-    Piece *pieces;                 // 2 per group
-    uint32_t *contrib;             // 2 per group: piece contribution adv_{(Rp-vend)*128}(raw)
+    uint64_t workers;              // warps sharing the rows equally
+    Piece *pieces;                 // 2 per warp
+    uint32_t *contrib;             // 2 per warp: piece contribution adv_{(Rp-vend)*512}(raw)
     uint64_t tile_begin, tile_end; // chunk: tiles (compaction)
     uint32_t page_size, log2_page;
     uint32_t z_page;
@@ -111,7 +111,7 @@ struct ZeroDesc {
 int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t *page_alloc,
                             uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
                             cudaStream_t st);
-uint64_t scan_groups(uint64_t rows, int n_sms);
+uint64_t scan_workers(uint64_t rows, int n_sms);
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);
 int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, uint32_t *tile_off,
                      cudaStream_t st);

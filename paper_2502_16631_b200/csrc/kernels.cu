@@ -1,34 +1,43 @@
 // kernels.cu -- sm_100a kernels of the device-memory snapshot path
-// (DESIGN.md §4; SURVEY.md §8(a) rows A1-A9).
+// (DESIGN.md §5; SURVEY.md §8(a) rows A1-A9).
 //
-//  K0 build_page_table   A1: page -> allocation, tile -> allocation maps
-//  K1 scan               A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
-//                        all-zero test, dirty diff, class; tile summaries
-//  K1b fold_slices       pages > 64 KiB: fold the 64 KiB slice registers
-//  K2 tile_scan          A5: chunk-local exclusive scan of PRESENT bytes per tile (pack offsets);
-//                        chunk totals via CTA-aggregated atomics, published by K1b's last CTA
-//  K3 pagemap_*          A5: maximal runs -> CRIU-style pagemap entries
-//  K4 pack               A6: stream-compaction of PRESENT pages into staging
-//  K6 scatter            A8: staged image pieces -> allocation pages
-//  K7 zero_fill          A8: ZERO runs
+//  K0  build_page_table  A1: page -> allocation, tile -> allocation maps
+//  K1  scan              A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
+//                        all-zero test, dirty diff, class, tile counters
+//  K1b fold_contrib/final  pages cut by a warp's range boundary: fold the
+//                        partial registers; publish the chunk totals
+//  K2  tile_scan         A5: chunk-local exclusive scan of PRESENT bytes per
+//                        tile (the pack's destination offsets)
+//  K3  pagemap_*         A5: maximal runs -> CRIU-style pagemap entries
+//  K4  pack              A6: stream-compaction of PRESENT pages into staging
+//  K6  scatter           A8: staged image pieces -> allocation pages
+//  K7  zero_fill         A8: ZERO runs
 //
-// CRC32C arithmetic (DESIGN.md §4.2).  raw(x) is the register after x from 0
-// (GF(2)-linear); crc(x) = raw(x) ^ Z(|x|).  A group of 8 lanes streams its
-// segment as 128-byte rows; lane q owns words 4q..4q+3 of every row ("braids",
-// the zlib braided-CRC idea).  The braid register x_b evolves as
-// x_b <- adv_128(x_b) ^ w_b per row; after the last row the 128-byte block
-// Y = (x_0..x_31) satisfies raw(segment) = raw(Y).  Each lane folds its 16
-// bytes of Y (raw16) and a 3-level shuffle tree combines the lanes
-// (distances 16/32/64 B).  Segments combine with adv_16K / adv_32K and
-// 64 KiB slices of large pages with adv_64K.  Short (tail) pages are
-// processed as if front-padded with zeros to the full page, which leaves raw()
-// unchanged, so every page uses the same geometry and constants.
+// CRC32C arithmetic (DESIGN.md §5.3).  raw(x) is the register after x from 0
+// (GF(2)-linear); crc(x) = raw(x) ^ Z(|x|).  A warp streams 512-byte rows;
+// lane l owns words 4l..4l+3 of every row ("braids", the zlib braided-CRC
+// idea).  Braid register x_b evolves as x_b <- adv_512(x_b) ^ w_b per row;
+// after the last row of a page the 512-byte block Y = (x_0..x_127) satisfies
+// raw(page) = raw(Y).  Each lane folds its 16 bytes of Y (raw16) and a 5-level
+// shuffle tree combines the lanes (distances 16..256 B).  A short (tail) page
+// is processed as if front-padded with zeros to the full page -- leading
+// zeros leave raw() unchanged -- so every page uses the same geometry.
 //
-// adv_128 is evaluated with four 256-entry tables held LANE-PRIVATE in shared
+// adv_512 is evaluated with four 256-entry tables held LANE-PRIVATE in shared
 // memory (entry e of table k for lane l at byte (k>>1)*64K + e*256 +
 // (k&1)*128 + l*4, so the bank always equals the lane: conflict-free).  The
 // byte index is extracted and scaled in ONE prmt: prmt(x, l*4, 0x55k4) =
-// (byte_k(x) << 8) | l*4.  Per 4 data bytes: 4 PRMT + 4 LDS + 2 LOP3.
+// (byte_k(x) << 8) | l*4.  Per 4 data bytes: 4 PRMT + 4 LDS + 4 IMAD.IADD
+// (FMA pipe) + 2 LOP3.
+//
+// Work split: the chunk's REAL rows (the virtual padding of short pages is not
+// counted) are divided into equal contiguous ranges, one per warp, so every
+// warp streams the same bytes whatever the page or chunk size (no wave
+// quantization) and every page event is warp-uniform (no divergence).  A warp
+// streams its range continuously across page and allocation boundaries with
+// the next block of rows always in flight: a LOAD cursor walks contiguous
+// address runs, a PROCESS cursor finalizes pages.  Pages cut by a range
+// boundary leave PIECES that K1b folds.
 #include <cstdio>
 
 #include "gcr_internal.h"
@@ -38,9 +47,10 @@ namespace gcr {
 namespace {
 
 constexpr uint32_t kBraidSmem = 4u * 256u * 32u * 4u;  // 128 KiB
-constexpr uint32_t kSmallTables = 4;                   // t4 a16 a32 a64
+constexpr uint32_t kSmallTables = 6;                   // t4 a16 a32 a64 a128 a256
 constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u;
-constexpr uint32_t kFoldTables = 14;  // adv_{128 * 2^j}, j < 14: row distances < 16384 (P <= 2 MiB)
+constexpr uint32_t kFoldTables = 12;  // adv_{512 * 2^j}, j < 12: row distances < 4096 (P <= 2 MiB)
+constexpr uint32_t kLog2Row = 9;
 #ifndef GCR_SCAN_THREADS
 #define GCR_SCAN_THREADS 640
 #endif
@@ -49,8 +59,9 @@ constexpr int kScanThreads = GCR_SCAN_THREADS;
 #define GCR_SCAN_UNROLL 5
 #endif
 constexpr int kScanUnroll = GCR_SCAN_UNROLL;
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
-enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3 };
+enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3, kA128 = 4, kA256 = 5 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
@@ -74,7 +85,7 @@ __device__ __forceinline__ uint32_t lds_imm(uint32_t saddr) {
     return v;
 }
 
-// x -> adv_128(x) through the lane-private braid tables (shared address sb =
+// x -> adv_512(x) through the lane-private braid tables (shared address sb =
 // table base).  prmt(x, l*4, 0x55k4) = byte_k(x) << 8 | l*4 builds the scaled
 // index in one instruction; the table number lives in the ld.shared
 // immediate.  The base add runs on the FMA pipe (IMAD.IADD), which the
@@ -88,109 +99,33 @@ __device__ __forceinline__ uint32_t braid(uint32_t x, uint32_t lane4, uint32_t s
     return lds_imm<0>(i0) ^ lds_imm<128>(i1) ^ lds_imm<65536>(i2) ^ lds_imm<65536 + 128>(i3);
 }
 
-struct BraidCtx {
-    uint32_t lane4, sb;
-};
-
-// v -> adv_d(v) through an unreplicated 4x256 table (used once per segment).
+// v -> adv_d(v) through an unreplicated 4x256 table (used once per page).
 __device__ __forceinline__ uint32_t apply_tab(const uint32_t *tb, uint32_t v) {
     return tb[v & 255u] ^ tb[256u + ((v >> 8) & 255u)] ^ tb[512u + ((v >> 16) & 255u)] ^
            tb[768u + (v >> 24)];
 }
 
-__device__ __forceinline__ void row_step(BraidCtx cl, uint32_t (&x)[4], uint32_t &acc, const uint4 &w) {
+__device__ __forceinline__ void row_step(uint32_t lane4, uint32_t sb, uint32_t (&x)[4], uint32_t &acc,
+                                         const uint4 &w) {
     acc |= w.x | w.y | w.z | w.w;
-    x[0] = braid(x[0], cl.lane4, cl.sb) ^ w.x;
-    x[1] = braid(x[1], cl.lane4, cl.sb) ^ w.y;
-    x[2] = braid(x[2], cl.lane4, cl.sb) ^ w.z;
-    x[3] = braid(x[3], cl.lane4, cl.sb) ^ w.w;
+    x[0] = braid(x[0], lane4, sb) ^ w.x;
+    x[1] = braid(x[1], lane4, sb) ^ w.y;
+    x[2] = braid(x[2], lane4, sb) ^ w.z;
+    x[3] = braid(x[3], lane4, sb) ^ w.w;
 }
 
-// Stream rows [r0, R) of one segment.  gp is this lane's pointer for virtual
-// row 0 (gp + r*128 is its 16 bytes of row r); first_ok masks lanes of row r0
-// that lie in the virtual zero padding of a short page.
-template <int U>
-__device__ __forceinline__ void load_block(uint4 (&w)[U], const char *gp, int r, bool mask_first, bool first_ok) {
-    const char *p = gp + (size_t)r * kRowBytes;
-#pragma unroll
-    for (int u = 0; u < U; u++)
-        w[u] = (u > 0 || !mask_first || first_ok) ? ldg_stream(p + u * kRowBytes) : make_uint4(0, 0, 0, 0);
-}
-
-template <int U, bool kFirst>
-__device__ __forceinline__ void proc_block(BraidCtx cl, uint32_t (&x)[4], uint32_t &acc, const uint4 (&w)[U]) {
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-        if (kFirst && u == 0) {  // x = 0 before the first row: adv_128(0) ^ w == w
-            x[0] = w[0].x;
-            x[1] = w[0].y;
-            x[2] = w[0].z;
-            x[3] = w[0].w;
-            acc = w[0].x | w[0].y | w[0].z | w[0].w;
-        } else {
-            row_step(cl, x, acc, w[u]);
-        }
-    }
-}
-
-// Rows are consumed in blocks of U with the next block's loads in flight
-// (register double buffering): the scan is bound by bytes in flight per SM.
-template <int U>
-__device__ __forceinline__ void seg_stream(BraidCtx cl, const char *gp, int r0, int R, bool first_ok,
-                                           uint32_t (&x)[4], uint32_t &acc) {
-    const int nblk = (R - r0) / U;
-    int r = r0;
-    bool started = false;
-    if (nblk > 0) {
-        uint4 wa[U], wb[U];
-        load_block<U>(wa, gp, r, true, first_ok);
-        if (nblk > 1) load_block<U>(wb, gp, r + U, false, true);
-        proc_block<U, true>(cl, x, acc, wa);
-        r += U;
-        int b = 1;
-        for (; b + 1 < nblk; b += 2) {
-            load_block<U>(wa, gp, r + U, false, true);
-            proc_block<U, false>(cl, x, acc, wb);
-            r += U;
-            if (b + 2 < nblk) load_block<U>(wb, gp, r + U, false, true);
-            proc_block<U, false>(cl, x, acc, wa);
-            r += U;
-        }
-        if (b < nblk) {
-            proc_block<U, false>(cl, x, acc, wb);
-            r += U;
-        }
-        started = true;
-    }
-    for (; r < R; r++) {  // rows left over by a short (padded) page
-        const bool ok = started || r > r0 || first_ok;
-        const uint4 v = ok ? ldg_stream(gp + (size_t)r * kRowBytes) : make_uint4(0, 0, 0, 0);
-        if (!started && r == r0) {
-            x[0] = v.x;
-            x[1] = v.y;
-            x[2] = v.z;
-            x[3] = v.w;
-            acc = v.x | v.y | v.z | v.w;
-        } else {
-            row_step(cl, x, acc, v);
-        }
-    }
-}
-
-// raw() of the group's 128-byte Y block; valid in the group's lane q == 0.
-__device__ __forceinline__ uint32_t group_raw(const uint32_t *small, const uint32_t (&x)[4],
-                                              unsigned gmask) {
+// raw() of the warp's 512-byte Y block; valid in lane 0.
+__device__ __forceinline__ uint32_t warp_raw(const uint32_t *small, const uint32_t (&x)[4]) {
     const uint32_t *t4 = small + kT4 * 1024u;
     uint32_t v = apply_tab(t4, x[0]);
     v = apply_tab(t4, v ^ x[1]);
     v = apply_tab(t4, v ^ x[2]);
     v = apply_tab(t4, v ^ x[3]);
-    uint32_t o = __shfl_down_sync(gmask, v, 1, 8);
-    v = apply_tab(small + kA16 * 1024u, v) ^ o;
-    o = __shfl_down_sync(gmask, v, 2, 8);
-    v = apply_tab(small + kA32 * 1024u, v) ^ o;
-    o = __shfl_down_sync(gmask, v, 4, 8);
-    v = apply_tab(small + kA64 * 1024u, v) ^ o;
+#pragma unroll
+    for (int j = 0; j < 5; j++) {
+        const uint32_t o = __shfl_down_sync(kFull, v, 1 << j);
+        v = apply_tab(small + (kA16 + j) * 1024u, v) ^ o;
+    }
     return v;
 }
 
@@ -266,7 +201,7 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
     unsigned long long inc = v;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const unsigned long long o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        const unsigned long long o = __shfl_up_sync(kFull, inc, d);
         if (lane >= (uint32_t)d) inc += o;
     }
     if (lane == 31) warp_sums[warp] = inc;
@@ -276,7 +211,7 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
         unsigned long long s = lane < nw ? warp_sums[lane] : 0ull;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const unsigned long long o = __shfl_up_sync(0xFFFFFFFFu, s, d);
+            const unsigned long long o = __shfl_up_sync(kFull, s, d);
             if (lane >= (uint32_t)d) s += o;
         }
         if (lane < nw) warp_sums[lane] = s;  // inclusive
@@ -337,43 +272,163 @@ __global__ void __launch_bounds__(1024) k_tile_scan(TileInfo *ti, uint64_t tb, u
     }
 }
 
-// Allocation holding global real row r: 8-ary search by the 8 lanes of a
-// group (each round every lane probes one row0; one ballot narrows the range
-// 8x), so a group's start costs ~log8(n_allocs) dependent loads, not log2.
-__device__ __forceinline__ uint32_t alloc_of_row(const AllocDev *al, uint32_t n, uint64_t r, uint32_t q,
-                                                 uint32_t grp, unsigned gmask) {
+// Allocation holding global real row r: 32-ary search by the warp (each round
+// every lane probes one row0; one ballot narrows the range 32x).
+__device__ __forceinline__ uint32_t alloc_of_row(const AllocDev *al, uint32_t n, uint64_t r, uint32_t lane) {
     uint32_t lo = 0, hi = n;  // al[lo].row0 <= r < al[hi].row0 (al[n] = +inf)
     while (hi - lo > 1) {
-        const uint32_t step = (hi - lo + 7) / 8;
-        const uint32_t probe = lo + q * step;
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t probe = lo + lane * step;
         const bool le = probe < hi && __ldg(&al[probe].row0) <= r;
-        const unsigned b = (__ballot_sync(gmask, le) >> (8 * grp)) & 0xFFu;
-        const uint32_t qm = 31 - __clz(b);  // lane 0 (probe = lo) always qualifies
+        const uint32_t qm = 31 - __clz(__ballot_sync(kFull, le));  // lane 0 (probe = lo) always qualifies
         lo = lo + qm * step;
         hi = min(hi, lo + step);
     }
     return lo;
 }
 
-// K1.  The chunk's REAL rows (128-byte rows of page data; the virtual zero
-// padding in front of a short page is not counted) are split into equal
-// contiguous ranges, one per 8-lane group, so every group streams the same
-// number of bytes whatever the page size or the chunk size (no wave
-// quantization).  A group walks its range page by page: pages wholly inside
-// are finalized in place; a page cut by the range boundary yields a PIECE
-// (its raw register over the rows the group saw) that K1b folds.
+// Cached fields of one allocation (warp-uniform registers).
+struct AllocView {
+    uint64_t base, page0, tile0;
+    uint32_t n_pages, tail_len, z_tail, nfull;  // nfull: pages of length P
+};
+
+__device__ __forceinline__ AllocView load_alloc(const AllocDev *al, uint32_t P) {
+    AllocView v;
+    v.base = __ldg(&al->base);
+    v.page0 = __ldg(&al->page0);
+    v.tile0 = __ldg(&al->tile0);
+    v.n_pages = __ldg(&al->n_pages);
+    v.tail_len = __ldg(&al->tail_len);
+    v.z_tail = __ldg(&al->z_tail);
+    v.nfull = v.n_pages - (v.tail_len < P ? 1u : 0u);
+    return v;
+}
+
+// Both cursors walk the same sequence of PAGES; a block is the next
+// cnt = min(U, Rp - vr, rows left) rows, so a block never crosses a page (and
+// hence never an allocation or a short-page boundary): loads are U predicated
+// independent LDG.128 from one base, and a page ends only after a block.
+
+// LOAD cursor: this lane's pointer to the next row of its current page.
+struct LoadCursor {
+    const char *addr;
+    uint32_t a, pi, vr;
+    uint64_t base;
+    uint32_t n_pages, tail_len;
+    bool mask;  // next row is the first row of a short page and this lane's 16 B lie in its padding
+};
+
+__device__ __forceinline__ void lc_next_page(LoadCursor &lc, const AllocDev *allocs, uint32_t P, uint32_t lg,
+                                          uint32_t lane) {
+    if (++lc.pi == lc.n_pages) {
+        const AllocDev *al = allocs + (++lc.a);
+        lc.base = __ldg(&al->base);
+        lc.n_pages = __ldg(&al->n_pages);
+        lc.tail_len = __ldg(&al->tail_len);
+        lc.pi = 0;
+    }
+    const bool tail = lc.pi == lc.n_pages - 1 && lc.tail_len < P;
+    const uint32_t pad = tail ? P - lc.tail_len : 0u;
+    lc.vr = pad >> kLog2Row;
+    lc.addr = reinterpret_cast<const char *>(lc.base + ((uint64_t)lc.pi << lg)) - pad + (lc.vr << kLog2Row) +
+              lane * 16u;
+    lc.mask = (lc.vr << kLog2Row) + lane * 16u < pad;
+}
+
+template <int U>
+__device__ __forceinline__ void load_rows(uint4 (&w)[U], int &left, LoadCursor &lc, const AllocDev *allocs,
+                                          uint32_t P, uint32_t lg, uint32_t lane) {
+    const uint32_t Rp = P >> kLog2Row;
+    if (lc.vr == Rp) lc_next_page(lc, allocs, P, lg, lane);
+    const int cnt = min(min(U, left), (int)(Rp - lc.vr));
+    if (cnt == U && !lc.mask) {
+#pragma unroll
+        for (int u = 0; u < U; u++) w[u] = ldg_stream(lc.addr + (u << kLog2Row));
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (u < cnt) w[u] = (u == 0 && lc.mask) ? make_uint4(0, 0, 0, 0) : ldg_stream(lc.addr + (u << kLog2Row));
+    }
+    lc.addr += cnt << kLog2Row;
+    lc.vr += cnt;
+    lc.mask = false;
+    left -= cnt;
+}
+
+// PROCESS cursor: the page being digested and where this warp's part of it
+// started (vstart == r0: the warp saw the whole page).
+struct ProcCursor {
+    AllocView al;
+    uint32_t a, pi, vr, vstart, r0, slot;
+};
+
+__device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
+    const bool tail = pc.pi == pc.al.n_pages - 1 && pc.al.tail_len < P;
+    pc.r0 = tail ? (P - pc.al.tail_len) >> kLog2Row : 0u;
+    pc.vr = pc.r0;
+    pc.vstart = pc.r0;
+}
+
+// Page complete (vr == Rp): digest it (or leave a piece) and move on.
+__device__ __forceinline__ void page_end(const ScanParams &p, CtaTotals *ct, ProcCursor &pc, uint32_t (&x)[4],
+                                         uint32_t &acc, const uint32_t *small, uint64_t wid, uint32_t lane) {
+    const uint32_t P = p.page_size, lg = p.log2_page;
+    const uint32_t raw = warp_raw(small, x);
+    const bool nz = __any_sync(kFull, acc != 0);
+    const bool whole = pc.vstart == pc.r0;
+    if (lane == 0) {
+        const uint64_t g = pc.al.page0 + pc.pi;
+        if (whole) {
+            const bool tail = pc.pi == pc.al.n_pages - 1;
+            finalize_page(p, ct, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0,
+                          tail ? pc.al.tail_len : P, tail ? pc.al.z_tail : p.z_page, raw, nz);
+        } else {
+            p.pieces[2 * wid + pc.slot] = Piece{g, pc.a, pc.vstart, P >> kLog2Row, raw, nz ? 1u : 0u};
+        }
+    }
+    pc.slot += whole ? 0u : 1u;
+    x[0] = x[1] = x[2] = x[3] = 0u;
+    acc = 0u;
+    if (++pc.pi == pc.al.n_pages) {
+        if (++pc.a < p.n_allocs) pc.al = load_alloc(p.allocs + pc.a, P);
+        pc.pi = 0;
+    }
+    pc_set_page(pc, P);
+}
+
+// Digest the next block (the same cnt rows load_rows fetched into w).
+template <int U>
+__device__ __forceinline__ void process_rows(const ScanParams &p, CtaTotals *ct, ProcCursor &pc, const uint4 (&w)[U],
+                                             int &left, uint32_t (&x)[4], uint32_t &acc, const uint32_t *small,
+                                             uint32_t lane4, uint32_t sb, uint64_t wid, uint32_t lane) {
+    const uint32_t Rp = p.page_size >> kLog2Row;
+    const int cnt = min(min(U, left), (int)(Rp - pc.vr));
+    if (cnt == U) {
+#pragma unroll
+        for (int u = 0; u < U; u++) row_step(lane4, sb, x, acc, w[u]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (u < cnt) row_step(lane4, sb, x, acc, w[u]);
+    }
+    pc.vr += cnt;
+    left -= cnt;
+    if (pc.vr == Rp) page_end(p, ct, pc, x, acc, small, wid, lane);
+}
+
+// K1.
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
-    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
-    uint32_t *tabp = sm;
-    const uint32_t *small = tabp + kBraidSmem / 4;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
+    const uint32_t *small = sm + kBraidSmem / 4;
 
     // Stage the tables.  Each thread loads a few table words once (all loads
     // issued before any store) and writes the braid words to all 32 lane-private
     // replicas: word (k>>1)*16384 + e*64 + (k&1)*32 + l.
     {
         const uint32_t *gb = &p.tables->braid[0][0];
-        const uint32_t *gs = &p.tables->t4[0][0];  // t4, a16, a32, a64 are contiguous
+        const uint32_t *gs = &p.tables->t4[0][0];  // t4, a16, ..., a256 are contiguous
         constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
         constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
         uint32_t bv[kPer], sv[kPerS];
@@ -392,13 +447,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             const uint32_t ke = threadIdx.x + j * kScanThreads;
             if (ke < 1024u) {
                 const uint32_t k = ke >> 8, e = ke & 255u;
-                uint4 *dst = reinterpret_cast<uint4 *>(tabp + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
+                uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
                 const uint4 v4 = make_uint4(bv[j], bv[j], bv[j], bv[j]);
 #pragma unroll
                 for (int l = 0; l < 8; l++) dst[l] = v4;
             }
         }
-        uint32_t *ss = tabp + kBraidSmem / 4;
+        uint32_t *ss = sm + kBraidSmem / 4;
 #pragma unroll
         for (uint32_t j = 0; j < kPerS; j++) {
             const uint32_t i = threadIdx.x + j * kScanThreads;
@@ -410,72 +465,80 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t grp = lane >> 3, q = lane & 7u;
-    const BraidCtx cl{lane * 4u, tab};
-    const unsigned gmask = 0xFFu << (8u * grp);
-    const uint64_t gid = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4u + grp;
-    if (gid < p.groups) {
+    const uint32_t lane4 = lane * 4u;
+    const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (wid < p.workers) {
         const uint32_t P = p.page_size, lg = p.log2_page;
-        const int Rp = (int)(P >> 7);  // virtual rows per page
+        const uint32_t Rp = P >> kLog2Row;
         const uint64_t rows = p.row_end - p.row_begin;
-        uint64_t r = p.row_begin + rows * gid / p.groups;
-        const uint64_t rend = p.row_begin + rows * (gid + 1) / p.groups;
-        uint32_t a = alloc_of_row(p.allocs, p.n_allocs, r, q, grp, gmask);
-        int slot = 0;
-        Piece *pc = p.pieces + 2 * gid;
-        while (r < rend) {
-            const AllocDev *al = p.allocs + a;
-            const uint64_t row0 = __ldg(&al->row0), rows_a = __ldg(&al->n_rows);
-            if (r >= row0 + rows_a) {  // range continues in the next allocation
-                a++;
-                continue;
-            }
-            const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), tile0 = __ldg(&al->tile0);
-            const uint32_t n_pages = __ldg(&al->n_pages), tail_len = __ldg(&al->tail_len);
-            const uint64_t lr = r - row0;
-            uint64_t pi = lr >> (lg - 7);
-            if (pi >= n_pages) pi = n_pages - 1;
-            const bool tail = pi == (uint64_t)n_pages - 1;
-            const uint32_t len = tail ? tail_len : P;
-            const uint32_t pad = P - len;
-            const int r0 = (int)(pad >> 7);
-            const int vr = (int)(lr - (pi << (lg - 7))) + r0;
-            const uint64_t left = rend - r;
-            const int vend = (uint64_t)(Rp - vr) <= left ? Rp : vr + (int)left;
-            const char *gp = reinterpret_cast<const char *>(base + (pi << lg)) - pad + q * 16u;
-            const bool first_ok = vr > r0 || ((uint32_t)r0 * kRowBytes + q * 16u) >= pad;
-            uint32_t x[4], acc;
-            seg_stream<kScanUnroll>(cl, gp, vr, vend, first_ok, x, acc);
-            const uint32_t raw = group_raw(small, x, gmask);
-            const bool nz = (__ballot_sync(gmask, acc != 0) & gmask) != 0;
-            if (q == 0) {
-                if (vr == r0 && vend == Rp) {
-                    finalize_page(p, &ct, page0 + pi, tile_of_page(tile0, pi, P, lg), pi == 0, len,
-                                  tail ? __ldg(&al->z_tail) : p.z_page, raw, nz);
-                } else {
-                    pc[slot] = Piece{page0 + pi, a, (uint32_t)vr, (uint32_t)vend, raw, nz ? 1u : 0u};
-                    slot++;
-                }
-            }
-            slot = __shfl_sync(gmask, slot, 0, 8);
-            r += (uint64_t)(vend - vr);
+        const uint64_t r = p.row_begin + rows * wid / p.workers;
+        const uint64_t rend = p.row_begin + rows * (wid + 1) / p.workers;
+        const uint32_t a = alloc_of_row(p.allocs, p.n_allocs, r, lane);
+        // position of row r: a full page, or the short tail page
+        ProcCursor pc;
+        pc.a = a;
+        pc.al = load_alloc(p.allocs + a, P);
+        pc.slot = 0;
+        const uint64_t lr = r - __ldg(&p.allocs[a].row0);
+        uint32_t pad0 = 0;  // padding of the first page (non-zero only for a short tail page)
+        if (lr < ((uint64_t)pc.al.nfull << (lg - kLog2Row))) {
+            pc.pi = (uint32_t)(lr >> (lg - kLog2Row));
+            pc.r0 = 0;
+            pc.vr = (uint32_t)(lr & (Rp - 1));
+        } else {
+            pc.pi = pc.al.n_pages - 1;
+            pad0 = P - pc.al.tail_len;
+            pc.r0 = pad0 >> kLog2Row;
+            pc.vr = (uint32_t)(lr - ((uint64_t)pc.al.nfull << (lg - kLog2Row))) + pc.r0;
         }
-        if (q == 0)
-            for (; slot < 2; slot++) pc[slot] = Piece{~0ull, 0u, 0u, 0u, 0u, 0u};
+        pc.vstart = pc.vr;
+        LoadCursor lc;
+        lc.a = a;
+        lc.pi = pc.pi;
+        lc.vr = pc.vr;
+        lc.base = pc.al.base;
+        lc.n_pages = pc.al.n_pages;
+        lc.tail_len = pc.al.tail_len;
+        lc.addr = reinterpret_cast<const char *>(pc.al.base + ((uint64_t)pc.pi << lg)) - pad0 +
+                  (pc.vr << kLog2Row) + lane * 16u;
+        lc.mask = pc.vr == pc.r0 && (pc.r0 << kLog2Row) + lane * 16u < pad0;
+
+        constexpr int U = kScanUnroll;
+        int to_load = (int)(rend - r), to_proc = to_load;
+        uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u;
+        uint4 wa[U], wb[U];
+        load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
+        while (to_proc > 0) {
+            if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane);
+            process_rows<U>(p, &ct, pc, wa, to_proc, x, acc, small, lane4, sb, wid, lane);
+            if (to_proc <= 0) break;
+            if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
+            process_rows<U>(p, &ct, pc, wb, to_proc, x, acc, small, lane4, sb, wid, lane);
+        }
+        // the range ended inside a page: leave a piece
+        if (pc.vr != pc.vstart) {
+            const uint32_t raw = warp_raw(small, x);
+            const bool nz = __any_sync(kFull, acc != 0);
+            if (lane == 0)
+                p.pieces[2 * wid + pc.slot] = Piece{pc.al.page0 + pc.pi, pc.a, pc.vstart, pc.vr, raw, nz ? 1u : 0u};
+            pc.slot++;
+        }
+        if (lane == 0)
+            for (uint32_t s = pc.slot; s < 2; s++) p.pieces[2 * wid + s] = Piece{~0ull, 0u, 0u, 0u, 0u, 0u};
     }
     cta_totals_flush(p, &ct);
 }
 
-// K1b: fold the pieces of pages cut by group boundaries, in two launches.
+// K1b: fold the pieces of pages cut by warp-range boundaries, in two launches.
 // (a) every piece, in parallel: its contribution to its page's register,
-//     adv_{(Rp - vend) * 128}(raw), by the binary expansion of the row
-//     distance through tables fold[j] = adv_{128 * 2^j} (d < 2^14 rows).
+//     adv_{(Rp - vend) * 512}(raw), by the binary expansion of the row
+//     distance through tables fold[j] = adv_{512 * 2^j} (d < 2^12 rows).
 __global__ void __launch_bounds__(256) k_fold_contrib(const ScanParams p) {
     extern __shared__ uint32_t fsm[];  // kFoldTables x 1024 words
     for (uint32_t i = threadIdx.x; i < kFoldTables * 1024u; i += blockDim.x) fsm[i] = __ldg(&p.tables->fold[0][0][0] + i);
     __syncthreads();
-    const uint32_t Rp = p.page_size >> 7;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * p.groups;
+    const uint32_t Rp = p.page_size >> kLog2Row;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * p.workers;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const Piece pc = p.pieces[i];
         if (pc.page == ~0ull) continue;
@@ -486,16 +549,16 @@ __global__ void __launch_bounds__(256) k_fold_contrib(const ScanParams p) {
     }
 }
 
-// (b) the group holding a page's FIRST piece owns it: XOR of the contributions
-//     of its piece and of the HEAD pieces of the following groups, then c.1
+// (b) the warp holding a page's FIRST piece owns it: XOR of the contributions
+//     of its piece and of the HEAD pieces of the following warps, then c.1
 //     steps 3-5.  Its last CTA publishes the chunk totals.
 __global__ void __launch_bounds__(256) k_fold_final(const ScanParams p) {
     __shared__ CtaTotals ct;
     cta_totals_init(&ct);
     __syncthreads();
     const uint32_t P = p.page_size, lg = p.log2_page;
-    const uint32_t Rp = P >> 7;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.groups;
+    const uint32_t Rp = P >> kLog2Row;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.workers;
          j += (uint64_t)gridDim.x * blockDim.x) {
         for (int s = 1; s >= 0; s--) {
             const Piece pc = p.pieces[2 * j + s];
@@ -505,12 +568,12 @@ __global__ void __launch_bounds__(256) k_fold_final(const ScanParams p) {
             const uint32_t n_pages = __ldg(&al->n_pages);
             const bool tail = pi == (uint64_t)n_pages - 1;
             const uint32_t len = tail ? __ldg(&al->tail_len) : P;
-            const uint32_t r0 = (P - len) >> 7;
+            const uint32_t r0 = (P - len) >> kLog2Row;
             if (pc.vr_begin != r0) continue;  // not the page's first piece
             uint32_t raw = p.contrib[2 * j + s];
             bool nz = pc.nz != 0;
             uint32_t end = pc.vr_end;
-            for (uint64_t k = j + 1; end < Rp && k < p.groups; k++) {
+            for (uint64_t k = j + 1; end < Rp && k < p.workers; k++) {
                 raw ^= p.contrib[2 * k];
                 nz |= p.pieces[2 * k].nz != 0;
                 end = p.pieces[2 * k].vr_end;
@@ -725,12 +788,12 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
     return launched(1);
 }
 
-uint64_t scan_groups(uint64_t rows, int n_sms) {
-    // every group streams >= 32 rows (4 KiB); at most all groups of a full grid
-    const uint64_t full = (uint64_t)n_sms * (kScanThreads / 32) * 4;
-    uint64_t g = rows / 32;
-    if (g < 1) g = 1;
-    return g < full ? g : full;
+uint64_t scan_workers(uint64_t rows, int n_sms) {
+    // every warp streams >= 8 rows (4 KiB); at most all warps of a full grid
+    const uint64_t full = (uint64_t)n_sms * (kScanThreads / 32);
+    uint64_t w = rows / 8;
+    if (w < 1) w = 1;
+    return w < full ? w : full;
 }
 
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
@@ -745,8 +808,8 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
         attr_done[dev] = true;
     }
     if (p.row_end == p.row_begin) return 0;
-    const uint64_t gpb = (kScanThreads / 32) * 4;
-    const uint64_t grid = (p.groups + gpb - 1) / gpb;
+    const uint64_t wpb = kScanThreads / 32;
+    const uint64_t grid = (p.workers + wpb - 1) / wpb;
     k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
     static bool fold_attr[64] = {};
     if (dev < 64 && !fold_attr[dev]) {
@@ -755,10 +818,10 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
             return -1;
         fold_attr[dev] = true;
     }
-    uint64_t gc = (2 * p.groups + 255) / 256;
+    uint64_t gc = (2 * p.workers + 255) / 256;
     if (gc > (uint64_t)n_sms) gc = n_sms;
     k_fold_contrib<<<(unsigned)gc, 256, kFoldTables * 4096u, st>>>(p);
-    uint64_t g2 = (p.groups + 255) / 256;
+    uint64_t g2 = (p.workers + 255) / 256;
     if (g2 > (uint64_t)n_sms * 4) g2 = n_sms * 4;
     k_fold_final<<<(unsigned)g2, 256, 0, st>>>(p);
     return launched(3);
