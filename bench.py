@@ -178,7 +178,8 @@ def run_ours(args):
     ts = w.materialize()
     torch.cuda.synchronize()
     ctx = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20,
-                      n_copy_streams=args.streams)
+                      n_copy_streams=args.streams,
+                      direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
     for t in ts:
         ctx.register_tensor(t)
     ctx.reserve_host(w.total_bytes + (256 << 20))
@@ -279,7 +280,8 @@ def run_ours(args):
         "data": "synthetic (seeded counter-based generator; training-state-shaped fp32/bf16 values)",
         "config": {"workload": _workload_desc(args.config, w), "registered_bytes_per_rank": R,
                    "allocations": len(w.allocs), "page_size": w.page_size, "chunk_bytes": args.chunk_mb << 20,
-                   "copy_streams": args.streams, "parallelism": f"independent ranks x{world} (gloo control plane)",
+                   "copy_streams": args.streams, "direct_min_bytes": int(args.direct_min_mb * (1 << 20)) if args.direct_min_mb >= 0 else None,
+                   "parallelism": f"independent ranks x{world} (gloo control plane)",
                    "l2": "inputs larger than L2 (registered state >> 126 MB; no flush needed)"},
         "per_gpu": {"checkpoint_GBps": round(ck_gbs, 3), "restore_GBps": round(rs_gbs, 3),
                     "roundtrip_GBps": round(R * K / t_dev / 1e9, 3),
@@ -389,9 +391,14 @@ def main():
     ap.add_argument("--gib", type=int, default=None, help="C4/C5 GiB per GPU")
     ap.add_argument("--chunk-mb", type=int, default=256)
     ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--direct-min-mb", type=float, default=None,
+                    help="runs >= this go by direct DMA (default: the library's); -1 = always staged")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.direct_min_mb is None:
+        from paper_2502_16631_b200 import gcr as _g
+        args.direct_min_mb = _g.default_config().direct_min_bytes / (1 << 20)
     if args.gib is None:
         args.gib = {"C4": 40, "C5": 16}.get(args.config, 16)
     if args.impl == "reference":

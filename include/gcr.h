@@ -83,6 +83,16 @@ typedef struct {
                                  (reading R-11); 0 = no verify pass (then restore never returns
                                  GCR_E_VERIFY) */
     uint64_t lock_timeout_ms; /* default 10000 -- "10 seconds by default" (R-12) */
+    uint64_t direct_min_bytes;/* PRESENT runs of at least this many bytes move by DMA directly
+                                 between the allocation and the pinned image (no staging, no
+                                 pack/scatter kernel); shorter runs are packed (checkpoint) or
+                                 scattered (restore) through the staging slots.  Checkpoint runs
+                                 are built from whole 64 KiB tiles whose pages are all PRESENT
+                                 (a tile mixing classes is always packed); restore runs are
+                                 pagemap runs.  Default 16 MiB (shorter DMAs lose link
+                                 efficiency); 0 = every eligible run direct;
+                                 UINT64_MAX = every run staged.  The image bytes are identical
+                                 either way. */
 } gcr_config;
 
 /* Statistics of the most recent lock / checkpoint / restore / unlock
@@ -111,6 +121,10 @@ typedef struct {
     uint64_t restore_h2d_bytes;                  /* last restore: image bytes copied H2D */
     uint64_t kernel_launches;                    /* cumulative: every kernel libgcr launched */
     uint64_t pinned_alloc_ns;                    /* cumulative: time spent in cudaHostAlloc */
+    uint64_t direct_bytes;                       /* last checkpoint: image bytes drained straight from
+                                                    the allocations (the rest was packed) */
+    uint64_t restore_direct_bytes;               /* last restore: image bytes copied straight into
+                                                    the allocations (the rest was scattered) */
 } gcr_stats;
 
 /* gcr_image_hdr -- 96 bytes, offsets: magic 0, version 8, page_size 12,

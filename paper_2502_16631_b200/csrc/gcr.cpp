@@ -197,6 +197,8 @@ struct gcr_ctx {
     unsigned *done_d = nullptr;                               // per-chunk CTA tickets
     unsigned long long *misc_d = nullptr, *misc_h = nullptr;  // [0] n_entries, [1] verify count, [2] first bad
     unsigned long long *nent_h = nullptr, *nent_map = nullptr;  // mapped pinned n_entries
+    TileRec *tile_rec_h = nullptr, *tile_rec_map = nullptr;     // mapped pinned per-tile records
+    uint8_t *pack_flags_h = nullptr, *pack_flags_d = nullptr;   // per-tile: packed (1) or direct (0)
     uint32_t z_page = 0;
 
     // restore descriptor buffers (grow on demand)
@@ -259,12 +261,16 @@ bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P
 void free_layout(gcr_ctx *c) {
     void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
                     c->tile_off, c->pieces, c->contrib, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
-                    c->entries_d, c->totals_d, c->misc_d, c->done_d};
+                    c->entries_d, c->totals_d, c->misc_d, c->done_d, c->pack_flags_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->totals_h) cudaFreeHost(c->totals_h);
     if (c->misc_h) cudaFreeHost(c->misc_h);
     if (c->nent_h) cudaFreeHost(c->nent_h);
+    if (c->tile_rec_h) cudaFreeHost(c->tile_rec_h);
+    if (c->pack_flags_h) cudaFreeHost(c->pack_flags_h);
+    c->tile_rec_h = c->tile_rec_map = nullptr;
+    c->pack_flags_h = c->pack_flags_d = nullptr;
     c->nent_h = c->nent_map = nullptr;
     c->done_d = nullptr;
     c->totals_map = nullptr;
@@ -372,6 +378,10 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->done_d, sizeof(unsigned) * nch));
     CUDA_TRY(c, cudaMemset(c->done_d, 0, sizeof(unsigned) * nch));
     CUDA_TRY(c, cudaHostAlloc(&c->nent_h, 64, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostAlloc(&c->tile_rec_h, sizeof(TileRec) * t, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->tile_rec_map), c->tile_rec_h, 0));
+    CUDA_TRY(c, cudaHostAlloc(&c->pack_flags_h, t, cudaHostAllocDefault));
+    CUDA_TRY(c, cudaMalloc(&c->pack_flags_d, t));
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->nent_map), c->nent_h, 0));
     CUDA_TRY(c, cudaMalloc(&c->misc_d, 8 * 4));
     CUDA_TRY(c, cudaHostAlloc(&c->misc_h, 8 * 4, cudaHostAllocDefault));
@@ -479,6 +489,7 @@ gcr_status gcr_config_default(gcr_config *out) {
     out->n_staging_slots = 0;
     out->verify = 1;
     out->lock_timeout_ms = 10000;
+    out->direct_min_bytes = 16ull << 20;
     return GCR_OK;
 }
 
@@ -699,7 +710,10 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
     cudaEvent_t t0 = c->ev();
     CUDA_TRY(c, cudaEventRecord(t0, c->compute));
-    // Enqueue every chunk's scan + compaction on the compute stream up front.
+    // Enqueue every chunk's scan (K1 + K1b) and compaction (K2) on the compute
+    // stream up front.  K1b publishes the chunk totals and K2 the per-tile
+    // records straight into mapped pinned memory, so planning the drain never
+    // waits on a DMA queued behind the previous chunk's drain.
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         sp.tile_begin = ch.tile_begin;
@@ -712,17 +726,28 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         sp.totals_host = c->totals_map + i;
         k1s[i] = c->ev();
         k1e[i] = c->ev();
+        tot[i] = c->ev();
         CUDA_TRY(c, cudaEventRecord(k1s[i], c->compute));
-        // K1 (+K1b) -- its last CTA runs the chunk compaction K2 and stores the
-        // totals into mapped pinned memory: no DMA on the drain's copy engines.
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
         CUDA_TRY(c, cudaEventRecord(k1e[i], c->compute));
-        tot[i] = k1e[i];
+        LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off,
+                                       c->tile_rec_map + ch.tile_begin, c->compute));
+        CUDA_TRY(c, cudaEventRecord(tot[i], c->compute));
     }
-    // Drain: as each chunk's totals land, pack it into its slot and copy out.
+    // Drain: as each chunk's records land, plan it -- runs of fully PRESENT
+    // tiles of at least direct_min_bytes go straight from the allocation to the
+    // pinned image; the other PRESENT tiles are packed (K4) into the chunk's
+    // staging slot and copied out in contiguous ranges.
     uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0;
     Clock::time_point drain0;
     const size_t S = c->copy.size();
+    const uint64_t direct_min = c->cfg.direct_min_bytes;
+    uint64_t direct_bytes = 0, staged_bytes = 0;
+    struct Run {
+        uint64_t src, off, bytes, t_first, t_last;
+    };
+    std::vector<Run> direct;
+    std::vector<std::pair<uint64_t, uint64_t>> staged;  // chunk-local image ranges [lo, hi)
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         CUDA_TRY(c, cudaEventSynchronize(tot[i]));
@@ -734,23 +759,101 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         n_present += T.n_present;
         n_zero += T.n_zero;
         n_parent += T.n_parent;
+        if (base + T.image_bytes > R) return fail(c, GCR_E_CUDA, "checkpoint: image larger than registry");
+        // ---- plan (host walk of the chunk's tiles) ----
+        direct.clear();
+        staged.clear();
+        uint8_t *flags = c->pack_flags_h + ch.tile_begin;
+        bool any_staged = false;
+        if (T.image_bytes) {
+            std::memset(flags, 0, ch.tile_end - ch.tile_begin);
+            Run run{0, 0, 0, 0, 0};
+            bool open = false;
+            auto stage_tiles = [&](uint64_t t_first, uint64_t t_last) {
+                for (uint64_t t = t_first; t <= t_last; t++) flags[t - ch.tile_begin] = 1;
+                any_staged = true;
+            };
+            auto close = [&]() {
+                if (!open) return;
+                if (run.bytes >= direct_min) direct.push_back(run);
+                else stage_tiles(run.t_first, run.t_last);
+                open = false;
+            };
+            size_t a = 0;
+            {
+                size_t lo = 0, hi = c->allocs_h.size();
+                while (hi - lo > 1) {
+                    size_t mid = (lo + hi) / 2;
+                    if (c->allocs_h[mid].tile0 <= ch.tile_begin) lo = mid; else hi = mid;
+                }
+                a = lo;
+            }
+            const volatile uint32_t *rec = reinterpret_cast<const volatile uint32_t *>(c->tile_rec_h + ch.tile_begin);
+            for (uint64_t t = ch.tile_begin; t < ch.tile_end; t++) {
+                while (t >= c->allocs_h[a].tile0 + c->allocs_h[a].n_tiles) a++;
+                const uint2 r = make_uint2(rec[2 * (t - ch.tile_begin)], rec[2 * (t - ch.tile_begin) + 1]);
+                if (r.x == 0) continue;
+                const AllocDev &al = c->allocs_h[a];
+                const uint64_t lt = t - al.tile0;
+                uint64_t src, span;
+                if (P <= kTileBytes) {
+                    src = al.base + lt * kTileBytes;
+                    span = std::min<uint64_t>(kTileBytes, al.bytes - lt * kTileBytes);
+                } else {  // anchor tile of a page: the whole page
+                    const uint64_t pi = lt / (P / kTileBytes);
+                    src = al.base + pi * P;
+                    span = pi == al.n_pages - 1 ? al.tail_len : P;
+                }
+                // last tile the page(s) cover: the anchor itself, or all 64 KiB slices of a big page
+                const uint64_t t_end = P <= kTileBytes ? t : t + P / kTileBytes - 1;
+                if (r.x == span) {  // every page of the tile PRESENT: contiguous in memory and in the image
+                    if (open && run.src + run.bytes == src && run.off + run.bytes == r.y) {
+                        run.bytes += span;
+                        run.t_last = t_end;
+                    } else {
+                        close();
+                        run = Run{src, r.y, span, t, t_end};
+                        open = true;
+                    }
+                } else {
+                    close();
+                    stage_tiles(t, t);
+                }
+            }
+            close();
+            if (any_staged) {  // contiguous image ranges of consecutive staged tiles
+                for (uint64_t t = ch.tile_begin; t < ch.tile_end; t++) {
+                    if (!flags[t - ch.tile_begin]) continue;
+                    const uint2 r = make_uint2(rec[2 * (t - ch.tile_begin)], rec[2 * (t - ch.tile_begin) + 1]);
+                    if (!staged.empty() && staged.back().second == r.y) staged.back().second += r.x;
+                    else staged.emplace_back(r.y, (uint64_t)r.y + r.x);
+                }
+            }
+        }
+        // ---- execute on copy stream i mod S ----
         cudaStream_t cs = c->copy[i % S];
         if (i == 0) drain0 = Clock::now();
         CUDA_TRY(c, cudaStreamWaitEvent(cs, tot[i], 0));
         pks[i] = c->ev();
         pke[i] = c->ev();
         CUDA_TRY(c, cudaEventRecord(pks[i], cs));
-        if (T.image_bytes) {
-            LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off, cs));
+        if (any_staged) {
+            CUDA_TRY(c, cudaMemcpyAsync(c->pack_flags_d + ch.tile_begin, flags, ch.tile_end - ch.tile_begin,
+                                        cudaMemcpyHostToDevice, cs));
             LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, c->tile_off, ch.tile_begin, ch.tile_end, P,
-                                      c->lg, c->slots[i % S], c->n_sms, cs));
+                                      c->lg, c->slots[i % S], c->pack_flags_d + ch.tile_begin, c->n_sms, cs));
         }
-        if (!T.image_bytes)  // nothing to pack, but the tile counters must be re-zeroed
-            LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off, cs));
         CUDA_TRY(c, cudaEventRecord(pke[i], cs));
-        if (base + T.image_bytes > R) return fail(c, GCR_E_CUDA, "checkpoint: image larger than registry");
-        if (T.image_bytes)
-            CUDA_TRY(c, cudaMemcpyAsync(img->data + base, c->slots[i % S], T.image_bytes, cudaMemcpyDeviceToHost, cs));
+        for (const auto &rg : staged) {
+            CUDA_TRY(c, cudaMemcpyAsync(img->data + base + rg.first, c->slots[i % S] + rg.first, rg.second - rg.first,
+                                        cudaMemcpyDeviceToHost, cs));
+            staged_bytes += rg.second - rg.first;
+        }
+        for (const Run &rn : direct) {
+            CUDA_TRY(c, cudaMemcpyAsync(img->data + base + rn.off, reinterpret_cast<const void *>(rn.src), rn.bytes,
+                                        cudaMemcpyDeviceToHost, cs));
+            direct_bytes += rn.bytes;
+        }
         if (ch.page_end > ch.page_begin)
             CUDA_TRY(c, cudaMemcpyAsync(img->digests + ch.page_begin, Dnew + ch.page_begin,
                                         4 * (ch.page_end - ch.page_begin), cudaMemcpyDeviceToHost, cs));
@@ -758,6 +861,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         CUDA_TRY(c, cudaEventRecord(dde[i], cs));
         base += T.image_bytes;
     }
+    if (direct_bytes + staged_bytes != base) return fail(c, GCR_E_CUDA, "checkpoint: drain plan does not cover the image");
+    st.direct_bytes = direct_bytes;
     // K3 pagemap over all pages (maximal runs, independent of chunking).
     auto pm0 = c->ev(), pm1 = c->ev();
     CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
@@ -940,23 +1045,35 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
     const uint64_t slot = c->cfg.chunk_bytes;
     const size_t S = c->copy.size();
 
-    // ---- descriptors for every image (host walk of the pagemaps) ----------
-    struct ImgPlan {
-        uint64_t sc_begin, sc_end, z_begin, z_end;
-        std::vector<uint64_t> chunk_desc;  // scatter desc index where chunk j starts (size nchunks+1)
+    // ---- plan every image (host walk of the pagemaps) ----------------------
+    // In image-data order, a PRESENT run of at least direct_min_bytes is one
+    // DIRECT item (H2D from the pinned image straight into the allocation); a
+    // maximal sequence of consecutive shorter runs (contiguous in the image) up
+    // to one slot is a STAGED item (one H2D into a staging slot + K6 scatter).
+    struct Item {
+        bool direct;
+        uint64_t img_off, bytes, dst;  // direct: dst device address
+        uint64_t d_begin, d_end;       // staged: scatter descriptors
     };
+    struct ImgPlan {
+        std::vector<Item> items;
+        uint64_t z_begin, z_end;
+    };
+    const uint64_t direct_min = c->cfg.direct_min_bytes;
     std::vector<ImgPlan> plans(n);
     std::vector<ScatterDesc> sdesc;
     std::vector<ZeroDesc> zdesc;
-    uint64_t h2d_bytes = 0;
+    uint64_t h2d_bytes = 0, direct_bytes = 0;
     for (uint32_t k = 0; k < n; k++) {
         const gcr_image *im = chain[k];
         ImgPlan &pl = plans[k];
-        pl.sc_begin = sdesc.size();
         pl.z_begin = zdesc.size();
-        const uint64_t nchunks = (im->hdr.image_bytes + slot - 1) / slot;
-        pl.chunk_desc.assign(nchunks + 1, 0);
-        uint64_t cursor = 0, e = 0, next_chunk = 0;
+        uint64_t cursor = 0, e = 0;
+        bool group_open = false;
+        auto close_group = [&]() {
+            if (group_open) pl.items.back().d_end = sdesc.size();
+            group_open = false;
+        };
         for (uint32_t a = 0; a < im->hdr.n_allocs; a++) {
             const uint64_t m = pages_of(c->reg[a].bytes, P);
             uint64_t p = 0;
@@ -967,15 +1084,31 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
                                              : (uint64_t)pe.nr_pages * P;
                 uint64_t dst = c->reg[a].dptr + p * P;  // remapped by allocation index (R-14)
                 if (pe.flags == GCR_PE_PRESENT) {
-                    while (bytes) {
-                        const uint64_t j = cursor / slot;
-                        while (next_chunk <= j) pl.chunk_desc[next_chunk++] = sdesc.size();
-                        const uint64_t room = (j + 1) * slot - cursor;
-                        const uint64_t piece = std::min(std::min(bytes, room), kPieceBytes);
-                        sdesc.push_back(ScatterDesc{dst, cursor - j * slot, piece});
-                        dst += piece;
-                        cursor += piece;
-                        bytes -= piece;
+                    if (bytes >= direct_min) {
+                        close_group();
+                        while (bytes) {  // pieces of at most one slot keep the copy streams busy
+                            const uint64_t piece = std::min(bytes, slot);
+                            pl.items.push_back(Item{true, cursor, piece, dst, 0, 0});
+                            direct_bytes += piece;
+                            dst += piece;
+                            cursor += piece;
+                            bytes -= piece;
+                        }
+                    } else {
+                        while (bytes) {
+                            if (group_open && pl.items.back().bytes + bytes > slot) close_group();
+                            if (!group_open) {
+                                pl.items.push_back(Item{false, cursor, 0, 0, sdesc.size(), 0});
+                                group_open = true;
+                            }
+                            Item &g = pl.items.back();
+                            const uint64_t piece = std::min(std::min(bytes, kPieceBytes), slot - g.bytes);
+                            sdesc.push_back(ScatterDesc{dst, cursor - g.img_off, piece});
+                            g.bytes += piece;
+                            dst += piece;
+                            cursor += piece;
+                            bytes -= piece;
+                        }
                     }
                 } else if (pe.flags == GCR_PE_ZERO) {
                     while (bytes) {
@@ -988,8 +1121,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
                 p = last;
             }
         }
-        while (next_chunk <= nchunks) pl.chunk_desc[next_chunk++] = sdesc.size();
-        pl.sc_end = sdesc.size();
+        close_group();
         pl.z_end = zdesc.size();
         h2d_bytes += im->hdr.image_bytes;
     }
@@ -1011,15 +1143,18 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         cudaEvent_t start = c->ev();
         CUDA_TRY(c, cudaEventRecord(start, c->compute));
         for (size_t i = 0; i < S; i++) CUDA_TRY(c, cudaStreamWaitEvent(c->copy[i], start, 0));
-        const uint64_t nchunks = pl.chunk_desc.size() - 1;
-        for (uint64_t j = 0; j < nchunks; j++) {
+        for (size_t j = 0; j < pl.items.size(); j++) {
+            const Item &it = pl.items[j];
             cudaStream_t cs = c->copy[j % S];
-            const uint64_t lo = j * slot, hi = std::min(im->hdr.image_bytes, lo + slot);
-            CUDA_TRY(c, cudaMemcpyAsync(c->slots[j % S], im->data + lo, hi - lo, cudaMemcpyHostToDevice, cs));
+            if (it.direct) {
+                CUDA_TRY(c, cudaMemcpyAsync(reinterpret_cast<void *>(it.dst), im->data + it.img_off, it.bytes,
+                                            cudaMemcpyHostToDevice, cs));
+                continue;
+            }
+            CUDA_TRY(c, cudaMemcpyAsync(c->slots[j % S], im->data + it.img_off, it.bytes, cudaMemcpyHostToDevice, cs));
             cudaEvent_t a = c->ev(), b = c->ev();
             CUDA_TRY(c, cudaEventRecord(a, cs));
-            LAUNCH_TRY(c, launch_scatter(sd + pl.chunk_desc[j], pl.chunk_desc[j + 1] - pl.chunk_desc[j],
-                                         c->slots[j % S], c->n_sms, cs));
+            LAUNCH_TRY(c, launch_scatter(sd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
             CUDA_TRY(c, cudaEventRecord(b, cs));
             sc0.push_back(a);
             sc1.push_back(b);
@@ -1038,6 +1173,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
             CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
         }
     }
+    st.restore_direct_bytes = direct_bytes;
     // ---- verify: recompute every digest and compare with D_k (R-11) ---------
     const gcr_image *last = chain[n - 1];
     const int scratch = c->have_parent ? 1 - c->parent_idx : 0;

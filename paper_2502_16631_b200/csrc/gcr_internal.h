@@ -49,6 +49,12 @@ struct TileInfo {
     uint32_t counts;         // n_present | n_zero << 10 | n_parent << 20 (pages anchored here)
 };
 
+// Per-tile record the host reads (mapped pinned) to plan the drain.
+struct TileRec {
+    uint32_t present_bytes;  // PRESENT bytes anchored at the tile
+    uint32_t image_off;      // chunk-local image offset of the tile's first PRESENT byte
+};
+
 struct ChunkTotals {
     unsigned long long image_bytes;
     unsigned long long n_present, n_zero, n_parent;
@@ -114,10 +120,11 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
 uint64_t scan_workers(uint64_t rows, int n_sms);
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);
 int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, uint32_t *tile_off,
-                     cudaStream_t st);
+                     TileRec *host_rec, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
                 const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
-                uint32_t page_size, uint32_t log2_page, uint8_t *slot, int n_sms, cudaStream_t st);
+                uint32_t page_size, uint32_t log2_page, uint8_t *slot, const uint8_t *pack_flags, int n_sms,
+                cudaStream_t st);
 // Pagemap over all pages: phase 1 counts run starts per block and scans them,
 // writing the entry count to *n_entries_dev; phase 2 writes the entries.
 int launch_pagemap_count(const uint8_t *cls, uint64_t n_pages, uint32_t *blk_cnt, uint32_t *blk_off,

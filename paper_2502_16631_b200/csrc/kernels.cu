@@ -252,7 +252,8 @@ __device__ __forceinline__ void last_cta_publish(const ScanParams &p) {
 // tile_off (the pack's destination offsets); re-zeroes the tile counters.
 // One CTA, coalesced rounds of blockDim tiles.  Runs on the copy stream right
 // before K4, off the scan's critical path.
-__global__ void __launch_bounds__(1024) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te, uint32_t *tile_off) {
+__global__ void __launch_bounds__(1024) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te, uint32_t *tile_off,
+                                                    TileRec *host_rec) {
     __shared__ unsigned long long carry;
     if (threadIdx.x == 0) carry = 0ull;
     __syncthreads();
@@ -265,11 +266,18 @@ __global__ void __launch_bounds__(1024) k_tile_scan(TileInfo *ti, uint64_t tb, u
         }
         unsigned long long tot;
         const unsigned long long off = block_exclusive_scan(v, &tot) + carry;
-        if (t < te) tile_off[t] = (uint32_t)off;
+        if (t < te) {
+            tile_off[t] = (uint32_t)off;
+            // the host plans direct DMAs vs pack from these (mapped pinned; 8 B per tile)
+            asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(host_rec + (t - tb)), "r"(v),
+                         "r"((uint32_t)off)
+                         : "memory");
+        }
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
         __syncthreads();
     }
+    if (threadIdx.x == 0) __threadfence_system();
 }
 
 // Allocation holding global real row r: 32-ary search by the warp (each round
@@ -614,11 +622,12 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
 __global__ void __launch_bounds__(256) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
                                               const uint8_t *cls, const uint32_t *tile_off,
                                               uint64_t tb, uint64_t te, uint32_t P, uint32_t lg,
-                                              uint8_t *slot) {
+                                              uint8_t *slot, const uint8_t *pack_flags) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t t = tb + (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < te;
          t += nwarps) {
+        if (pack_flags && !pack_flags[t - tb]) continue;  // moved by a direct DMA
         const uint32_t a = __ldg(tile_alloc + t);
         const AllocDev *al = allocs + a;
         const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), tile0 = __ldg(&al->tile0);
@@ -827,19 +836,21 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     return launched(3);
 }
 
-int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off, cudaStream_t st) {
+int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off, TileRec *host_rec,
+                     cudaStream_t st) {
     if (te == tb) return 0;
-    k_tile_scan<<<1, 1024, 0, st>>>(tile_info, tb, te, tile_off);
+    k_tile_scan<<<1, 1024, 0, st>>>(tile_info, tb, te, tile_off, host_rec);
     return launched(1);
 }
 
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, const uint32_t *tile_off,
-                uint64_t tb, uint64_t te, uint32_t P, uint32_t lg, uint8_t *slot, int n_sms, cudaStream_t st) {
+                uint64_t tb, uint64_t te, uint32_t P, uint32_t lg, uint8_t *slot, const uint8_t *pack_flags, int n_sms,
+                cudaStream_t st) {
     const uint64_t tiles = te - tb;
     if (tiles == 0) return 0;
     uint64_t grid = (tiles + 7) / 8;
     if (grid > (uint64_t)n_sms * 4) grid = n_sms * 4;
-    k_pack<<<(unsigned)grid, 256, 0, st>>>(allocs, tile_alloc, cls, tile_off, tb, te, P, lg, slot);
+    k_pack<<<(unsigned)grid, 256, 0, st>>>(allocs, tile_alloc, cls, tile_off, tb, te, P, lg, slot, pack_flags);
     return launched(1);
 }
 

@@ -30,14 +30,15 @@ GCR_PE_PARENT, GCR_PE_PRESENT, GCR_PE_ZERO = 1, 4, 8
 
 class gcr_config(C.Structure):
     _fields_ = [("page_size", C.c_uint32), ("n_copy_streams", C.c_uint32), ("chunk_bytes", C.c_uint64),
-                ("n_staging_slots", C.c_uint32), ("verify", C.c_uint32), ("lock_timeout_ms", C.c_uint64)]
+                ("n_staging_slots", C.c_uint32), ("verify", C.c_uint32), ("lock_timeout_ms", C.c_uint64),
+                ("direct_min_bytes", C.c_uint64)]
 
 
 _STAT_FIELDS = ["lock_ns", "unlock_ns", "checkpoint_ns", "restore_ns", "scan_dev_ns", "scan_launches", "scan_bytes",
                 "compact_dev_ns", "pack_dev_ns", "drain_ns", "restore_h2d_ns", "scatter_dev_ns", "verify_dev_ns",
                 "verify_launches", "pages_scanned", "pages_zero", "pages_parent", "pages_written", "image_bytes",
                 "n_entries", "verify_failures", "first_bad_page", "restore_h2d_bytes", "kernel_launches",
-                "pinned_alloc_ns"]
+                "pinned_alloc_ns", "direct_bytes", "restore_direct_bytes"]
 
 
 class gcr_stats(C.Structure):

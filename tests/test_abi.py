@@ -45,6 +45,7 @@ def test_config_defaults_without_gpu(built):
     cfg = gcr.default_config()
     assert (cfg.page_size, cfg.n_copy_streams, cfg.chunk_bytes, cfg.verify, cfg.lock_timeout_ms) == \
         (65536, 2, 256 << 20, 1, 10000)   # lock timeout: "10 seconds by default"
+    assert cfg.direct_min_bytes == 16 << 20
     assert gcr.gcr_config_default(None) == gcr.GCR_E_INVAL
 
 

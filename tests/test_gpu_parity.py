@@ -51,10 +51,14 @@ def test_gpu_generator_matches_cpu_twin(G, kind):
     assert np.array_equal(got[8000:8000 + 77 * 8], exp2)
 
 
-def _ckpt_restore_parity(G, orc, sizes, P, zero_pages=(), chunk=None, streams=2, seed=99):
+ALWAYS_STAGED = (1 << 64) - 1
+DIRECT_MINS = [0, 1 << 20, ALWAYS_STAGED]   # every run direct / 1 MiB / every run staged
+
+
+def _ckpt_restore_parity(G, orc, sizes, P, zero_pages=(), chunk=None, streams=2, seed=99, direct_min=1 << 20):
     gcr, synth = G
     ts = _mk(G, sizes, seed, zero_pages=zero_pages, P=P)
-    cfg = dict(page_size=P, n_copy_streams=streams)
+    cfg = dict(page_size=P, n_copy_streams=streams, direct_min_bytes=direct_min)
     if chunk:
         cfg["chunk_bytes"] = chunk
     ctx = gcr.Context(0, **cfg)
@@ -68,10 +72,21 @@ def _ckpt_restore_parity(G, orc, sizes, P, zero_pages=(), chunk=None, streams=2,
         assert got == exp, first_diff(got, exp)
         for t in ts:
             t.fill_(0xA5)
+        st = ctx.stats()
+        assert st["direct_bytes"] <= st["image_bytes"]
+        if direct_min == 0 and P >= 65536:  # every PRESENT page is a whole tile (or slices of one)
+            assert st["direct_bytes"] == st["image_bytes"]
+        if direct_min == ALWAYS_STAGED:
+            assert st["direct_bytes"] == 0
         ctx.restore([img])
         for t, c in zip(ts, cont):
             assert np.array_equal(t.cpu().numpy(), c)
-        assert ctx.stats()["verify_failures"] == 0
+        st = ctx.stats()
+        assert st["verify_failures"] == 0
+        if direct_min == 0:
+            assert st["restore_direct_bytes"] == st["restore_h2d_bytes"]
+        if direct_min == ALWAYS_STAGED:
+            assert st["restore_direct_bytes"] == 0
         ctx.unlock()
         img.free()
     finally:
@@ -107,8 +122,9 @@ def test_c1_full_parity_and_round_trip(G, orc):
         ctx.close()
 
 
+@pytest.mark.parametrize("direct_min", DIRECT_MINS)
 @pytest.mark.parametrize("P", [4096, 8192, 16384, 32768, 65536, 131072, 262144, 2097152])
-def test_page_sizes_tails_and_zero_pages(G, orc, P):
+def test_page_sizes_tails_and_zero_pages(G, orc, P, direct_min):
     """Several tiles and a ragged tail per allocation at every page-size regime
     (group-owned pages, 2 groups/page, 4 groups/page, 64 KiB slices)."""
     rng = np.random.default_rng(P)
@@ -124,17 +140,19 @@ def test_page_sizes_tails_and_zero_pages(G, orc, P):
         for p in range(m):
             if rng.random() < 0.3:
                 zp.append((a, p))
-    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, seed=P + 1)
+    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, seed=P + 1, direct_min=direct_min)
 
 
+@pytest.mark.parametrize("direct_min", [0, ALWAYS_STAGED, 256 << 10])
 @pytest.mark.parametrize("chunk,streams", [(65536, 1), (131072, 3), (1 << 20, 2), (4 << 20, 8)])
-def test_chunking_and_copy_streams(G, orc, chunk, streams):
+def test_chunking_and_copy_streams(G, orc, chunk, streams, direct_min):
     """Many pipeline chunks (image offsets stitched across chunks, slots reused)."""
     P = 65536 if chunk >= 65536 else 4096
     sizes = [3 << 20, (5 << 20) + 4096, 64 * 1024 + 1024, 7 << 20]
     rng = np.random.default_rng(chunk)
     zp = [(a, int(p)) for a in range(4) for p in rng.choice((sizes[a] + P - 1) // P, min(3, (sizes[a] + P - 1) // P), replace=False)]
-    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=max(chunk, P), streams=streams, seed=chunk)
+    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=max(chunk, P), streams=streams, seed=chunk,
+                         direct_min=direct_min)
 
 
 def test_chunking_small_pages_many_chunks(G, orc):
@@ -164,15 +182,16 @@ def _mutate(ts, rng, k, P):
     return muts
 
 
+@pytest.mark.parametrize("direct_min", [0, ALWAYS_STAGED])
 @pytest.mark.parametrize("P", [4096, 65536, 262144])
-def test_incremental_chain_parity(G, orc, P):
+def test_incremental_chain_parity(G, orc, P, direct_min):
     """Full, then two incrementals with exact dirty counts; every stream equals
     the oracle's; restore(I0, I1, I2) into poison == state at I2."""
     gcr, synth = G
     rng = np.random.default_rng(P + 7)
     sizes = [40 * P + 1024, 17 * P, 3 * P + 16]
     ts = _mk(G, sizes, 31, zero_pages=[(0, 2), (1, 5)], P=P)
-    ctx = gcr.Context(0, page_size=P, chunk_bytes=max(P, 4 * 65536) * 4)
+    ctx = gcr.Context(0, page_size=P, chunk_bytes=max(P, 4 * 65536) * 4, direct_min_bytes=direct_min)
     try:
         reg = registry_of(ctx, ts)
         cont = host_copies(ts)
@@ -302,7 +321,7 @@ def test_gpt2_small_full_size_parity(G, orc):
     assert w.total_bytes == 1_493_277_696 and len(w.allocs) == 444
     ts = w.materialize()
     torch.cuda.synchronize()
-    ctx = gcr.Context(0, page_size=w.page_size)
+    ctx = gcr.Context(0, page_size=w.page_size)   # default direct_min: big tensors direct, small ones packed
     try:
         reg = registry_of(ctx, ts)
         ctx.reserve_host(w.total_bytes + (64 << 20))
@@ -312,13 +331,16 @@ def test_gpt2_small_full_size_parity(G, orc):
         got = img.stream()
         exp = oracle_stream(orc, w.page_size, reg, cont)
         assert got == exp, first_diff(got, exp)
+        st = ctx.stats()
+        assert 0 < st["direct_bytes"] < st["image_bytes"]   # both drain paths used (wte, wpe... direct)
         del got, exp
         for t in ts:
             t.fill_(0xA5)
         ctx.restore([img])
         for a in range(0, len(ts), 37):
             assert np.array_equal(ts[a].cpu().numpy(), cont[a])
-        assert ctx.stats()["verify_failures"] == 0
+        st = ctx.stats()
+        assert st["verify_failures"] == 0 and 0 < st["restore_direct_bytes"] < st["restore_h2d_bytes"]
         ctx.unlock()
     finally:
         ctx.close()
