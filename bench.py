@@ -182,13 +182,37 @@ def run_ours(args):
                       direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
     for t in ts:
         ctx.register_tensor(t)
-    ctx.reserve_host(w.total_bytes + (256 << 20))
+    R0 = w.total_bytes
+    keep_chain = False
+    if args.mode == "incremental":
+        # base image + the worst-case buffer a checkpoint takes before shrinking + kept incrementals
+        per_inc = int(args.dirty * R0 * 1.05) + (64 << 20)
+        need = 2 * R0 + (args.steps + args.warmup) * per_inc + (256 << 20)
+        mem_total = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        keep_chain = need < 0.7 * mem_total
+        ctx.reserve_host(need if keep_chain else 2 * R0 + 2 * per_inc + (256 << 20))
+    else:
+        ctx.reserve_host(R0 + (256 << 20))
     probes = probe_links(torch)
     R = w.total_bytes
     cst = ctx.stream()
     stream = torch.cuda.ExternalStream(cst)
 
+    incremental = args.mode == "incremental"
+    base_img, incs = None, []
+    if incremental:  # the full checkpoint the incrementals diff against (untimed)
+        ctx.lock()
+        base_img = ctx.checkpoint(gcr.GCR_FULL)
+        ctx.unlock()
+    step_no = [0]
+
     def step(timed):
+        if incremental:  # the "training step": dirty a fresh seeded set of pages (untimed harness work)
+            muts = synth.dirty_mutations(w, args.dirty, rng_seed=9000 + step_no[0], clustered=args.clustered)
+            synth.gpu_xor_batch([ts[a].data_ptr() + o for (a, o, x) in muts], [x for (a, o, x) in muts],
+                                torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+        step_no[0] += 1
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         h0 = time.perf_counter()
@@ -199,12 +223,16 @@ def run_ours(args):
                 raise RuntimeError(f"lock vote failed: {st}")
         else:
             ctx.lock()
-        img = ctx.checkpoint(gcr.GCR_FULL)
+        img = ctx.checkpoint(gcr.GCR_INCREMENTAL if incremental else gcr.GCR_FULL)
         s_ck = ctx.stats()
-        ctx.restore([img])
+        if not incremental:
+            ctx.restore([img])
         ctx.unlock()
         e1.record(stream)
-        img.free()
+        if incremental and keep_chain:
+            incs.append(img)
+        else:
+            img.free()
         h1 = time.perf_counter()
         e1.synchronize()
         s = ctx.stats()
@@ -227,13 +255,27 @@ def run_ours(args):
         torch.cuda.synchronize()
         _barrier(pg)
     launches = ctx.stats()["kernel_launches"] - launches0
+    chain_restore = None
+    if incremental and keep_chain:  # restore the whole chain once: full + every incremental, then verify
+        ctx.lock()
+        t0 = time.perf_counter()
+        ctx.restore([base_img] + incs)
+        t_rs = time.perf_counter() - t0
+        ctx.unlock()
+        sr = ctx.stats()
+        chain_restore = {"images": 1 + len(incs), "seconds": round(t_rs, 4), "GBps_registered": round(R / t_rs / 1e9, 3),
+                         "h2d_bytes": sr["restore_h2d_bytes"], "verify_failures": sr["verify_failures"]}
+        for im in incs:
+            im.free()
+    if base_img is not None:
+        base_img.free()
     t_dev = _max_over_ranks(pg, sum(dev))
     t_host = _max_over_ranks(pg, sum(host))
     R_all = _sum_over_ranks(pg, float(R))
     K = args.steps
     # per-phase, per-rank means
     ck = sum(r[0]["checkpoint_ns"] for r in recs) / K * 1e-9
-    rs = sum(r[1]["restore_ns"] for r in recs) / K * 1e-9
+    rs = sum(r[1]["restore_ns"] for r in recs) / K * 1e-9 if not incremental else float("nan")
     sc = recs[-1][0]
     scan_ns = sum(r[0]["scan_dev_ns"] for r in recs)
     scan_l = sum(r[0]["scan_launches"] for r in recs)
@@ -264,7 +306,7 @@ def run_ours(args):
     d2h = sc["image_bytes"] + 4 * sc["pages_scanned"] + 16 * sc["n_entries"]
     h2d = recs[-1][1]["restore_h2d_bytes"] + 4 * sc["pages_scanned"]
     ck_gbs = R / ck / 1e9
-    rs_gbs = R / rs / 1e9
+    rs_gbs = R / rs / 1e9 if not incremental else float("nan")
     result = {
         "metric": "checkpoint & restore GB/s per GPU and box-aggregate at 1/2/4/8 B200 vs roofline",
         "value": round(R_all * K / t_dev / 1e9, 3),
@@ -278,7 +320,8 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic (seeded counter-based generator; training-state-shaped fp32/bf16 values)",
-        "config": {"workload": _workload_desc(args.config, w), "registered_bytes_per_rank": R,
+        "config": {"workload": _workload_desc(args.config + ("i" if incremental and args.config == "C4" else ""), w),
+                   "dirty_fraction": args.dirty if incremental else None, "registered_bytes_per_rank": R,
                    "allocations": len(w.allocs), "page_size": w.page_size, "chunk_bytes": args.chunk_mb << 20,
                    "copy_streams": args.streams, "direct_min_bytes": int(args.direct_min_mb * (1 << 20)) if args.direct_min_mb >= 0 else None,
                    "parallelism": f"independent ranks x{world} (gloo control plane)",
@@ -291,7 +334,7 @@ def run_ours(args):
         "link_roofline": {"drain_GBps": round(img_b / (sc["drain_ns"] * 1e-9) / 1e9, 2),
                           "d2h_probe_GBps": probes["d2h_gbs"], "h2d_probe_GBps": probes["h2d_gbs"],
                           "checkpoint_frac_of_d2h": round(ck_gbs / probes["d2h_gbs"] * img_b / R, 3),
-                          "restore_frac_of_h2d": round(rs_gbs / probes["h2d_gbs"] * img_b / R, 3)},
+                          "restore_frac_of_h2d": round(rs_gbs / probes["h2d_gbs"] * img_b / R, 3) if not incremental else None},
         "roofline": {"kernel": "K1 scan_digest_classify (k_scan)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 3), "traffic": traffic,
@@ -303,6 +346,8 @@ def run_ours(args):
                 "what": "host wall clock of Context.lock/checkpoint/restore/unlock/free via the Python binding"},
         "gpu_launches": int(_sum_over_ranks(pg, float(launches))),
         "paper_context": PAPER_CONTEXT,
+        "mode": args.mode,
+        "chain_restore": chain_restore,
         "probes": probes,
     }
     result["clocks"] = clk.summary()
@@ -320,6 +365,7 @@ def _workload_desc(name, w):
             "C2": "C2: GPT-2 small training state, fp32 weights + Adam m/v (444 allocations), full checkpoint + restore",
             "C3": "C3: Llama-3 8B ZeRO-3 shard per rank (bf16 param/grad + fp32 master/m/v), full checkpoint + restore",
             "C4": f"C4: {len(w.allocs)} x 1 GiB per GPU, full checkpoint + restore",
+            "C4i": f"C4: {len(w.allocs)} x 1 GiB per GPU, incremental checkpoint of a seeded dirty set per step",
             "C5": f"C5: {len(w.allocs)} GiB per GPU, 25% zero 2 MiB regions, full checkpoint + restore"}[name]
 
 
@@ -394,6 +440,11 @@ def main():
     ap.add_argument("--direct-min-mb", type=float, default=None,
                     help="runs >= this go by direct DMA (default: the library's); -1 = always staged")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--mode", default="full", choices=["full", "incremental"],
+                    help="full: checkpoint+restore per step (default); incremental: dirty --dirty of the pages, "
+                         "then an incremental checkpoint per step; the whole chain is restored once at the end")
+    ap.add_argument("--dirty", type=float, default=0.01)
+    ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.direct_min_mb is None:

@@ -32,6 +32,10 @@ int gsy_fill(uint64_t dptr, uint64_t bytes, uint64_t seed, uint32_t key, uint32_
 /* XOR the u32 at dptr with x (one mutation: the page becomes dirty).  Async. */
 int gsy_xor_u32(uint64_t dptr, uint32_t x, void *cuda_stream);
 
+/* n mutations at once: dptrs[i] ^= xs[i] (host arrays, copied; synchronous
+ * with respect to the host arrays, asynchronous on cuda_stream otherwise). */
+int gsy_xor_u32_batch(const uint64_t *dptrs, const uint32_t *xs, uint64_t n, void *cuda_stream);
+
 /* Fault-injection helpers for the lock-timeout test: a mapped pinned flag and
  * a kernel that spins on `cuda_stream` until the flag becomes non-zero. */
 int gsy_flag_alloc(uint64_t *host_ptr, uint64_t *dev_ptr);

@@ -681,10 +681,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
 
     uint64_t R = 0;
     for (const RegEntry &r : c->reg) R += r.bytes;
-    img->data_cap = R;
-    img->data = static_cast<uint8_t *>(c->pool.alloc(R));
+    // Small metadata first, then the worst-case (R) data buffer, which is
+    // shrunk to the image size right after the drain: nothing is ever placed
+    // behind the data buffer, so the pool does not fragment across checkpoints.
     img->digests_cap = 4 * c->n_pages;
     img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
+    img->data_cap = R;
+    img->data = static_cast<uint8_t *>(c->pool.alloc(R));
     st.pinned_alloc_ns = c->pool.pin_ns;
     if (!img->data || !img->digests) return fail(c, GCR_E_NOMEM, "checkpoint: pinned host allocation failed");
 
@@ -863,6 +866,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     }
     if (direct_bytes + staged_bytes != base) return fail(c, GCR_E_CUDA, "checkpoint: drain plan does not cover the image");
     st.direct_bytes = direct_bytes;
+    c->pool.shrink(img->data, img->data_cap, base);  // the tail is free before the pagemap is allocated
+    img->data_cap = base;
     // K3 pagemap over all pages (maximal runs, independent of chunking).
     auto pm0 = c->ev(), pm1 = c->ev();
     CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
@@ -921,8 +926,6 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     st.n_entries = ne;
 
     // image model
-    c->pool.shrink(img->data, img->data_cap, base);
-    img->data_cap = base;
     gcr_image_hdr &h = img->hdr;
     std::memcpy(h.magic, kMagic, 8);
     h.version = 1;

@@ -48,6 +48,11 @@ __global__ void k_fill(uint64_t *dst, uint64_t nwords, uint64_t ctr_base, uint32
 
 __global__ void k_xor(uint32_t *p, uint32_t x) { *p ^= x; }
 
+__global__ void k_xor_batch(const uint64_t *ptrs, const uint32_t *xs, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        *reinterpret_cast<uint32_t *>(ptrs[i]) ^= xs[i];
+}
+
 __global__ void k_spin(const volatile uint32_t *flag) {
     while (*flag == 0) {
         __nanosleep(1000);
@@ -71,6 +76,26 @@ int gsy_fill(uint64_t dptr, uint64_t bytes, uint64_t seed, uint32_t key, uint32_
 int gsy_xor_u32(uint64_t dptr, uint32_t x, void *stream) {
     k_xor<<<1, 1, 0, (cudaStream_t)stream>>>((uint32_t *)dptr, x);
     return (int)cudaGetLastError();
+}
+
+int gsy_xor_u32_batch(const uint64_t *dptrs, const uint32_t *xs, uint64_t n, void *stream) {
+    if (n == 0) return 0;
+    uint64_t *dp = nullptr;
+    uint32_t *dx = nullptr;
+    cudaError_t e = cudaMalloc(&dp, n * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&dx, n * 4);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dp, dptrs, n * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dx, xs, n * 4, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+    if (e == cudaSuccess) {
+        uint64_t grid = (n + 255) / 256;
+        if (grid > 148ull * 16) grid = 148ull * 16;
+        k_xor_batch<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(dp, dx, n);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(dp);
+    cudaFree(dx);
+    return (int)e;
 }
 
 int gsy_flag_alloc(uint64_t *host_ptr, uint64_t *dev_ptr) {

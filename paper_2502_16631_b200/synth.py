@@ -94,6 +94,7 @@ def synth_lib():
         L = C.CDLL(path)
         L.gsy_fill.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]
         L.gsy_xor_u32.argtypes = [C.c_uint64, C.c_uint32, C.c_void_p]
+        L.gsy_xor_u32_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
         L.gsy_flag_alloc.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.gsy_flag_set.argtypes = [C.c_uint64, C.c_uint32]
         L.gsy_flag_free.argtypes = [C.c_uint64]
@@ -112,6 +113,15 @@ def gpu_xor_u32(dptr: int, x: int, stream: int = 0):
     rc = synth_lib().gsy_xor_u32(dptr, x & 0xFFFFFFFF, C.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"gsy_xor_u32 failed: cuda error {rc}")
+
+
+def gpu_xor_batch(dptrs, xs, stream: int = 0):
+    """Apply many XOR mutations with one kernel launch (harness)."""
+    p = np.ascontiguousarray(dptrs, dtype=np.uint64)
+    x = np.ascontiguousarray(np.asarray(xs, dtype=np.uint64).astype(np.uint32))
+    rc = synth_lib().gsy_xor_u32_batch(p.ctypes.data, x.ctypes.data, p.size, C.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(f"gsy_xor_u32_batch failed: cuda error {rc}")
 
 
 # ---------------------------------------------------------------------------
@@ -188,8 +198,8 @@ class Workload:
         st = torch.cuda.current_stream().cuda_stream
         for (a, o, n) in zero_ranges:
             ts[a][o:o + n].zero_()
-        for (a, o, x) in mutations:
-            gpu_xor_u32(ts[a].data_ptr() + o, x, st)
+        if mutations:
+            gpu_xor_batch([ts[a].data_ptr() + o for (a, o, x) in mutations], [x for (a, o, x) in mutations], st)
 
 
 def gpt2_small_params():
