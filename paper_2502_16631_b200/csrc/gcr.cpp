@@ -189,15 +189,17 @@ struct gcr_ctx {
     uint8_t *cls = nullptr;
     TileInfo *tile_info = nullptr;
     uint32_t *tile_off = nullptr;
-    Piece *pieces = nullptr;  // 2 per K1 group
+    Piece *pieces = nullptr;  // 2 per K1 warp, two buffers (chunk parity)
     uint32_t *contrib = nullptr;
+    uint64_t pieces_per_buf = 0;
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
     ChunkTotals *totals_d = nullptr, *totals_h = nullptr, *totals_map = nullptr;  // totals_h: mapped pinned
     unsigned *done_d = nullptr;                               // per-chunk CTA tickets
     unsigned long long *misc_d = nullptr, *misc_h = nullptr;  // [0] n_entries, [1] verify count, [2] first bad
     unsigned long long *nent_h = nullptr, *nent_map = nullptr;  // mapped pinned n_entries
-    TileRec *tile_rec_h = nullptr, *tile_rec_map = nullptr;     // mapped pinned per-tile records
+    TileRec *tile_rec_h = nullptr, *tile_rec_map = nullptr;     // mapped pinned non-empty tile records
+    unsigned long long *rec_count_h = nullptr, *rec_count_map = nullptr;  // per chunk: records written
     uint8_t *pack_flags_h = nullptr, *pack_flags_d = nullptr;   // per-tile: packed (1) or direct (0)
     uint32_t z_page = 0;
 
@@ -268,6 +270,8 @@ void free_layout(gcr_ctx *c) {
     if (c->misc_h) cudaFreeHost(c->misc_h);
     if (c->nent_h) cudaFreeHost(c->nent_h);
     if (c->tile_rec_h) cudaFreeHost(c->tile_rec_h);
+    if (c->rec_count_h) cudaFreeHost(c->rec_count_h);
+    c->rec_count_h = c->rec_count_map = nullptr;
     if (c->pack_flags_h) cudaFreeHost(c->pack_flags_h);
     c->tile_rec_h = c->tile_rec_map = nullptr;
     c->pack_flags_h = c->pack_flags_d = nullptr;
@@ -365,8 +369,9 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->tile_info, sizeof(TileInfo) * t));
     CUDA_TRY(c, cudaMalloc(&c->tile_off, 4 * t));
     CUDA_TRY(c, cudaMemset(c->tile_info, 0, sizeof(TileInfo) * t));
-    CUDA_TRY(c, cudaMalloc(&c->pieces, sizeof(Piece) * 2 * scan_workers(~0ull >> 8, c->n_sms)));
-    CUDA_TRY(c, cudaMalloc(&c->contrib, sizeof(uint32_t) * 2 * scan_workers(~0ull >> 8, c->n_sms)));
+    c->pieces_per_buf = 2 * scan_workers(~0ull >> 8, c->n_sms);
+    CUDA_TRY(c, cudaMalloc(&c->pieces, sizeof(Piece) * 2 * c->pieces_per_buf));
+    CUDA_TRY(c, cudaMalloc(&c->contrib, sizeof(uint32_t) * 2 * c->pieces_per_buf));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_cnt, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
@@ -379,6 +384,8 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMemset(c->done_d, 0, sizeof(unsigned) * nch));
     CUDA_TRY(c, cudaHostAlloc(&c->nent_h, 64, cudaHostAllocMapped));
     CUDA_TRY(c, cudaHostAlloc(&c->tile_rec_h, sizeof(TileRec) * t, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostAlloc(&c->rec_count_h, sizeof(unsigned long long) * nch, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->rec_count_map), c->rec_count_h, 0));
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->tile_rec_map), c->tile_rec_h, 0));
     CUDA_TRY(c, cudaHostAlloc(&c->pack_flags_h, t, cudaHostAllocDefault));
     CUDA_TRY(c, cudaMalloc(&c->pack_flags_d, t));
@@ -709,7 +716,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.tile_off = c->tile_off;
 
     const size_t nch = c->chunks.size();
-    std::vector<cudaEvent_t> k1s(nch), k1e(nch), tot(nch), pks(nch), pke(nch), dde(nch);
+    std::vector<cudaEvent_t> k1s(nch), k1m(nch), k1e(nch), k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
     cudaEvent_t t0 = c->ev();
     CUDA_TRY(c, cudaEventRecord(t0, c->compute));
@@ -717,7 +724,12 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // stream up front.  K1b publishes the chunk totals and K2 the per-tile
     // records straight into mapped pinned memory, so planning the drain never
     // waits on a DMA queued behind the previous chunk's drain.
-    for (size_t i = 0; i < nch; i++) {
+    // A rolling window of kLookahead chunks is kept enqueued, so the host can
+    // plan chunk 0's drain as soon as it is scanned (enqueueing every chunk up
+    // front delayed the first drain by ~0.5 ms of API calls on big registries).
+    constexpr size_t kLookahead = 3;
+    size_t enqueued = 0;
+    auto enqueue_scan = [&](size_t i) -> gcr_status {
         const Chunk &ch = c->chunks[i];
         sp.tile_begin = ch.tile_begin;
         sp.tile_end = ch.tile_end;
@@ -730,12 +742,29 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         k1s[i] = c->ev();
         k1e[i] = c->ev();
         tot[i] = c->ev();
+        // pieces are double-buffered by chunk parity so K1 of the next chunk can
+        // run while K1b folds this one (post stream, on the SMs K1 leaves free)
+        sp.pieces = c->pieces + (i & 1) * c->pieces_per_buf;
+        sp.contrib = c->contrib + (i & 1) * c->pieces_per_buf;
+        if (i >= 2)  // K1(i) overwrites the buffer K1b(i-2) read
+            CUDA_TRY(c, cudaStreamWaitEvent(c->compute, k1e[i - 2], 0));
         CUDA_TRY(c, cudaEventRecord(k1s[i], c->compute));
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
-        CUDA_TRY(c, cudaEventRecord(k1e[i], c->compute));
+        k1m[i] = c->ev();
+        CUDA_TRY(c, cudaEventRecord(k1m[i], c->compute));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->post, k1m[i], 0));
+        LAUNCH_TRY(c, launch_fold(sp, c->n_sms, c->post));
+        CUDA_TRY(c, cudaEventRecord(k1e[i], c->post));
+        k2s[i] = c->ev();
+        CUDA_TRY(c, cudaEventRecord(k2s[i], c->post));
         LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off,
-                                       c->tile_rec_map + ch.tile_begin, c->compute));
-        CUDA_TRY(c, cudaEventRecord(tot[i], c->compute));
+                                       c->tile_rec_map + ch.tile_begin, c->rec_count_map + i, c->post));
+        CUDA_TRY(c, cudaEventRecord(tot[i], c->post));
+        return GCR_OK;
+    };
+    for (; enqueued < std::min(nch, kLookahead); enqueued++) {
+        gcr_status es = enqueue_scan(enqueued);
+        if (es != GCR_OK) return es;
     }
     // Drain: as each chunk's records land, plan it -- runs of fully PRESENT
     // tiles of at least direct_min_bytes go straight from the allocation to the
@@ -754,6 +783,10 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         CUDA_TRY(c, cudaEventSynchronize(tot[i]));
+        if (enqueued < nch) {  // keep the scan queue kLookahead chunks deep
+            gcr_status es = enqueue_scan(enqueued++);
+            if (es != GCR_OK) return es;
+        }
         ChunkTotals T;
         {
             const volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(c->totals_h + i);
@@ -792,10 +825,11 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                 a = lo;
             }
             const volatile uint32_t *rec = reinterpret_cast<const volatile uint32_t *>(c->tile_rec_h + ch.tile_begin);
-            for (uint64_t t = ch.tile_begin; t < ch.tile_end; t++) {
+            const uint64_t nrec = *reinterpret_cast<const volatile unsigned long long *>(c->rec_count_h + i);
+            for (uint64_t k = 0; k < nrec; k++) {
+                const uint64_t t = ch.tile_begin + rec[4 * k];
+                const uint2 r = make_uint2(rec[4 * k + 1], rec[4 * k + 2]);
                 while (t >= c->allocs_h[a].tile0 + c->allocs_h[a].n_tiles) a++;
-                const uint2 r = make_uint2(rec[2 * (t - ch.tile_begin)], rec[2 * (t - ch.tile_begin) + 1]);
-                if (r.x == 0) continue;
                 const AllocDev &al = c->allocs_h[a];
                 const uint64_t lt = t - al.tile0;
                 uint64_t src, span;
@@ -824,12 +858,12 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                 }
             }
             close();
-            if (any_staged) {  // contiguous image ranges of consecutive staged tiles
-                for (uint64_t t = ch.tile_begin; t < ch.tile_end; t++) {
-                    if (!flags[t - ch.tile_begin]) continue;
-                    const uint2 r = make_uint2(rec[2 * (t - ch.tile_begin)], rec[2 * (t - ch.tile_begin) + 1]);
-                    if (!staged.empty() && staged.back().second == r.y) staged.back().second += r.x;
-                    else staged.emplace_back(r.y, (uint64_t)r.y + r.x);
+            if (any_staged) {  // contiguous image ranges of consecutive staged (non-empty) tiles
+                for (uint64_t k = 0; k < nrec; k++) {
+                    if (!flags[rec[4 * k]]) continue;
+                    const uint64_t lo = rec[4 * k + 2], len = rec[4 * k + 1];
+                    if (!staged.empty() && staged.back().second == lo) staged.back().second += len;
+                    else staged.emplace_back(lo, lo + len);
                 }
             }
         }
@@ -868,7 +902,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     st.direct_bytes = direct_bytes;
     c->pool.shrink(img->data, img->data_cap, base);  // the tail is free before the pagemap is allocated
     img->data_cap = base;
-    // K3 pagemap over all pages (maximal runs, independent of chunking).
+    // K3 pagemap over all pages (maximal runs, independent of chunking); the
+    // classes of cut pages are final only after the last K1b (post stream).
+    CUDA_TRY(c, cudaStreamWaitEvent(c->compute, tot[nch - 1], 0));
     auto pm0 = c->ev(), pm1 = c->ev();
     CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
     LAUNCH_TRY(c, launch_pagemap_count(c->cls, c->n_pages, c->pm_blk_cnt, c->pm_blk_off, c->nent_map, c->compute));
@@ -896,7 +932,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     st.scan_dev_ns = 0;
     st.pack_dev_ns = 0;
     for (size_t i = 0; i < nch; i++) {
-        CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s[i], k1e[i]));
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s[i], k1m[i]));  // K1 proper (K1b runs on the post stream)
         st.scan_dev_ns += (uint64_t)(ms * 1e6);
         CUDA_TRY(c, cudaEventElapsedTime(&ms, pks[i], pke[i]));
         st.pack_dev_ns += (uint64_t)(ms * 1e6);
@@ -911,9 +947,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         };
         std::fprintf(stderr, "{\"gcr_trace\": \"checkpoint\", \"chunks\": [");
         for (size_t i = 0; i < nch; i++)
-            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k1s[i]), rel(k1e[i]),
-                         rel(tot[i]), rel(pks[i]), rel(pke[i]), rel(dde[i]));
-        std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": \"k1_start k1_end totals pack_start pack_end d2h_end\"}\n",
+            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k1s[i]),
+                         rel(k1m[i]), rel(k1e[i]), rel(k2s[i]), rel(tot[i]), rel(pks[i]), rel(pke[i]), rel(dde[i]));
+        std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": \"k1_start k1_end k1b_end k2_start k2_end pack_start pack_end d2h_end\"}\n",
                      rel(pm0), rel(pm1));
     }
     st.scan_launches = nch;
@@ -1206,6 +1242,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.tables = c->tables_d;
         CUDA_TRY(c, cudaEventRecord(v0, c->compute));
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
+        LAUNCH_TRY(c, launch_fold(sp, c->n_sms, c->compute));
         CUDA_TRY(c, cudaEventRecord(v1, c->compute));
         CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));
         verify_launches = 1;

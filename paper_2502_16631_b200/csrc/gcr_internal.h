@@ -49,10 +49,12 @@ struct TileInfo {
     uint32_t counts;         // n_present | n_zero << 10 | n_parent << 20 (pages anchored here)
 };
 
-// Per-tile record the host reads (mapped pinned) to plan the drain.
+// Record of one NON-EMPTY tile the host reads (mapped pinned) to plan the drain.
 struct TileRec {
+    uint32_t tile;           // chunk-local tile index
     uint32_t present_bytes;  // PRESENT bytes anchored at the tile
     uint32_t image_off;      // chunk-local image offset of the tile's first PRESENT byte
+    uint32_t pad;
 };
 
 struct ChunkTotals {
@@ -118,9 +120,10 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
                             uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
                             cudaStream_t st);
 uint64_t scan_workers(uint64_t rows, int n_sms);
-int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);
+int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1
+int launch_fold(const ScanParams &p, int n_sms, cudaStream_t st);  // K1b (must follow K1 on st)
 int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, uint32_t *tile_off,
-                     TileRec *host_rec, cudaStream_t st);
+                     TileRec *host_rec, unsigned long long *rec_count, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
                 const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, const uint8_t *pack_flags, int n_sms,

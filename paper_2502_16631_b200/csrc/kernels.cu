@@ -249,35 +249,50 @@ __device__ __forceinline__ void last_cta_publish(const ScanParams &p) {
 }
 
 // K2: chunk-local exclusive scan of PRESENT bytes over the chunk's tiles ->
-// tile_off (the pack's destination offsets); re-zeroes the tile counters.
-// One CTA, coalesced rounds of blockDim tiles.  Runs on the copy stream right
-// before K4, off the scan's critical path.
-__global__ void __launch_bounds__(1024) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te, uint32_t *tile_off,
-                                                    TileRec *host_rec) {
-    __shared__ unsigned long long carry;
-    if (threadIdx.x == 0) carry = 0ull;
-    __syncthreads();
-    for (uint64_t base = tb; base < te; base += blockDim.x) {
-        const uint64_t t = base + threadIdx.x;
-        unsigned v = 0;
-        if (t < te) {
-            v = ti[t].present_bytes;
-            ti[t] = TileInfo{0u, 0u};
-        }
-        unsigned long long tot;
-        const unsigned long long off = block_exclusive_scan(v, &tot) + carry;
-        if (t < te) {
-            tile_off[t] = (uint32_t)off;
-            // the host plans direct DMAs vs pack from these (mapped pinned; 8 B per tile)
-            asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(host_rec + (t - tb)), "r"(v),
-                         "r"((uint32_t)off)
-                         : "memory");
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) carry += tot;
-        __syncthreads();
+// tile_off (the pack's destination offsets); re-zeroes the tile counters and
+// writes the NON-EMPTY tiles, compacted, into mapped pinned host memory
+// ({tile, present bytes, image offset}; count in rec_count) so the host plans
+// the drain from ~d*T records instead of T.  One CTA: the chunk's counters
+// are staged in shared memory with coalesced loads, each thread then scans a
+// contiguous run of tiles.  Runs on the post stream, beside the next scan.
+constexpr int kTileScanThreads = 1024;
+
+__global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te,
+                                                                uint32_t *tile_off, TileRec *host_rec,
+                                                                unsigned long long *rec_count) {
+    extern __shared__ uint32_t pb[];  // present bytes per tile of the chunk
+    const uint32_t n = (uint32_t)(te - tb);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        pb[i] = ti[tb + i].present_bytes;
+        ti[tb + i] = TileInfo{0u, 0u};
     }
-    if (threadIdx.x == 0) __threadfence_system();
+    __syncthreads();
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(n, per * threadIdx.x), hi = min(n, lo + per);
+    unsigned long long s = 0, cnt = 0;
+    for (uint32_t i = lo; i < hi; i++) {
+        s += pb[i];
+        cnt += pb[i] != 0u;
+    }
+    unsigned long long tot_b, tot_c;
+    unsigned long long off = block_exclusive_scan(s, &tot_b);
+    unsigned long long k = block_exclusive_scan(cnt, &tot_c);
+    for (uint32_t i = lo; i < hi; i++) {
+        tile_off[tb + i] = (uint32_t)off;
+        if (pb[i]) {
+            TileRec *r = host_rec + k;
+            asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(r), "r"(i), "r"(pb[i]),
+                         "r"((uint32_t)off), "r"(0u)
+                         : "memory");
+            k++;
+        }
+        off += pb[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *reinterpret_cast<volatile unsigned long long *>(rec_count) = tot_c;
+        __threadfence_system();
+    }
 }
 
 // Allocation holding global real row r: 32-ary search by the warp (each round
@@ -797,9 +812,18 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
     return launched(1);
 }
 
+// K1 leaves kFreeSMs SMs unoccupied so that the previous chunk's K2/K4 (and
+// the restore's K6) start the moment they are enqueued instead of waiting
+// for the persistent scan to release an SM (measured: a pack queued behind
+// two scan launches delayed its chunk's drain by ~0.5 ms).
+constexpr int kFreeSMs = 10;   // = pack CTAs (8) + K2 (1) + 1 spare
+constexpr int kPackCtas = 8;
+
+static int scan_sms(int n_sms) { return n_sms > 4 * kFreeSMs ? n_sms - kFreeSMs : n_sms; }
+
 uint64_t scan_workers(uint64_t rows, int n_sms) {
     // every warp streams >= 8 rows (4 KiB); at most all warps of a full grid
-    const uint64_t full = (uint64_t)n_sms * (kScanThreads / 32);
+    const uint64_t full = (uint64_t)scan_sms(n_sms) * (kScanThreads / 32);
     uint64_t w = rows / 8;
     if (w < 1) w = 1;
     return w < full ? w : full;
@@ -820,6 +844,13 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     const uint64_t wpb = kScanThreads / 32;
     const uint64_t grid = (p.workers + wpb - 1) / wpb;
     k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    return launched(1);
+}
+
+int launch_fold(const ScanParams &p, int n_sms, cudaStream_t st) {
+    if (p.row_end == p.row_begin) return 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
     static bool fold_attr[64] = {};
     if (dev < 64 && !fold_attr[dev]) {
         if (cudaFuncSetAttribute(k_fold_contrib, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -827,19 +858,29 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
             return -1;
         fold_attr[dev] = true;
     }
+    // the fold may run beside the next chunk's scan: stay on the SMs K1 leaves free
+    const uint64_t cap = n_sms > 4 * kFreeSMs ? kFreeSMs - 1 : n_sms;
     uint64_t gc = (2 * p.workers + 255) / 256;
-    if (gc > (uint64_t)n_sms) gc = n_sms;
+    if (gc > cap) gc = cap;
     k_fold_contrib<<<(unsigned)gc, 256, kFoldTables * 4096u, st>>>(p);
     uint64_t g2 = (p.workers + 255) / 256;
-    if (g2 > (uint64_t)n_sms * 4) g2 = n_sms * 4;
+    if (g2 > cap) g2 = cap;
     k_fold_final<<<(unsigned)g2, 256, 0, st>>>(p);
-    return launched(3);
+    return launched(2);
 }
 
 int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off, TileRec *host_rec,
-                     cudaStream_t st) {
-    if (te == tb) return 0;
-    k_tile_scan<<<1, 1024, 0, st>>>(tile_info, tb, te, tile_off, host_rec);
+                     unsigned long long *rec_count, cudaStream_t st) {
+    const size_t smem = (size_t)(te - tb) * 4;
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev]) {  // up to 2 GiB chunks: 32768 tiles = 128 KiB
+        if (cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4) != cudaSuccess)
+            return -1;
+        attr_done[dev] = true;
+    }
+    k_tile_scan<<<1, kTileScanThreads, smem, st>>>(tile_info, tb, te, tile_off, host_rec, rec_count);
     return launched(1);
 }
 
@@ -848,8 +889,10 @@ int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_
                 cudaStream_t st) {
     const uint64_t tiles = te - tb;
     if (tiles == 0) return 0;
+    // the pack runs beside the next chunk's scan: stay on the SMs K1 leaves free
     uint64_t grid = (tiles + 7) / 8;
-    if (grid > (uint64_t)n_sms * 4) grid = n_sms * 4;
+    const uint64_t cap = n_sms > 4 * kFreeSMs ? kPackCtas : (uint64_t)n_sms * 4;
+    if (grid > cap) grid = cap;
     k_pack<<<(unsigned)grid, 256, 0, st>>>(allocs, tile_alloc, cls, tile_off, tb, te, P, lg, slot, pack_flags);
     return launched(1);
 }
