@@ -170,7 +170,11 @@ def probe_links(torch, nbytes=1 << 30):
 def run_ours(args):
     import torch
     world, rank, local, pg = _dist()
-    torch.cuda.set_device(local)
+    # one rank per GPU; on a box with fewer GPUs than ranks (functional tests)
+    # ranks share devices round-robin
+    dev = local % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    local = dev
     from paper_2502_16631_b200 import dist as gdist
     from paper_2502_16631_b200 import gcr, synth
 
