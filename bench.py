@@ -293,10 +293,11 @@ def run_ours(args):
                     "alg_bytes_per_step": R, "GBps": R * K / max(scan_ns, 1)},
         "K4_pack": {"dev_ms_per_step": pack_ns / K * 1e-6, "alg_bytes_per_step": 2 * img_b,
                     "GBps": 2 * img_b * K / max(pack_ns, 1)},
-        "K6K7_scatter_zero": {"dev_ms_per_step": scat_ns / K * 1e-6, "alg_bytes_per_step": 2 * img_b,
-                              "GBps": 2 * img_b * K / max(scat_ns, 1)},
-        "K8_verify": {"dev_ms_per_step": ver_ns / K * 1e-6, "alg_bytes_per_step": R,
-                      "GBps": R * K / max(ver_ns, 1)},
+        "K6K7_scatter_zero": None if incremental else
+        {"dev_ms_per_step": scat_ns / K * 1e-6, "alg_bytes_per_step": 2 * img_b,
+         "GBps": 2 * img_b * K / max(scat_ns, 1)},
+        "K8_verify": None if incremental else
+        {"dev_ms_per_step": ver_ns / K * 1e-6, "alg_bytes_per_step": R, "GBps": R * K / max(ver_ns, 1)},
     }
     # dominant kernel = the scan (K1 + K8 share it: largest algorithmic HBM work per step)
     achieved = R * K / max(scan_ns, 1)  # bytes/ns == GB/s
@@ -343,7 +344,7 @@ def run_ours(args):
                      "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 3), "traffic": traffic,
                      "peak_source": peaks["source"], "hbm_read_probe_GBps": probes["hbm_read_gbs"]},
-        "kernels": {k: {kk: round(vv, 4) if isinstance(vv, float) else vv for kk, vv in v.items()}
+        "kernels": {k: ({kk: round(vv, 4) if isinstance(vv, float) else vv for kk, vv in v.items()} if v else None)
                     for k, v in kern.items()},
         "e2e": {"value": round(R_all * K / t_host / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
