@@ -634,7 +634,7 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
 }
 
 // K4: gather PRESENT pages of the tiles [tb, te) into the staging slot.
-__global__ void __launch_bounds__(256) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
+__global__ void __launch_bounds__(1024) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
                                               const uint8_t *cls, const uint32_t *tile_off,
                                               uint64_t tb, uint64_t te, uint32_t P, uint32_t lg,
                                               uint8_t *slot, const uint8_t *pack_flags) {
@@ -889,11 +889,12 @@ int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_
                 cudaStream_t st) {
     const uint64_t tiles = te - tb;
     if (tiles == 0) return 0;
-    // the pack runs beside the next chunk's scan: stay on the SMs K1 leaves free
-    uint64_t grid = (tiles + 7) / 8;
+    // the pack runs beside the next chunk's scan: stay on the SMs K1 leaves free,
+    // with 32 warps each (4 KiB of loads in flight per warp) to fill them
+    uint64_t grid = (tiles + 31) / 32;
     const uint64_t cap = n_sms > 4 * kFreeSMs ? kPackCtas : (uint64_t)n_sms * 4;
     if (grid > cap) grid = cap;
-    k_pack<<<(unsigned)grid, 256, 0, st>>>(allocs, tile_alloc, cls, tile_off, tb, te, P, lg, slot, pack_flags);
+    k_pack<<<(unsigned)grid, 1024, 0, st>>>(allocs, tile_alloc, cls, tile_off, tb, te, P, lg, slot, pack_flags);
     return launched(1);
 }
 
