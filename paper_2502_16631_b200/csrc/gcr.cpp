@@ -194,8 +194,7 @@ struct gcr_ctx {
     uint64_t pieces_per_buf = 0;
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
-    ChunkTotals *totals_d = nullptr, *totals_h = nullptr, *totals_map = nullptr;  // totals_h: mapped pinned
-    unsigned *done_d = nullptr;                               // per-chunk CTA tickets
+    ChunkTotals *totals_h = nullptr, *totals_map = nullptr;  // mapped pinned, written by K2
     unsigned long long *misc_d = nullptr, *misc_h = nullptr;  // [0] n_entries, [1] verify count, [2] first bad
     unsigned long long *nent_h = nullptr, *nent_map = nullptr;  // mapped pinned n_entries
     TileRec *tile_rec_h = nullptr, *tile_rec_map = nullptr;     // mapped pinned non-empty tile records
@@ -263,7 +262,7 @@ bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P
 void free_layout(gcr_ctx *c) {
     void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
                     c->tile_off, c->pieces, c->contrib, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
-                    c->entries_d, c->totals_d, c->misc_d, c->done_d, c->pack_flags_d};
+                    c->entries_d, c->misc_d, c->pack_flags_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->totals_h) cudaFreeHost(c->totals_h);
@@ -276,7 +275,6 @@ void free_layout(gcr_ctx *c) {
     c->tile_rec_h = c->tile_rec_map = nullptr;
     c->pack_flags_h = c->pack_flags_d = nullptr;
     c->nent_h = c->nent_map = nullptr;
-    c->done_d = nullptr;
     c->totals_map = nullptr;
     c->allocs_d = nullptr;
     c->page_alloc = c->tile_alloc = c->D[0] = c->D[1] = nullptr;
@@ -287,7 +285,7 @@ void free_layout(gcr_ctx *c) {
     c->contrib = nullptr;
     c->pm_blk_cnt = c->pm_blk_off = c->run_start = nullptr;
     c->entries_d = nullptr;
-    c->totals_d = c->totals_h = nullptr;
+    c->totals_h = nullptr;
     c->misc_d = c->misc_h = nullptr;
     c->layout_valid = false;
     c->have_parent = false;
@@ -376,12 +374,8 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
     CUDA_TRY(c, cudaMalloc(&c->entries_d, sizeof(gcr_pagemap_entry) * g));
-    CUDA_TRY(c, cudaMalloc(&c->totals_d, sizeof(ChunkTotals) * nch));
-    CUDA_TRY(c, cudaMemset(c->totals_d, 0, sizeof(ChunkTotals) * nch));
     CUDA_TRY(c, cudaHostAlloc(&c->totals_h, sizeof(ChunkTotals) * nch, cudaHostAllocMapped));
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->totals_map), c->totals_h, 0));
-    CUDA_TRY(c, cudaMalloc(&c->done_d, sizeof(unsigned) * nch));
-    CUDA_TRY(c, cudaMemset(c->done_d, 0, sizeof(unsigned) * nch));
     CUDA_TRY(c, cudaHostAlloc(&c->nent_h, 64, cudaHostAllocMapped));
     CUDA_TRY(c, cudaHostAlloc(&c->tile_rec_h, sizeof(TileRec) * t, cudaHostAllocMapped));
     CUDA_TRY(c, cudaHostAlloc(&c->rec_count_h, sizeof(unsigned long long) * nch, cudaHostAllocMapped));
@@ -712,58 +706,64 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.cls = c->cls;
     sp.tile_info = c->tile_info;
     sp.tables = c->tables_d;
-    sp.done = c->done_d;
-    sp.tile_off = c->tile_off;
 
     const size_t nch = c->chunks.size();
-    std::vector<cudaEvent_t> k1s(nch), k1m(nch), k1e(nch), k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
+    // Scan groups: K1 launch g covers chunks [grp[g], grp[g+1]) -- 1, 1, 2, 4,
+    // then 8 chunks: the first drain starts after a small scan, later scans are
+    // long launches (their fixed cost amortised), the drain stays per chunk.
+    std::vector<size_t> grp{0};
+    for (size_t want = 1, g = 0; grp.back() < nch; g++) {
+        grp.push_back(std::min(nch, grp.back() + want));
+        if (g >= 1) want = std::min<size_t>(want * 2, 8);
+    }
+    const size_t ngrp = grp.size() - 1;
+    std::vector<cudaEvent_t> k1s(ngrp), k1m(ngrp), k1e(ngrp), k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
     cudaEvent_t t0 = c->ev();
     CUDA_TRY(c, cudaEventRecord(t0, c->compute));
-    // Enqueue every chunk's scan (K1 + K1b) and compaction (K2) on the compute
-    // stream up front.  K1b publishes the chunk totals and K2 the per-tile
-    // records straight into mapped pinned memory, so planning the drain never
-    // waits on a DMA queued behind the previous chunk's drain.
-    // A rolling window of kLookahead chunks is kept enqueued, so the host can
-    // plan chunk 0's drain as soon as it is scanned (enqueueing every chunk up
-    // front delayed the first drain by ~0.5 ms of API calls on big registries).
-    constexpr size_t kLookahead = 3;
-    size_t enqueued = 0;
-    auto enqueue_scan = [&](size_t i) -> gcr_status {
-        const Chunk &ch = c->chunks[i];
-        sp.tile_begin = ch.tile_begin;
-        sp.tile_end = ch.tile_end;
-        sp.row_begin = ch.row_begin;
-        sp.row_end = ch.row_end;
-        sp.workers = scan_workers(ch.row_end - ch.row_begin, c->n_sms);
-        sp.chunk_idx = (uint32_t)i;
-        sp.totals_dev = c->totals_d + i;
-        sp.totals_host = c->totals_map + i;
-        k1s[i] = c->ev();
-        k1e[i] = c->ev();
-        tot[i] = c->ev();
-        // pieces are double-buffered by chunk parity so K1 of the next chunk can
-        // run while K1b folds this one (post stream, on the SMs K1 leaves free)
-        sp.pieces = c->pieces + (i & 1) * c->pieces_per_buf;
-        sp.contrib = c->contrib + (i & 1) * c->pieces_per_buf;
-        if (i >= 2)  // K1(i) overwrites the buffer K1b(i-2) read
-            CUDA_TRY(c, cudaStreamWaitEvent(c->compute, k1e[i - 2], 0));
-        CUDA_TRY(c, cudaEventRecord(k1s[i], c->compute));
+    // K1 on the compute stream; K1b (fold) and K2 (per chunk: image offsets,
+    // non-empty tile records and chunk totals straight into mapped pinned
+    // memory) on the post stream, beside the next scan.  Planning the drain
+    // therefore never waits on a DMA queued behind the previous drain.  Two
+    // scan groups are kept enqueued ahead of the drain (enqueueing everything
+    // up front delayed the first drain by ~0.5 ms of API calls).
+    size_t enqueued = 0;  // scan groups enqueued
+    auto enqueue_group = [&](size_t g) -> gcr_status {
+        const Chunk &c0 = c->chunks[grp[g]], &c1 = c->chunks[grp[g + 1] - 1];
+        sp.tile_begin = c0.tile_begin;
+        sp.tile_end = c1.tile_end;
+        sp.row_begin = c0.row_begin;
+        sp.row_end = c1.row_end;
+        sp.workers = scan_workers(sp.row_end - sp.row_begin, c->n_sms);
+        // pieces are double-buffered by group parity so K1 of the next group can
+        // run while K1b folds this one
+        sp.pieces = c->pieces + (g & 1) * c->pieces_per_buf;
+        sp.contrib = c->contrib + (g & 1) * c->pieces_per_buf;
+        k1s[g] = c->ev();
+        k1m[g] = c->ev();
+        k1e[g] = c->ev();
+        if (g >= 2)  // K1(g) overwrites the buffer K1b(g-2) read
+            CUDA_TRY(c, cudaStreamWaitEvent(c->compute, k1e[g - 2], 0));
+        CUDA_TRY(c, cudaEventRecord(k1s[g], c->compute));
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
-        k1m[i] = c->ev();
-        CUDA_TRY(c, cudaEventRecord(k1m[i], c->compute));
-        CUDA_TRY(c, cudaStreamWaitEvent(c->post, k1m[i], 0));
+        CUDA_TRY(c, cudaEventRecord(k1m[g], c->compute));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->post, k1m[g], 0));
         LAUNCH_TRY(c, launch_fold(sp, c->n_sms, c->post));
-        CUDA_TRY(c, cudaEventRecord(k1e[i], c->post));
-        k2s[i] = c->ev();
-        CUDA_TRY(c, cudaEventRecord(k2s[i], c->post));
-        LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off,
-                                       c->tile_rec_map + ch.tile_begin, c->rec_count_map + i, c->post));
-        CUDA_TRY(c, cudaEventRecord(tot[i], c->post));
+        CUDA_TRY(c, cudaEventRecord(k1e[g], c->post));
+        for (size_t i = grp[g]; i < grp[g + 1]; i++) {
+            const Chunk &ch = c->chunks[i];
+            k2s[i] = c->ev();
+            tot[i] = c->ev();
+            CUDA_TRY(c, cudaEventRecord(k2s[i], c->post));
+            LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off,
+                                           c->tile_rec_map + ch.tile_begin, c->rec_count_map + i,
+                                           c->totals_map + i, c->post));
+            CUDA_TRY(c, cudaEventRecord(tot[i], c->post));
+        }
         return GCR_OK;
     };
-    for (; enqueued < std::min(nch, kLookahead); enqueued++) {
-        gcr_status es = enqueue_scan(enqueued);
+    for (; enqueued < std::min<size_t>(ngrp, 2); enqueued++) {
+        gcr_status es = enqueue_group(enqueued);
         if (es != GCR_OK) return es;
     }
     // Drain: as each chunk's records land, plan it -- runs of fully PRESENT
@@ -783,8 +783,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         CUDA_TRY(c, cudaEventSynchronize(tot[i]));
-        if (enqueued < nch) {  // keep the scan queue kLookahead chunks deep
-            gcr_status es = enqueue_scan(enqueued++);
+        // keep two scan groups ahead of the drain
+        while (enqueued < ngrp && i >= grp[enqueued - 1]) {  // drain reached the last enqueued group
+            gcr_status es = enqueue_group(enqueued++);
             if (es != GCR_OK) return es;
         }
         ChunkTotals T;
@@ -931,9 +932,11 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     float ms;
     st.scan_dev_ns = 0;
     st.pack_dev_ns = 0;
-    for (size_t i = 0; i < nch; i++) {
-        CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s[i], k1m[i]));  // K1 proper (K1b runs on the post stream)
+    for (size_t g = 0; g < ngrp; g++) {
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s[g], k1m[g]));  // K1 proper (K1b runs on the post stream)
         st.scan_dev_ns += (uint64_t)(ms * 1e6);
+    }
+    for (size_t i = 0; i < nch; i++) {
         CUDA_TRY(c, cudaEventElapsedTime(&ms, pks[i], pke[i]));
         st.pack_dev_ns += (uint64_t)(ms * 1e6);
     }
@@ -945,14 +948,19 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             cudaEventElapsedTime(&m, t0, e);
             return m;
         };
-        std::fprintf(stderr, "{\"gcr_trace\": \"checkpoint\", \"chunks\": [");
+        std::fprintf(stderr, "{\"gcr_trace\": \"checkpoint\", \"scans\": [");
+        for (size_t g = 0; g < ngrp; g++)
+            std::fprintf(stderr, "%s[%zu, %zu, %.3f, %.3f, %.3f]", g ? ", " : "", grp[g], grp[g + 1], rel(k1s[g]),
+                         rel(k1m[g]), rel(k1e[g]));
+        std::fprintf(stderr, "], \"chunks\": [");
         for (size_t i = 0; i < nch; i++)
-            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k1s[i]),
-                         rel(k1m[i]), rel(k1e[i]), rel(k2s[i]), rel(tot[i]), rel(pks[i]), rel(pke[i]), rel(dde[i]));
-        std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": \"k1_start k1_end k1b_end k2_start k2_end pack_start pack_end d2h_end\"}\n",
+            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k2s[i]), rel(tot[i]),
+                         rel(pks[i]), rel(pke[i]), rel(dde[i]));
+        std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": {\"scans\": \"chunk_lo chunk_hi k1_start "
+                             "k1_end k1b_end\", \"chunks\": \"k2_start k2_end pack_start pack_end d2h_end\"}}\n",
                      rel(pm0), rel(pm1));
     }
-    st.scan_launches = nch;
+    st.scan_launches = ngrp;
     st.scan_bytes = R;
     st.pages_scanned = c->n_pages;
     st.pages_zero = n_zero;
@@ -1013,8 +1021,6 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
         sync_all(c);
         // re-arm the per-launch device state the kernels leave zeroed on success
         cudaMemset(c->tile_info, 0, sizeof(TileInfo) * c->n_tiles);
-        cudaMemset(c->done_d, 0, sizeof(unsigned) * c->chunks.size());
-        cudaMemset(c->totals_d, 0, sizeof(ChunkTotals) * c->chunks.size());
         cudaGetLastError();
         image_free_buffers(img);
         delete img;

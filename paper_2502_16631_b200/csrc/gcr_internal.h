@@ -94,12 +94,6 @@ struct ScanParams {
     unsigned long long *verify_count;
     unsigned long long *first_bad;
     const CrcTables *tables;
-    // chunk compaction by the last CTA (full / incremental)
-    unsigned *done;              // per-chunk CTA tickets, zero between launches
-    uint32_t chunk_idx;
-    uint32_t *tile_off;
-    ChunkTotals *totals_dev;     // device accumulator (zero between launches)
-    ChunkTotals *totals_host;    // mapped pinned, published by K1b's last CTA
 };
 
 struct ScatterDesc {
@@ -123,7 +117,7 @@ uint64_t scan_workers(uint64_t rows, int n_sms);
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1
 int launch_fold(const ScanParams &p, int n_sms, cudaStream_t st);  // K1b (must follow K1 on st)
 int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, uint32_t *tile_off,
-                     TileRec *host_rec, unsigned long long *rec_count, cudaStream_t st);
+                     TileRec *host_rec, unsigned long long *rec_count, ChunkTotals *totals_host, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
                 const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, const uint8_t *pack_flags, int n_sms,

@@ -5,9 +5,9 @@
 //  K1  scan              A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
 //                        all-zero test, dirty diff, class, tile counters
 //  K1b fold_contrib/final  pages cut by a warp's range boundary: fold the
-//                        partial registers; publish the chunk totals
+//                        partial registers
 //  K2  tile_scan         A5: chunk-local exclusive scan of PRESENT bytes per
-//                        tile (the pack's destination offsets)
+//                        tile (the pack's destination offsets) and chunk totals
 //  K3  pagemap_*         A5: maximal runs -> CRIU-style pagemap entries
 //  K4  pack              A6: stream-compaction of PRESENT pages into staging
 //  K6  scatter           A8: staged image pieces -> allocation pages
@@ -135,18 +135,11 @@ __device__ __forceinline__ uint64_t tile_of_page(uint64_t tile0, uint64_t pi, ui
     return P <= kTileBytes ? tile0 + (pi >> (kLog2Tile - lg)) : tile0 + (pi << (lg - kLog2Tile));
 }
 
-// Per-CTA accumulators of the chunk totals (flushed with one global atomic
-// per CTA per counter: no same-address atomic storm at L2).
-struct CtaTotals {
-    unsigned long long image_bytes, n_present, n_zero, n_parent;
-};
-
 // c.1 steps 3-5 for one page given its raw register and non-zero flag (or
-// the A9 verify comparison), plus the per-tile and per-CTA compaction
-// counters.  Executed by one lane.
-__device__ __forceinline__ void finalize_page(const ScanParams &p, CtaTotals *ct, uint64_t g, uint64_t tile,
-                                              bool alloc_start, uint32_t len, uint32_t zlen, uint32_t raw,
-                                              bool nz) {
+// the A9 verify comparison), plus the per-tile compaction counters that K2
+// turns into image offsets and chunk totals.  Executed by one lane.
+__device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, uint64_t tile, bool alloc_start,
+                                              uint32_t len, uint32_t zlen, uint32_t raw, bool nz) {
     const uint32_t d = raw ^ zlen;
     if (p.mode == kScanVerify) {
         if (d != __ldg(p.d_ref + g)) {
@@ -160,37 +153,17 @@ __device__ __forceinline__ void finalize_page(const ScanParams &p, CtaTotals *ct
     if (!nz) {
         c = kClsZero;
         inc = 1u << 10;
-        atomicAdd(&ct->n_zero, 1ull);
     } else if (p.mode == kScanIncremental && __ldg(p.d_ref + g) == d) {
         c = kClsParent;
         inc = 1u << 20;
-        atomicAdd(&ct->n_parent, 1ull);
     } else {
         c = kClsPresent;
         inc = 1u;
         atomicAdd(&p.tile_info[tile].present_bytes, len);
-        atomicAdd(&ct->n_present, 1ull);
-        atomicAdd(&ct->image_bytes, (unsigned long long)len);
     }
     atomicAdd(&p.tile_info[tile].counts, inc);
     p.d_out[g] = d;
     p.cls[g] = c | (alloc_start ? kClsAllocStart : 0);
-}
-
-__device__ __forceinline__ void cta_totals_init(CtaTotals *ct) {
-    if (threadIdx.x == 0) *ct = CtaTotals{0ull, 0ull, 0ull, 0ull};
-}
-
-// Flush this CTA's totals into the chunk accumulator (device memory).
-__device__ __forceinline__ void cta_totals_flush(const ScanParams &p, CtaTotals *ct) {
-    __syncthreads();
-    if (threadIdx.x == 0 && p.mode != kScanVerify) {
-        unsigned long long *acc = reinterpret_cast<unsigned long long *>(p.totals_dev);
-        if (ct->image_bytes) atomicAdd(acc + 0, ct->image_bytes);
-        if (ct->n_present) atomicAdd(acc + 1, ct->n_present);
-        if (ct->n_zero) atomicAdd(acc + 2, ct->n_zero);
-        if (ct->n_parent) atomicAdd(acc + 3, ct->n_parent);
-    }
 }
 
 // Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
@@ -224,46 +197,29 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
     return res;
 }
 
-// Last-CTA-done of K1b: every CTA has flushed its totals; the CTA holding the
-// last ticket publishes the chunk totals straight into mapped pinned host
-// memory (no DMA queued behind the drain on the copy engines), re-zeroes the
-// device accumulator and re-arms the ticket counter.
-__device__ __forceinline__ void last_cta_publish(const ScanParams &p) {
-    __shared__ bool am_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) am_last = atomicAdd(p.done + p.chunk_idx, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!am_last || threadIdx.x != 0) return;
-    __threadfence();
-    volatile unsigned long long *acc = reinterpret_cast<volatile unsigned long long *>(p.totals_dev);
-    volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(p.totals_host);
-    const unsigned long long a0 = acc[0], a1 = acc[1], a2 = acc[2], a3 = acc[3];
-    h[0] = a0;
-    h[1] = a1;
-    h[2] = a2;
-    h[3] = a3;
-    acc[0] = acc[1] = acc[2] = acc[3] = 0ull;
-    __threadfence_system();
-    p.done[p.chunk_idx] = 0u;
-}
-
 // K2: chunk-local exclusive scan of PRESENT bytes over the chunk's tiles ->
-// tile_off (the pack's destination offsets); re-zeroes the tile counters and
-// writes the NON-EMPTY tiles, compacted, into mapped pinned host memory
-// ({tile, present bytes, image offset}; count in rec_count) so the host plans
-// the drain from ~d*T records instead of T.  One CTA: the chunk's counters
-// are staged in shared memory with coalesced loads, each thread then scans a
-// contiguous run of tiles.  Runs on the post stream, beside the next scan.
+// tile_off (the pack's destination offsets); re-zeroes the tile counters;
+// writes the chunk totals and the NON-EMPTY tiles, compacted, into mapped
+// pinned host memory ({tile, present bytes, image offset}; count in
+// rec_count) so the host plans the drain from ~d*T records instead of T.  One
+// CTA: the chunk's counters are staged in shared memory with coalesced loads,
+// each thread then scans a contiguous run of tiles.  Runs on the post stream,
+// beside the next scan, on the SMs the scan leaves free.
 constexpr int kTileScanThreads = 1024;
 
 __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te,
                                                                 uint32_t *tile_off, TileRec *host_rec,
-                                                                unsigned long long *rec_count) {
+                                                                unsigned long long *rec_count,
+                                                                ChunkTotals *totals_host) {
     extern __shared__ uint32_t pb[];  // present bytes per tile of the chunk
     const uint32_t n = (uint32_t)(te - tb);
+    unsigned long long np = 0, nz = 0, npa = 0;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        pb[i] = ti[tb + i].present_bytes;
+        const TileInfo x = ti[tb + i];
+        pb[i] = x.present_bytes;
+        np += x.counts & 1023u;
+        nz += (x.counts >> 10) & 1023u;
+        npa += (x.counts >> 20) & 1023u;
         ti[tb + i] = TileInfo{0u, 0u};
     }
     __syncthreads();
@@ -274,9 +230,12 @@ __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, ui
         s += pb[i];
         cnt += pb[i] != 0u;
     }
-    unsigned long long tot_b, tot_c;
+    unsigned long long tot_b, tot_c, tp, tz, tpa;
     unsigned long long off = block_exclusive_scan(s, &tot_b);
     unsigned long long k = block_exclusive_scan(cnt, &tot_c);
+    block_exclusive_scan(np, &tp);
+    block_exclusive_scan(nz, &tz);
+    block_exclusive_scan(npa, &tpa);
     for (uint32_t i = lo; i < hi; i++) {
         tile_off[tb + i] = (uint32_t)off;
         if (pb[i]) {
@@ -290,6 +249,11 @@ __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, ui
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(totals_host);
+        h[0] = tot_b;
+        h[1] = tp;
+        h[2] = tz;
+        h[3] = tpa;
         *reinterpret_cast<volatile unsigned long long *>(rec_count) = tot_c;
         __threadfence_system();
     }
@@ -394,7 +358,7 @@ __device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
 }
 
 // Page complete (vr == Rp): digest it (or leave a piece) and move on.
-__device__ __forceinline__ void page_end(const ScanParams &p, CtaTotals *ct, ProcCursor &pc, uint32_t (&x)[4],
+__device__ __forceinline__ void page_end(const ScanParams &p, ProcCursor &pc, uint32_t (&x)[4],
                                          uint32_t &acc, const uint32_t *small, uint64_t wid, uint32_t lane) {
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t raw = warp_raw(small, x);
@@ -404,7 +368,7 @@ __device__ __forceinline__ void page_end(const ScanParams &p, CtaTotals *ct, Pro
         const uint64_t g = pc.al.page0 + pc.pi;
         if (whole) {
             const bool tail = pc.pi == pc.al.n_pages - 1;
-            finalize_page(p, ct, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0,
+            finalize_page(p, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0,
                           tail ? pc.al.tail_len : P, tail ? pc.al.z_tail : p.z_page, raw, nz);
         } else {
             p.pieces[2 * wid + pc.slot] = Piece{g, pc.a, pc.vstart, P >> kLog2Row, raw, nz ? 1u : 0u};
@@ -422,7 +386,7 @@ __device__ __forceinline__ void page_end(const ScanParams &p, CtaTotals *ct, Pro
 
 // Digest the next block (the same cnt rows load_rows fetched into w).
 template <int U>
-__device__ __forceinline__ void process_rows(const ScanParams &p, CtaTotals *ct, ProcCursor &pc, const uint4 (&w)[U],
+__device__ __forceinline__ void process_rows(const ScanParams &p, ProcCursor &pc, const uint4 (&w)[U],
                                              int &left, uint32_t (&x)[4], uint32_t &acc, const uint32_t *small,
                                              uint32_t lane4, uint32_t sb, uint64_t wid, uint32_t lane) {
     const uint32_t Rp = p.page_size >> kLog2Row;
@@ -437,7 +401,7 @@ __device__ __forceinline__ void process_rows(const ScanParams &p, CtaTotals *ct,
     }
     pc.vr += cnt;
     left -= cnt;
-    if (pc.vr == Rp) page_end(p, ct, pc, x, acc, small, wid, lane);
+    if (pc.vr == Rp) page_end(p, pc, x, acc, small, wid, lane);
 }
 
 // K1.
@@ -483,8 +447,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             if (i < kSmallTables * 1024u) ss[i] = sv[j];
         }
     }
-    __shared__ CtaTotals ct;
-    cta_totals_init(&ct);
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -533,10 +495,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
         while (to_proc > 0) {
             if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane);
-            process_rows<U>(p, &ct, pc, wa, to_proc, x, acc, small, lane4, sb, wid, lane);
+            process_rows<U>(p, pc, wa, to_proc, x, acc, small, lane4, sb, wid, lane);
             if (to_proc <= 0) break;
             if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
-            process_rows<U>(p, &ct, pc, wb, to_proc, x, acc, small, lane4, sb, wid, lane);
+            process_rows<U>(p, pc, wb, to_proc, x, acc, small, lane4, sb, wid, lane);
         }
         // the range ended inside a page: leave a piece
         if (pc.vr != pc.vstart) {
@@ -549,7 +511,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         if (lane == 0)
             for (uint32_t s = pc.slot; s < 2; s++) p.pieces[2 * wid + s] = Piece{~0ull, 0u, 0u, 0u, 0u, 0u};
     }
-    cta_totals_flush(p, &ct);
 }
 
 // K1b: fold the pieces of pages cut by warp-range boundaries, in two launches.
@@ -574,11 +535,8 @@ __global__ void __launch_bounds__(256) k_fold_contrib(const ScanParams p) {
 
 // (b) the warp holding a page's FIRST piece owns it: XOR of the contributions
 //     of its piece and of the HEAD pieces of the following warps, then c.1
-//     steps 3-5.  Its last CTA publishes the chunk totals.
+//     steps 3-5.
 __global__ void __launch_bounds__(256) k_fold_final(const ScanParams p) {
-    __shared__ CtaTotals ct;
-    cta_totals_init(&ct);
-    __syncthreads();
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t Rp = P >> kLog2Row;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.workers;
@@ -601,12 +559,10 @@ __global__ void __launch_bounds__(256) k_fold_final(const ScanParams p) {
                 nz |= p.pieces[2 * k].nz != 0;
                 end = p.pieces[2 * k].vr_end;
             }
-            finalize_page(p, &ct, pc.page, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
+            finalize_page(p, pc.page, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
                           tail ? __ldg(&al->z_tail) : p.z_page, raw, nz);
         }
     }
-    cta_totals_flush(p, &ct);
-    if (p.mode != kScanVerify) last_cta_publish(p);
 }
 
 // K0: page -> allocation and tile -> allocation (A1).  One CTA per allocation.
@@ -870,7 +826,7 @@ int launch_fold(const ScanParams &p, int n_sms, cudaStream_t st) {
 }
 
 int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off, TileRec *host_rec,
-                     unsigned long long *rec_count, cudaStream_t st) {
+                     unsigned long long *rec_count, ChunkTotals *totals_host, cudaStream_t st) {
     const size_t smem = (size_t)(te - tb) * 4;
     static bool attr_done[64] = {};
     int dev = 0;
@@ -880,7 +836,7 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *ti
             return -1;
         attr_done[dev] = true;
     }
-    k_tile_scan<<<1, kTileScanThreads, smem, st>>>(tile_info, tb, te, tile_off, host_rec, rec_count);
+    k_tile_scan<<<1, kTileScanThreads, smem, st>>>(tile_info, tb, te, tile_off, host_rec, rec_count, totals_host);
     return launched(1);
 }
 
