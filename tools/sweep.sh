@@ -16,10 +16,10 @@ run C2 --config C2 --steps 10
 run C2_P4K --config C2 --page-size 4096 --steps 5
 run C2_P2M --config C2 --page-size 2097152 --steps 5
 run C3 --config C3 --steps 3 --warmup 3 --chunk-mb 1024
-run C4_inc1 --config C4 --mode incremental --dirty 0.01 --steps 5 --chunk-mb 2048
-run C4_inc1_clustered --config C4 --mode incremental --dirty 0.01 --clustered --steps 5 --chunk-mb 2048
-run C4_inc5 --config C4 --mode incremental --dirty 0.05 --steps 5 --chunk-mb 2048
-run C4_inc25 --config C4 --mode incremental --dirty 0.25 --gib 16 --steps 4 --chunk-mb 2048
+run C4_inc1 --config C4 --mode incremental --dirty 0.01 --steps 5 --chunk-mb 1024
+run C4_inc1_clustered --config C4 --mode incremental --dirty 0.01 --clustered --steps 5 --chunk-mb 1024
+run C4_inc5 --config C4 --mode incremental --dirty 0.05 --steps 5 --chunk-mb 1024
+run C4_inc25 --config C4 --mode incremental --dirty 0.25 --gib 16 --steps 4 --chunk-mb 1024
 run C5_16G_P4K --config C5 --gib 16 --page-size 4096 --steps 3 --chunk-mb 1024
 run C5_16G_P64K --config C5 --gib 16 --steps 3 --chunk-mb 1024
 run C5_16G_P2M --config C5 --gib 16 --page-size 2097152 --steps 3 --chunk-mb 1024
