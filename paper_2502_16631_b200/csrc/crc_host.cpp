@@ -85,7 +85,21 @@ void build_tables(CrcTables *t) {
     fill_table(t->a64, 64);
     fill_table(t->a128, 128);
     fill_table(t->a256, 256);
-    for (int j = 0; j < 12; j++) fill_table(t->fold[j], (uint64_t)kRowBytes << j);
+    // fold_m[d] = adv_{512 d}(x^0): x^0 is bit 31 of the reflected register
+    uint32_t row[4][256];
+    fill_table(row, kRowBytes);
+    t->fold_m[0] = 0x80000000u;
+    for (int d = 1; d < 4096; d++) t->fold_m[d] = apply4(row, t->fold_m[d - 1]);
+}
+
+// The reflected GF(2) product K1 evaluates lane-parallel (lane k: v * x^k).
+static uint32_t mulmod(uint32_t m, uint32_t v) {
+    uint32_t r = 0;
+    for (int k = 0; k < 32; k++) {
+        if ((m >> (31 - k)) & 1u) r ^= v;
+        v = (v >> 1) ^ ((v & 1u) ? kPoly : 0u);
+    }
+    return r;
 }
 
 uint32_t zero_digest(uint64_t n) { return mat_vec(adv_matrix(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu; }
@@ -138,10 +152,10 @@ bool crc_self_test() {
     // braid table consistency: adv_512 == (adv_4)^128 on a probe value
     uint32_t v = 0x12345678u, w = v;
     for (int k = 0; k < 128; k++) w = apply4(t->t4, w);
-    // fold tables: adv_{512*2} through fold[1] == braid applied twice
+    // fold products: fold_m[d] (*) v == adv_{512 d}(v) by an independent matrix power
     bool ok = a == 0xE3069283u && b == 0xE3069283u && apply4(t->braid, v) == w &&
-              zero_digest(65536) == 0x72C0C4A4u && apply4(t->fold[0], v) == w &&
-              apply4(t->fold[1], v) == apply4(t->braid, apply4(t->braid, v));
+              zero_digest(65536) == 0x72C0C4A4u && mulmod(t->fold_m[1], v) == w;
+    for (uint32_t d : {0u, 2u, 3u, 127u, 128u, 1000u, 4095u}) ok = ok && mulmod(t->fold_m[d], v) == mat_vec(adv_matrix(512ull * d), v);
     delete t;
     return ok;
 }

@@ -39,6 +39,7 @@ uint64_t ns_since(Clock::time_point t0) {
 
 constexpr uint64_t kMaxChunk = 2ull << 30;
 constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity
+constexpr size_t kDigestChunks = 4;           // checkpoint: chunks per digest D2H
 const char kMagic[8] = {'G', 'C', 'R', 'I', 'M', 'G', 0x00, 0x01};
 
 // ---------------------------------------------------------------------------
@@ -171,6 +172,7 @@ struct gcr_ctx {
 
     cudaStream_t compute = nullptr;
     cudaStream_t post = nullptr;  // K2 compaction + totals, off the scan's critical path
+    cudaStream_t packs = nullptr; // K4 packs, one at a time, feeding the copy streams
     std::vector<cudaStream_t> copy;
     std::vector<uint8_t *> slots;
     CrcTables *tables_d = nullptr;
@@ -188,10 +190,11 @@ struct gcr_ctx {
     uint32_t *D[2] = {nullptr, nullptr};
     uint8_t *cls = nullptr;
     TileInfo *tile_info = nullptr;
-    uint32_t *tile_off = nullptr;
-    Piece *pieces = nullptr;  // 2 per K1 warp, two buffers (chunk parity)
-    uint32_t *contrib = nullptr;
-    uint64_t pieces_per_buf = 0;
+    uint64_t *chunk_rows_d = nullptr;  // chunk row boundaries (nch + 1), then {0, n_rows} for verify
+    uint32_t *chunk_sync_d = nullptr;  // per chunk: K1 arrival counter [0, nch), chunk_done [nch, 2 nch)
+    uint32_t epoch = 0;                // K1 launch id published in chunk_done
+    uint32_t *fold_slots = nullptr;  // K1's cut-page fold: 2 words per K1 warp, zero between launches
+    FoldSlots fold{};
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
     ChunkTotals *totals_h = nullptr, *totals_map = nullptr;  // mapped pinned, written by K2
@@ -199,7 +202,8 @@ struct gcr_ctx {
     unsigned long long *nent_h = nullptr, *nent_map = nullptr;  // mapped pinned n_entries
     TileRec *tile_rec_h = nullptr, *tile_rec_map = nullptr;     // mapped pinned non-empty tile records
     unsigned long long *rec_count_h = nullptr, *rec_count_map = nullptr;  // per chunk: records written
-    uint8_t *pack_flags_h = nullptr, *pack_flags_d = nullptr;   // per-tile: packed (1) or direct (0)
+    uint8_t *pack_flags_h = nullptr;   // per-tile plan scratch: packed (1) or direct (0)
+    StageItem *stage_h = nullptr, *stage_map = nullptr;  // mapped pinned K4 work lists, indexed by global tile
     uint32_t z_page = 0;
 
     // restore descriptor buffers (grow on demand)
@@ -261,8 +265,8 @@ bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P
 
 void free_layout(gcr_ctx *c) {
     void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
-                    c->tile_off, c->pieces, c->contrib, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
-                    c->entries_d, c->misc_d, c->pack_flags_d};
+                    c->chunk_rows_d, c->chunk_sync_d, c->fold_slots, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
+                    c->entries_d, c->misc_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->totals_h) cudaFreeHost(c->totals_h);
@@ -272,17 +276,19 @@ void free_layout(gcr_ctx *c) {
     if (c->rec_count_h) cudaFreeHost(c->rec_count_h);
     c->rec_count_h = c->rec_count_map = nullptr;
     if (c->pack_flags_h) cudaFreeHost(c->pack_flags_h);
+    if (c->stage_h) cudaFreeHost(c->stage_h);
+    c->stage_h = c->stage_map = nullptr;
     c->tile_rec_h = c->tile_rec_map = nullptr;
-    c->pack_flags_h = c->pack_flags_d = nullptr;
+    c->pack_flags_h = nullptr;
     c->nent_h = c->nent_map = nullptr;
     c->totals_map = nullptr;
     c->allocs_d = nullptr;
     c->page_alloc = c->tile_alloc = c->D[0] = c->D[1] = nullptr;
     c->cls = nullptr;
     c->tile_info = nullptr;
-    c->tile_off = nullptr;
-    c->pieces = nullptr;
-    c->contrib = nullptr;
+    c->chunk_rows_d = nullptr;
+    c->chunk_sync_d = nullptr;
+    c->fold_slots = nullptr;
     c->pm_blk_cnt = c->pm_blk_off = c->run_start = nullptr;
     c->entries_d = nullptr;
     c->totals_h = nullptr;
@@ -365,11 +371,25 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaMalloc(&c->D[1], 4 * g));
     CUDA_TRY(c, cudaMalloc(&c->cls, g));
     CUDA_TRY(c, cudaMalloc(&c->tile_info, sizeof(TileInfo) * t));
-    CUDA_TRY(c, cudaMalloc(&c->tile_off, 4 * t));
     CUDA_TRY(c, cudaMemset(c->tile_info, 0, sizeof(TileInfo) * t));
-    c->pieces_per_buf = 2 * scan_workers(~0ull >> 8, c->n_sms);
-    CUDA_TRY(c, cudaMalloc(&c->pieces, sizeof(Piece) * 2 * c->pieces_per_buf));
-    CUDA_TRY(c, cudaMalloc(&c->contrib, sizeof(uint32_t) * 2 * c->pieces_per_buf));
+    {
+        std::vector<uint64_t> cr;
+        for (const Chunk &ch : c->chunks) cr.push_back(ch.row_begin);
+        cr.push_back(rows);
+        cr.push_back(0);
+        cr.push_back(rows);
+        CUDA_TRY(c, cudaMalloc(&c->chunk_rows_d, 8 * cr.size()));
+        CUDA_TRY(c, cudaMemcpy(c->chunk_rows_d, cr.data(), 8 * cr.size(), cudaMemcpyHostToDevice));
+        const uint64_t ns = std::max<uint64_t>(nch, 1);
+        CUDA_TRY(c, cudaMalloc(&c->chunk_sync_d, 2 * 4 * ns));
+        CUDA_TRY(c, cudaMemset(c->chunk_sync_d, 0, 2 * 4 * ns));
+        // fold slots: one pair per K1 warp per chunk (warps run ahead into later
+        // chunks independently, so chunks never share slots)
+        const uint64_t w = scan_workers(c->n_sms) * ns;
+        CUDA_TRY(c, cudaMalloc(&c->fold_slots, 2 * 4 * w));
+        CUDA_TRY(c, cudaMemset(c->fold_slots, 0, 2 * 4 * w));
+        c->fold = FoldSlots{c->fold_slots, c->fold_slots + w};
+    }
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_cnt, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->run_start, 4 * g));
@@ -382,7 +402,8 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->rec_count_map), c->rec_count_h, 0));
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->tile_rec_map), c->tile_rec_h, 0));
     CUDA_TRY(c, cudaHostAlloc(&c->pack_flags_h, t, cudaHostAllocDefault));
-    CUDA_TRY(c, cudaMalloc(&c->pack_flags_d, t));
+    CUDA_TRY(c, cudaHostAlloc(&c->stage_h, sizeof(StageItem) * t, cudaHostAllocMapped));
+    CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->stage_map), c->stage_h, 0));
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->nent_map), c->nent_h, 0));
     CUDA_TRY(c, cudaMalloc(&c->misc_d, 8 * 4));
     CUDA_TRY(c, cudaHostAlloc(&c->misc_h, 8 * 4, cudaHostAllocDefault));
@@ -400,6 +421,7 @@ gcr_status build_layout(gcr_ctx *c) {
 void sync_all(gcr_ctx *c) {
     cudaStreamSynchronize(c->compute);
     if (c->post) cudaStreamSynchronize(c->post);
+    if (c->packs) cudaStreamSynchronize(c->packs);
     for (cudaStream_t s : c->copy) cudaStreamSynchronize(s);
     cudaGetLastError();
 }
@@ -523,6 +545,7 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     if (cudaStreamCreateWithFlags(&c->post, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
+    if (cudaStreamCreateWithFlags(&c->packs, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     for (uint32_t i = 0; i < cfg.n_copy_streams; i++) {
         cudaStream_t s;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
@@ -557,6 +580,7 @@ gcr_status gcr_destroy(gcr_ctx *c) {
     for (cudaStream_t s : c->copy) cudaStreamDestroy(s);
     if (c->compute) cudaStreamDestroy(c->compute);
     if (c->post) cudaStreamDestroy(c->post);
+    if (c->packs) cudaStreamDestroy(c->packs);
     if (c->tables_d) cudaFree(c->tables_d);
     if (c->desc_d) cudaFree(c->desc_d);
     if (c->desc_h) cudaFreeHost(c->desc_h);
@@ -695,8 +719,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     ScanParams sp{};
     sp.allocs = c->allocs_d;
     sp.n_allocs = (uint32_t)c->allocs_h.size();
-    sp.pieces = c->pieces;
-    sp.contrib = c->contrib;
+    sp.fold = c->fold;
     sp.page_size = P;
     sp.log2_page = c->lg;
     sp.z_page = c->z_page;
@@ -708,83 +731,46 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.tables = c->tables_d;
 
     const size_t nch = c->chunks.size();
-    // Scan groups: K1 launch g covers chunks [grp[g], grp[g+1]) -- 1, 1, 2,
-    // then 4 chunks: the first drain starts after a small scan, later scans are
-    // long launches (their fixed cost amortised), the drain stays per chunk.
-    // Sizes ramp up (1, 1, 2, 4, ...) so the first drain starts early and
-    // down again at the end (..., 4, 2, 1, 1) so the drain of the last group
-    // -- which can only start once that group is scanned -- is short.
-    std::vector<size_t> grp{0};
-    {
-        // (ramp down only for incremental checkpoints: a full checkpoint is drain
-        // bound by ~50x, so its tail is the drain anyway and fewer launches win)
-        const bool ramp_down = mode == GCR_INCREMENTAL;
-        std::vector<size_t> ramp{1, 1, 2, 4}, head, tail;
-        size_t left = nch;
-        for (size_t k = 0; k < ramp.size() && left; k++) {
-            const size_t a = std::min(ramp[k], left);
-            head.push_back(a);
-            left -= a;
-            if (!left || !ramp_down) continue;
-            const size_t b = std::min(ramp[k], left);
-            tail.push_back(b);
-            left -= b;
-        }
-        // at most 4 chunks per scan: larger groups deliver chunks to the drain in
-        // bursts (measured: 8 -> 11.0 ms, 4 -> 10.6 ms on C4 1%); GCR_SCAN_GROUP_MAX overrides
-        static const size_t gmax = std::getenv("GCR_SCAN_GROUP_MAX") ? std::atoi(std::getenv("GCR_SCAN_GROUP_MAX")) : 4;
-        for (; left; left -= std::min<size_t>(gmax, left)) head.push_back(std::min<size_t>(gmax, left));
-        for (size_t k = tail.size(); k-- > 0;) head.push_back(tail[k]);
-        for (size_t h : head) grp.push_back(grp.back() + h);
-    }
-    const size_t ngrp = grp.size() - 1;
-    std::vector<cudaEvent_t> k1s(ngrp), k1m(ngrp), k1e(ngrp), k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
+    // One persistent K1 for the whole registry, walking the chunks in order;
+    // K2(i) is enqueued ahead on the post stream and waits on K1's per-chunk
+    // publication, so chunk i reaches the drain ~one chunk's scan after it
+    // was scanned (no per-launch ramp and tail, no launch gaps: under a
+    // saturated D2H every launch or event the GPU front-end fetches from host
+    // memory costs tens of us).
+    sp.chunk_rows = c->chunk_rows_d;
+    sp.n_chunks = (uint32_t)nch;
+    sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;  // never 0 (the flags' initial value)
+    sp.chunk_arrive = c->chunk_sync_d;
+    sp.chunk_done = c->chunk_sync_d + std::max<size_t>(nch, 1);
+    sp.workers = scan_workers(c->n_sms);
+    std::vector<cudaEvent_t> k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
-    cudaEvent_t t0 = c->ev();
+    cudaEvent_t t0 = c->ev(), k1s = c->ev(), k1m = c->ev();
     CUDA_TRY(c, cudaEventRecord(t0, c->compute));
-    // K1 on the compute stream; K1b (fold) and K2 (per chunk: image offsets,
-    // non-empty tile records and chunk totals straight into mapped pinned
-    // memory) on the post stream, beside the next scan.  Planning the drain
-    // therefore never waits on a DMA queued behind the previous drain.  Two
-    // scan groups are kept enqueued ahead of the drain (enqueueing everything
-    // up front delayed the first drain by ~0.5 ms of API calls).
-    size_t enqueued = 0;  // scan groups enqueued
-    auto enqueue_group = [&](size_t g) -> gcr_status {
-        const Chunk &c0 = c->chunks[grp[g]], &c1 = c->chunks[grp[g + 1] - 1];
-        sp.tile_begin = c0.tile_begin;
-        sp.tile_end = c1.tile_end;
-        sp.row_begin = c0.row_begin;
-        sp.row_end = c1.row_end;
-        sp.workers = scan_workers(sp.row_end - sp.row_begin, c->n_sms);
-        // pieces are double-buffered by group parity so K1 of the next group can
-        // run while K1b folds this one
-        sp.pieces = c->pieces + (g & 1) * c->pieces_per_buf;
-        sp.contrib = c->contrib + (g & 1) * c->pieces_per_buf;
-        k1s[g] = c->ev();
-        k1m[g] = c->ev();
-        k1e[g] = c->ev();
-        if (g >= 2)  // K1(g) overwrites the buffer K1b(g-2) read
-            CUDA_TRY(c, cudaStreamWaitEvent(c->compute, k1e[g - 2], 0));
-        CUDA_TRY(c, cudaEventRecord(k1s[g], c->compute));
-        LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
-        CUDA_TRY(c, cudaEventRecord(k1m[g], c->compute));
-        CUDA_TRY(c, cudaStreamWaitEvent(c->post, k1m[g], 0));
-        LAUNCH_TRY(c, launch_fold(sp, c->n_sms, c->post));
-        CUDA_TRY(c, cudaEventRecord(k1e[g], c->post));
-        for (size_t i = grp[g]; i < grp[g + 1]; i++) {
-            const Chunk &ch = c->chunks[i];
-            k2s[i] = c->ev();
-            tot[i] = c->ev();
-            CUDA_TRY(c, cudaEventRecord(k2s[i], c->post));
-            LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, c->tile_off,
-                                           c->tile_rec_map + ch.tile_begin, c->rec_count_map + i,
-                                           c->totals_map + i, c->post));
-            CUDA_TRY(c, cudaEventRecord(tot[i], c->post));
-        }
+    const Clock::time_point host0 = Clock::now();  // trace: host enqueue times relative to t0
+    std::vector<double> host_seen(trace ? nch : 0), host_enq(trace ? nch : 0);
+    CUDA_TRY(c, cudaEventRecord(k1s, c->compute));
+    LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
+    CUDA_TRY(c, cudaEventRecord(k1m, c->compute));
+    // K2 (per chunk: image offsets, non-empty tile records and chunk totals
+    // straight into mapped pinned memory) on the post stream, beside the scan:
+    // planning the drain never waits on a DMA queued behind the previous
+    // drain.  Kept 3 chunks ahead of the drain (enqueueing everything up front
+    // delays the first drain by the API calls).
+    size_t enqueued = 0;  // K2s enqueued
+    auto enqueue_k2 = [&](size_t i) -> gcr_status {
+        const Chunk &ch = c->chunks[i];
+        k2s[i] = c->ev();
+        tot[i] = c->ev();
+        CUDA_TRY(c, cudaEventRecord(k2s[i], c->post));
+        LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, sp.chunk_done, (uint32_t)i, sp.epoch,
+                                       c->tile_rec_map + ch.tile_begin, c->rec_count_map + i, c->totals_map + i,
+                                       c->post));
+        CUDA_TRY(c, cudaEventRecord(tot[i], c->post));
         return GCR_OK;
     };
-    for (; enqueued < std::min<size_t>(ngrp, 3); enqueued++) {
-        gcr_status es = enqueue_group(enqueued);
+    for (; enqueued < std::min<size_t>(nch, 3); enqueued++) {
+        gcr_status es = enqueue_k2(enqueued);
         if (es != GCR_OK) return es;
     }
     // Drain: as each chunk's records land, plan it -- runs of fully PRESENT
@@ -801,12 +787,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     };
     std::vector<Run> direct;
     std::vector<std::pair<uint64_t, uint64_t>> staged;  // chunk-local image ranges [lo, hi)
+    size_t dg0 = 0;                                     // first chunk of the pending digest D2H
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         CUDA_TRY(c, cudaEventSynchronize(tot[i]));
-        // keep two scan groups ahead of the drain
-        while (enqueued < ngrp && i >= grp[enqueued - 2]) {  // keep two groups beyond the one draining
-            gcr_status es = enqueue_group(enqueued++);
+        if (trace) host_seen[i] = ns_since(host0) * 1e-6;
+        for (; enqueued < std::min(nch, i + 4); enqueued++) {
+            gcr_status es = enqueue_k2(enqueued);
             if (es != GCR_OK) return es;
         }
         ChunkTotals T;
@@ -817,11 +804,14 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         n_present += T.n_present;
         n_zero += T.n_zero;
         n_parent += T.n_parent;
+        if (T.image_bytes == ~0ull) return fail(c, GCR_E_CUDA, "checkpoint: scan did not publish a chunk in time");
         if (base + T.image_bytes > R) return fail(c, GCR_E_CUDA, "checkpoint: image larger than registry");
         // ---- plan (host walk of the chunk's tiles) ----
         direct.clear();
         staged.clear();
         uint8_t *flags = c->pack_flags_h + ch.tile_begin;
+        StageItem *items = c->stage_h + ch.tile_begin;
+        uint32_t n_items = 0;
         bool any_staged = false;
         if (T.image_bytes) {
             std::memset(flags, 0, ch.tile_end - ch.tile_begin);
@@ -880,10 +870,17 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                 }
             }
             close();
-            if (any_staged) {  // contiguous image ranges of consecutive staged (non-empty) tiles
+            if (any_staged) {  // K4's items, and contiguous image ranges of consecutive staged tiles
                 for (uint64_t k = 0; k < nrec; k++) {
-                    if (!flags[rec[4 * k]]) continue;
-                    const uint64_t lo = rec[4 * k + 2], len = rec[4 * k + 1];
+                    const uint32_t rt = rec[4 * k];
+                    if (!flags[rt]) continue;
+                    const uint32_t lo = rec[4 * k + 2], len = rec[4 * k + 1];
+                    if (P <= kTileBytes) {
+                        items[n_items++] = StageItem{rt, lo};
+                    } else {  // the anchor's record covers the whole page: one item per 64 KiB slice
+                        for (uint32_t j = 0; (uint64_t)j * kTileBytes < len; j++)
+                            items[n_items++] = StageItem{rt + j, lo + j * kTileBytes};
+                    }
                     if (!staged.empty() && staged.back().second == lo) staged.back().second += len;
                     else staged.emplace_back(lo, lo + len);
                 }
@@ -892,17 +889,26 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         // ---- execute on copy stream i mod S ----
         cudaStream_t cs = c->copy[i % S];
         if (i == 0) drain0 = Clock::now();
-        CUDA_TRY(c, cudaStreamWaitEvent(cs, tot[i], 0));
+        if (trace) host_enq[i] = ns_since(host0) * 1e-6;
+        // Packs run one at a time on their own stream (two concurrent packs,
+        // 16 CTAs, overflowed the SMs K1 leaves free and pushed the running
+        // scan into a second wave: 0.1 -> 0.2 ms on C2's last group), after
+        // K2(i) and once slot i mod S is drained; the copy streams then carry
+        // only D2Hs.  The drains share one host link, so serialising the packs
+        // costs nothing.
         pks[i] = c->ev();
         pke[i] = c->ev();
-        CUDA_TRY(c, cudaEventRecord(pks[i], cs));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->packs, tot[i], 0));
         if (any_staged) {
-            CUDA_TRY(c, cudaMemcpyAsync(c->pack_flags_d + ch.tile_begin, flags, ch.tile_end - ch.tile_begin,
-                                        cudaMemcpyHostToDevice, cs));
-            LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, c->tile_off, ch.tile_begin, ch.tile_end, P,
-                                      c->lg, c->slots[i % S], c->pack_flags_d + ch.tile_begin, c->n_sms, cs));
+            if (i >= S) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - S], 0));
+            CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
+            LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, ch.tile_begin, P, c->lg, c->slots[i % S],
+                                      c->stage_map + ch.tile_begin, n_items, c->n_sms, c->packs));
+        } else {
+            CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
         }
-        CUDA_TRY(c, cudaEventRecord(pke[i], cs));
+        CUDA_TRY(c, cudaEventRecord(pke[i], c->packs));
+        CUDA_TRY(c, cudaStreamWaitEvent(cs, pke[i], 0));
         for (const auto &rg : staged) {
             CUDA_TRY(c, cudaMemcpyAsync(img->data + base + rg.first, c->slots[i % S] + rg.first, rg.second - rg.first,
                                         cudaMemcpyDeviceToHost, cs));
@@ -913,13 +919,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                                         cudaMemcpyDeviceToHost, cs));
             direct_bytes += rn.bytes;
         }
-        // the digests of a whole scan group in one DMA, after its last chunk
-        // (one small DMA per chunk cost ~10% of the drain at 1% dirty)
-        if (i + 1 == grp[std::upper_bound(grp.begin(), grp.end(), i) - grp.begin()]) {
-            const size_t g = std::upper_bound(grp.begin(), grp.end(), i) - grp.begin() - 1;
-            const uint64_t pb = c->chunks[grp[g]].page_begin, pe = ch.page_end;
+        // the digests of every kDigestChunks chunks in one DMA (one small DMA per
+        // chunk cost ~10% of the drain at 1% dirty)
+        if (i + 1 - dg0 == kDigestChunks || i + 1 == nch) {
+            const uint64_t pb = c->chunks[dg0].page_begin, pe = ch.page_end;
             if (pe > pb)
                 CUDA_TRY(c, cudaMemcpyAsync(img->digests + pb, Dnew + pb, 4 * (pe - pb), cudaMemcpyDeviceToHost, cs));
+            dg0 = i + 1;
         }
         dde[i] = c->ev();
         CUDA_TRY(c, cudaEventRecord(dde[i], cs));
@@ -929,9 +935,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     st.direct_bytes = direct_bytes;
     c->pool.shrink(img->data, img->data_cap, base);  // the tail is free before the pagemap is allocated
     img->data_cap = base;
-    // K3 pagemap over all pages (maximal runs, independent of chunking); the
-    // classes of cut pages are final only after the last K1b (post stream).
-    CUDA_TRY(c, cudaStreamWaitEvent(c->compute, tot[nch - 1], 0));
+    // K3 pagemap over all pages (maximal runs, independent of chunking): every
+    // class is final once the last K1 (same stream) has ended.
     auto pm0 = c->ev(), pm1 = c->ev();
     CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
     LAUNCH_TRY(c, launch_pagemap_count(c->cls, c->n_pages, c->pm_blk_cnt, c->pm_blk_off, c->nent_map, c->compute));
@@ -958,10 +963,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     float ms;
     st.scan_dev_ns = 0;
     st.pack_dev_ns = 0;
-    for (size_t g = 0; g < ngrp; g++) {
-        CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s[g], k1m[g]));  // K1 proper (K1b runs on the post stream)
-        st.scan_dev_ns += (uint64_t)(ms * 1e6);
-    }
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, k1s, k1m));
+    st.scan_dev_ns = (uint64_t)(ms * 1e6);
     for (size_t i = 0; i < nch; i++) {
         CUDA_TRY(c, cudaEventElapsedTime(&ms, pks[i], pke[i]));
         st.pack_dev_ns += (uint64_t)(ms * 1e6);
@@ -974,19 +977,17 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             cudaEventElapsedTime(&m, t0, e);
             return m;
         };
-        std::fprintf(stderr, "{\"gcr_trace\": \"checkpoint\", \"scans\": [");
-        for (size_t g = 0; g < ngrp; g++)
-            std::fprintf(stderr, "%s[%zu, %zu, %.3f, %.3f, %.3f]", g ? ", " : "", grp[g], grp[g + 1], rel(k1s[g]),
-                         rel(k1m[g]), rel(k1e[g]));
+        std::fprintf(stderr, "{\"gcr_trace\": \"checkpoint\", \"scans\": [[0, %zu, %.3f, %.3f]", nch, rel(k1s),
+                     rel(k1m));
         std::fprintf(stderr, "], \"chunks\": [");
         for (size_t i = 0; i < nch; i++)
-            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k2s[i]), rel(tot[i]),
-                         rel(pks[i]), rel(pke[i]), rel(dde[i]));
+            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k2s[i]),
+                         rel(tot[i]), rel(pks[i]), rel(pke[i]), rel(dde[i]), host_seen[i], host_enq[i]);
         std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": {\"scans\": \"chunk_lo chunk_hi k1_start "
-                             "k1_end k1b_end\", \"chunks\": \"k2_start k2_end pack_start pack_end d2h_end\"}}\n",
+                             "k1_end\", \"chunks\": \"k2_start k2_end pack_start pack_end d2h_end host_saw_k2 host_enqueued\"}}\n",
                      rel(pm0), rel(pm1));
     }
-    st.scan_launches = ngrp;
+    st.scan_launches = 1;
     st.scan_bytes = R;
     st.pages_scanned = c->n_pages;
     st.pages_zero = n_zero;
@@ -1047,6 +1048,11 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
         sync_all(c);
         // re-arm the per-launch device state the kernels leave zeroed on success
         cudaMemset(c->tile_info, 0, sizeof(TileInfo) * c->n_tiles);
+        {
+            const uint64_t ns = std::max<size_t>(c->chunks.size(), 1);
+            cudaMemset(c->chunk_sync_d, 0, 2 * 4 * ns);
+            cudaMemset(c->fold_slots, 0, 2 * 4 * scan_workers(c->n_sms) * ns);
+        }
         cudaGetLastError();
         image_free_buffers(img);
         delete img;
@@ -1257,13 +1263,14 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         ScanParams sp{};
         sp.allocs = c->allocs_d;
         sp.n_allocs = (uint32_t)c->allocs_h.size();
-        sp.pieces = c->pieces;
-        sp.contrib = c->contrib;
-        sp.row_begin = 0;
-        sp.row_end = c->n_rows;
-        sp.workers = scan_workers(c->n_rows, c->n_sms);
-        sp.tile_begin = 0;
-        sp.tile_end = c->n_tiles;
+        sp.fold = c->fold;
+        const size_t nch = c->chunks.size();
+        sp.chunk_rows = c->chunk_rows_d + nch + 1;  // one chunk: every real row
+        sp.n_chunks = 1;
+        sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;
+        sp.chunk_arrive = c->chunk_sync_d;
+        sp.chunk_done = c->chunk_sync_d + std::max<size_t>(nch, 1);
+        sp.workers = scan_workers(c->n_sms);
         sp.page_size = P;
         sp.log2_page = c->lg;
         sp.z_page = c->z_page;
@@ -1274,7 +1281,6 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.tables = c->tables_d;
         CUDA_TRY(c, cudaEventRecord(v0, c->compute));
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
-        LAUNCH_TRY(c, launch_fold(sp, c->n_sms, c->compute));
         CUDA_TRY(c, cudaEventRecord(v1, c->compute));
         CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));
         verify_launches = 1;

@@ -35,12 +35,15 @@ struct AllocDev {
     uint64_t n_rows;    // (n_pages-1)*P/512 + ceil(tail_len/512)
 };
 
-// Partial raw register of a page cut by a K1 warp-range boundary (folded by K1b).
-struct Piece {
-    unsigned long long page;  // global page index, ~0 = empty slot
-    uint32_t alloc;
-    uint32_t vr_begin, vr_end;  // virtual rows [vr_begin, vr_end) of the page
-    uint32_t raw, nz;
+// A page cut by K1 warp-range boundaries is folded inside K1: every warp
+// holding a piece of it XORs the piece's contribution into the page's owner
+// slot (owner = the warp whose range holds the page's first real row), then
+// adds its row count (low 16 bits) and non-zero flag (<< 16) to the owner's
+// counter; the warp whose add completes the page's rows finalizes it and
+// re-zeroes both slots.  One slot pair per K1 warp.
+struct FoldSlots {
+    uint32_t *x;  // XOR of the contributions adv_{512 (Rp - vr_end)}(raw)
+    uint32_t *c;  // rows | n_nonzero_pieces << 16
 };
 
 // Per-tile result of the scan used by compaction (K2) and pack (K4).
@@ -55,6 +58,14 @@ struct TileRec {
     uint32_t present_bytes;  // PRESENT bytes anchored at the tile
     uint32_t image_off;      // chunk-local image offset of the tile's first PRESENT byte
     uint32_t pad;
+};
+
+// One staged tile for K4 (host-written, mapped pinned): the chunk-local tile
+// and the slot offset of its first PRESENT byte (for a page > 64 KiB: of the
+// slice itself).
+struct StageItem {
+    uint32_t tile;
+    uint32_t dst;
 };
 
 struct ChunkTotals {
@@ -73,17 +84,27 @@ struct CrcTables {
     uint32_t a64[4][256];    // d = 64  (level 2)
     uint32_t a128[4][256];   // d = 128 (level 3)
     uint32_t a256[4][256];   // d = 256 (level 4)
-    uint32_t fold[12][4][256];  // d = 512 * 2^j: arbitrary row-distance folds of K1b
+    // fold_m[d] = x^(8 * 512 d) mod P in the reflected representation (x^0 =
+    // 0x80000000), d < 4096 rows: a piece ending d rows before its page's end
+    // contributes fold_m[d] (*) raw, a GF(2) product K1 forms lane-parallel.
+    uint32_t fold_m[4096];
 };
 
+// K1 is ONE persistent launch per checkpoint (or verify): every warp walks
+// the chunks in order, taking its equal share of each chunk's real rows.  The
+// last warp to finish chunk c publishes chunk_done[c] = epoch, on which K2(c),
+// enqueued ahead on the post stream, waits -- no launch boundary, host
+// round-trip or launch latency between a chunk's scan and its compaction.
 struct ScanParams {
     const AllocDev *allocs;
     uint32_t n_allocs;
-    uint64_t row_begin, row_end;   // chunk: global real rows (page aligned)
-    uint64_t workers;              // warps sharing the rows equally
-    Piece *pieces;                 // 2 per warp
-    uint32_t *contrib;             // 2 per warp: piece contribution adv_{(Rp-vend)*512}(raw)
-    uint64_t tile_begin, tile_end; // chunk: tiles (compaction)
+    const uint64_t *chunk_rows;    // n_chunks + 1 global real-row boundaries (page aligned), device
+    uint32_t n_chunks;
+    uint32_t epoch;                // this launch's id, published in chunk_done (never 0)
+    uint32_t *chunk_arrive;        // per chunk: warps done (the last one re-zeroes it)
+    uint32_t *chunk_done;          // per chunk: epoch of the launch that last completed it
+    uint64_t workers;              // warps; every chunk is split among all of them
+    FoldSlots fold;                // workers slot pairs per chunk
     uint32_t page_size, log2_page;
     uint32_t z_page;
     int mode;
@@ -113,15 +134,15 @@ struct ZeroDesc {
 int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t *page_alloc,
                             uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
                             cudaStream_t st);
-uint64_t scan_workers(uint64_t rows, int n_sms);
+uint64_t scan_workers(int n_sms);                                   // K1 warps (a full persistent grid)
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1
-int launch_fold(const ScanParams &p, int n_sms, cudaStream_t st);  // K1b (must follow K1 on st)
-int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, uint32_t *tile_off,
-                     TileRec *host_rec, unsigned long long *rec_count, ChunkTotals *totals_host, cudaStream_t st);
-int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls,
-                const uint32_t *tile_off, uint64_t tile_begin, uint64_t tile_end,
-                uint32_t page_size, uint32_t log2_page, uint8_t *slot, const uint8_t *pack_flags, int n_sms,
-                cudaStream_t st);
+// K2 of one chunk: first waits (bounded) until chunk_done[chunk] == epoch.
+int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, const uint32_t *chunk_done,
+                     uint32_t chunk, uint32_t epoch, TileRec *host_rec, unsigned long long *rec_count,
+                     ChunkTotals *totals_host, cudaStream_t st);
+int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tile_begin,
+                uint32_t page_size, uint32_t log2_page, uint8_t *slot, const StageItem *items, uint32_t n_items,
+                int n_sms, cudaStream_t st);
 // Pagemap over all pages: phase 1 counts run starts per block and scans them,
 // writing the entry count to *n_entries_dev; phase 2 writes the entries.
 int launch_pagemap_count(const uint8_t *cls, uint64_t n_pages, uint32_t *blk_cnt, uint32_t *blk_off,

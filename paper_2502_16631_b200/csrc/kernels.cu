@@ -4,8 +4,6 @@
 //  K0  build_page_table  A1: page -> allocation, tile -> allocation maps
 //  K1  scan              A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
 //                        all-zero test, dirty diff, class, tile counters
-//  K1b fold_contrib/final  pages cut by a warp's range boundary: fold the
-//                        partial registers
 //  K2  tile_scan         A5: chunk-local exclusive scan of PRESENT bytes per
 //                        tile (the pack's destination offsets) and chunk totals
 //  K3  pagemap_*         A5: maximal runs -> CRIU-style pagemap entries
@@ -36,8 +34,10 @@
 // quantization) and every page event is warp-uniform (no divergence).  A warp
 // streams its range continuously across page and allocation boundaries with
 // the next block of rows always in flight: a LOAD cursor walks contiguous
-// address runs, a PROCESS cursor finalizes pages.  Pages cut by a range
-// boundary leave PIECES that K1b folds.
+// address runs, a PROCESS cursor finalizes pages.  A page cut by range
+// boundaries is folded in K1 itself: each piece is advanced to the page end
+// (one GF(2) product with fold_m[d], lane-parallel) and XORed into the page's
+// owner slot; the piece that completes the page's rows finalizes it.
 #include <cstdio>
 
 #include "gcr_internal.h"
@@ -49,7 +49,6 @@ namespace {
 constexpr uint32_t kBraidSmem = 4u * 256u * 32u * 4u;  // 128 KiB
 constexpr uint32_t kSmallTables = 6;                   // t4 a16 a32 a64 a128 a256
 constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u;
-constexpr uint32_t kFoldTables = 12;  // adv_{512 * 2^j}, j < 12: row distances < 4096 (P <= 2 MiB)
 constexpr uint32_t kLog2Row = 9;
 #ifndef GCR_SCAN_THREADS
 #define GCR_SCAN_THREADS 640
@@ -166,6 +165,54 @@ __device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, u
     p.cls[g] = c | (alloc_start ? kClsAllocStart : 0);
 }
 
+// GF(2) product m (*) v mod P in the reflected representation (bit 31 = x^0):
+// the sum over the set bits 31-k of m of v * x^k.  Lane k forms v * x^k (k
+// single-bit register steps, predicated so the loop is warp-uniform), and a
+// 5-level XOR butterfly sums the lanes.  All lanes return the product.
+__device__ __forceinline__ uint32_t warp_mulmod(uint32_t m, uint32_t v, uint32_t lane) {
+    constexpr uint32_t kPoly = 0x82F63B78u;
+#pragma unroll 1
+    for (uint32_t s = 0; s < 31; s++)
+        if (s < lane) v = (v >> 1) ^ ((v & 1u) ? kPoly : 0u);
+    uint32_t t = (m >> (31u - lane)) & 1u ? v : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t ^= __shfl_xor_sync(kFull, t, o);
+    return t;
+}
+
+// The chunk a warp is scanning: its real rows and its fold slots.
+struct ChunkCtx {
+    uint64_t rb, rows;  // first global real row, real rows
+    uint32_t *fx, *fc;  // fold slots of this chunk (one pair per warp)
+};
+
+// A piece of a cut page arrives at the page's owner slot (executed by one
+// lane).  The piece's contribution is already advanced to the page end.  The
+// arrival that completes the page's Rp - r0 real rows finalizes it.  Release:
+// the XOR is fenced before the counter add; acquire: fence after observing
+// the full count, then read-and-clear the XOR.
+__device__ __forceinline__ void fold_arrive(const ScanParams &p, const ChunkCtx &cc, uint64_t g, uint32_t a,
+                                            uint32_t pi, uint32_t r0, uint32_t rows, uint32_t contrib, bool nz) {
+    const uint32_t P = p.page_size, lg = p.log2_page, Rp = P >> kLog2Row;
+    const AllocDev *al = p.allocs + a;
+    // owner: the last warp whose range starts at or before the page's first
+    // real row; ranges are [rows*w/W, rows*(w+1)/W) relative to the chunk
+    const uint64_t x = __ldg(&al->row0) + (uint64_t)pi * Rp - cc.rb;
+    const uint64_t owner = ((x + 1) * p.workers - 1) / cc.rows;
+    atomicXor(cc.fx + owner, contrib);
+    __threadfence();
+    const uint32_t add = rows | (nz ? 1u << 16 : 0u);
+    const uint32_t tot = atomicAdd(cc.fc + owner, add) + add;
+    if ((tot & 0xFFFFu) != Rp - r0) return;
+    __threadfence();
+    const uint32_t raw = atomicExch(cc.fx + owner, 0u);
+    atomicExch(cc.fc + owner, 0u);
+    const uint32_t n_pages = __ldg(&al->n_pages);
+    const bool tail = pi == n_pages - 1;
+    finalize_page(p, g, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, tail ? __ldg(&al->tail_len) : P,
+                  tail ? __ldg(&al->z_tail) : p.z_page, raw, (tot >> 16) != 0u);
+}
+
 // Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
 __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
                                                                    unsigned long long *total) {
@@ -197,25 +244,59 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
     return res;
 }
 
-// K2: chunk-local exclusive scan of PRESENT bytes over the chunk's tiles ->
-// tile_off (the pack's destination offsets); re-zeroes the tile counters;
-// writes the chunk totals and the NON-EMPTY tiles, compacted, into mapped
-// pinned host memory ({tile, present bytes, image offset}; count in
-// rec_count) so the host plans the drain from ~d*T records instead of T.  One
-// CTA: the chunk's counters are staged in shared memory with coalesced loads,
-// each thread then scans a contiguous run of tiles.  Runs on the post stream,
-// beside the next scan, on the SMs the scan leaves free.
+// K2: chunk-local exclusive scan of PRESENT bytes over the chunk's tiles;
+// re-zeroes the tile counters; writes the chunk totals and the NON-EMPTY
+// tiles, compacted, into mapped pinned host memory ({tile, present bytes,
+// image offset}; count in rec_count) so the host plans the drain from ~d*T
+// records instead of T.  One CTA: the chunk's counters are staged in shared
+// memory with coalesced loads, each thread then scans a contiguous run of
+// tiles.  Enqueued ahead on the post stream; it first waits until the
+// persistent K1 publishes the chunk (chunk_done[chunk] == epoch), bounded by
+// kChunkWaitNs (a timeout reports image_bytes = ~0 and the checkpoint fails).
 constexpr int kTileScanThreads = 1024;
+constexpr uint64_t kChunkWaitNs = 30ull * 1000000000ull;
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te,
-                                                                uint32_t *tile_off, TileRec *host_rec,
+                                                                const uint32_t *chunk_done, uint32_t chunk,
+                                                                uint32_t epoch, TileRec *host_rec,
                                                                 unsigned long long *rec_count,
                                                                 ChunkTotals *totals_host) {
     extern __shared__ uint32_t pb[];  // present bytes per tile of the chunk
+    __shared__ int timed_out;
+    if (threadIdx.x == 0) {
+        const uint64_t t0 = globaltimer_ns();
+        int to = 0;
+        while (*reinterpret_cast<const volatile uint32_t *>(chunk_done + chunk) != epoch) {
+            if (globaltimer_ns() - t0 > kChunkWaitNs) {
+                to = 1;
+                break;
+            }
+            __nanosleep(200);
+        }
+        __threadfence();
+        timed_out = to;
+    }
+    __syncthreads();
+    if (timed_out) {
+        if (threadIdx.x == 0) {
+            reinterpret_cast<volatile unsigned long long *>(totals_host)[0] = ~0ull;
+            *reinterpret_cast<volatile unsigned long long *>(rec_count) = 0ull;
+            __threadfence_system();
+        }
+        return;
+    }
     const uint32_t n = (uint32_t)(te - tb);
     unsigned long long np = 0, nz = 0, npa = 0;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const TileInfo x = ti[tb + i];
+        // written by the concurrently running K1 (atomics at L2): bypass L1
+        const uint2 v = __ldcg(reinterpret_cast<const uint2 *>(ti + tb + i));
+        const TileInfo x{v.x, v.y};
         pb[i] = x.present_bytes;
         np += x.counts & 1023u;
         nz += (x.counts >> 10) & 1023u;
@@ -237,7 +318,6 @@ __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, ui
     block_exclusive_scan(nz, &tz);
     block_exclusive_scan(npa, &tpa);
     for (uint32_t i = lo; i < hi; i++) {
-        tile_off[tb + i] = (uint32_t)off;
         if (pb[i]) {
             TileRec *r = host_rec + k;
             asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(r), "r"(i), "r"(pb[i]),
@@ -347,7 +427,7 @@ __device__ __forceinline__ void load_rows(uint4 (&w)[U], int &left, LoadCursor &
 // started (vstart == r0: the warp saw the whole page).
 struct ProcCursor {
     AllocView al;
-    uint32_t a, pi, vr, vstart, r0, slot;
+    uint32_t a, pi, vr, vstart, r0;
 };
 
 __device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
@@ -358,8 +438,8 @@ __device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
 }
 
 // Page complete (vr == Rp): digest it (or leave a piece) and move on.
-__device__ __forceinline__ void page_end(const ScanParams &p, ProcCursor &pc, uint32_t (&x)[4],
-                                         uint32_t &acc, const uint32_t *small, uint64_t wid, uint32_t lane) {
+__device__ __forceinline__ void page_end(const ScanParams &p, const ChunkCtx &cc, ProcCursor &pc, uint32_t (&x)[4],
+                                         uint32_t &acc, const uint32_t *small, uint32_t lane) {
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t raw = warp_raw(small, x);
     const bool nz = __any_sync(kFull, acc != 0);
@@ -370,11 +450,10 @@ __device__ __forceinline__ void page_end(const ScanParams &p, ProcCursor &pc, ui
             const bool tail = pc.pi == pc.al.n_pages - 1;
             finalize_page(p, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0,
                           tail ? pc.al.tail_len : P, tail ? pc.al.z_tail : p.z_page, raw, nz);
-        } else {
-            p.pieces[2 * wid + pc.slot] = Piece{g, pc.a, pc.vstart, P >> kLog2Row, raw, nz ? 1u : 0u};
+        } else {  // the page's last piece: nothing left to advance over
+            fold_arrive(p, cc, g, pc.a, pc.pi, pc.r0, (P >> kLog2Row) - pc.vstart, raw, nz);
         }
     }
-    pc.slot += whole ? 0u : 1u;
     x[0] = x[1] = x[2] = x[3] = 0u;
     acc = 0u;
     if (++pc.pi == pc.al.n_pages) {
@@ -386,9 +465,9 @@ __device__ __forceinline__ void page_end(const ScanParams &p, ProcCursor &pc, ui
 
 // Digest the next block (the same cnt rows load_rows fetched into w).
 template <int U>
-__device__ __forceinline__ void process_rows(const ScanParams &p, ProcCursor &pc, const uint4 (&w)[U],
+__device__ __forceinline__ void process_rows(const ScanParams &p, const ChunkCtx &cc, ProcCursor &pc, const uint4 (&w)[U],
                                              int &left, uint32_t (&x)[4], uint32_t &acc, const uint32_t *small,
-                                             uint32_t lane4, uint32_t sb, uint64_t wid, uint32_t lane) {
+                                             uint32_t lane4, uint32_t sb, uint32_t lane) {
     const uint32_t Rp = p.page_size >> kLog2Row;
     const int cnt = min(min(U, left), (int)(Rp - pc.vr));
     if (cnt == U) {
@@ -401,7 +480,7 @@ __device__ __forceinline__ void process_rows(const ScanParams &p, ProcCursor &pc
     }
     pc.vr += cnt;
     left -= cnt;
-    if (pc.vr == Rp) page_end(p, pc, x, acc, small, wid, lane);
+    if (pc.vr == Rp) page_end(p, cc, pc, x, acc, small, lane);
 }
 
 // K1.
@@ -452,116 +531,79 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lane4 = lane * 4u;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (wid < p.workers) {
-        const uint32_t P = p.page_size, lg = p.log2_page;
-        const uint32_t Rp = P >> kLog2Row;
-        const uint64_t rows = p.row_end - p.row_begin;
-        const uint64_t r = p.row_begin + rows * wid / p.workers;
-        const uint64_t rend = p.row_begin + rows * (wid + 1) / p.workers;
-        const uint32_t a = alloc_of_row(p.allocs, p.n_allocs, r, lane);
-        // position of row r: a full page, or the short tail page
-        ProcCursor pc;
-        pc.a = a;
-        pc.al = load_alloc(p.allocs + a, P);
-        pc.slot = 0;
-        const uint64_t lr = r - __ldg(&p.allocs[a].row0);
-        uint32_t pad0 = 0;  // padding of the first page (non-zero only for a short tail page)
-        if (lr < ((uint64_t)pc.al.nfull << (lg - kLog2Row))) {
-            pc.pi = (uint32_t)(lr >> (lg - kLog2Row));
-            pc.r0 = 0;
-            pc.vr = (uint32_t)(lr & (Rp - 1));
-        } else {
-            pc.pi = pc.al.n_pages - 1;
-            pad0 = P - pc.al.tail_len;
-            pc.r0 = pad0 >> kLog2Row;
-            pc.vr = (uint32_t)(lr - ((uint64_t)pc.al.nfull << (lg - kLog2Row))) + pc.r0;
-        }
-        pc.vstart = pc.vr;
-        LoadCursor lc;
-        lc.a = a;
-        lc.pi = pc.pi;
-        lc.vr = pc.vr;
-        lc.base = pc.al.base;
-        lc.n_pages = pc.al.n_pages;
-        lc.tail_len = pc.al.tail_len;
-        lc.addr = reinterpret_cast<const char *>(pc.al.base + ((uint64_t)pc.pi << lg)) - pad0 +
-                  (pc.vr << kLog2Row) + lane * 16u;
-        lc.mask = pc.vr == pc.r0 && (pc.r0 << kLog2Row) + lane * 16u < pad0;
-
-        constexpr int U = kScanUnroll;
-        int to_load = (int)(rend - r), to_proc = to_load;
-        uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u;
-        uint4 wa[U], wb[U];
-        load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
-        while (to_proc > 0) {
-            if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane);
-            process_rows<U>(p, pc, wa, to_proc, x, acc, small, lane4, sb, wid, lane);
-            if (to_proc <= 0) break;
-            if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
-            process_rows<U>(p, pc, wb, to_proc, x, acc, small, lane4, sb, wid, lane);
-        }
-        // the range ended inside a page: leave a piece
-        if (pc.vr != pc.vstart) {
-            const uint32_t raw = warp_raw(small, x);
-            const bool nz = __any_sync(kFull, acc != 0);
-            if (lane == 0)
-                p.pieces[2 * wid + pc.slot] = Piece{pc.al.page0 + pc.pi, pc.a, pc.vstart, pc.vr, raw, nz ? 1u : 0u};
-            pc.slot++;
-        }
-        if (lane == 0)
-            for (uint32_t s = pc.slot; s < 2; s++) p.pieces[2 * wid + s] = Piece{~0ull, 0u, 0u, 0u, 0u, 0u};
-    }
-}
-
-// K1b: fold the pieces of pages cut by warp-range boundaries, in two launches.
-// (a) every piece, in parallel: its contribution to its page's register,
-//     adv_{(Rp - vend) * 512}(raw), by the binary expansion of the row
-//     distance through tables fold[j] = adv_{512 * 2^j} (d < 2^12 rows).
-__global__ void __launch_bounds__(256) k_fold_contrib(const ScanParams p) {
-    extern __shared__ uint32_t fsm[];  // kFoldTables x 1024 words
-    for (uint32_t i = threadIdx.x; i < kFoldTables * 1024u; i += blockDim.x) fsm[i] = __ldg(&p.tables->fold[0][0][0] + i);
-    __syncthreads();
-    const uint32_t Rp = p.page_size >> kLog2Row;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * p.workers;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const Piece pc = p.pieces[i];
-        if (pc.page == ~0ull) continue;
-        uint32_t d = Rp - pc.vr_end, c = pc.raw;
-        for (uint32_t j = 0; d; j++, d >>= 1)
-            if (d & 1u) c = apply_tab(fsm + j * 1024u, c);
-        p.contrib[i] = c;
-    }
-}
-
-// (b) the warp holding a page's FIRST piece owns it: XOR of the contributions
-//     of its piece and of the HEAD pieces of the following warps, then c.1
-//     steps 3-5.
-__global__ void __launch_bounds__(256) k_fold_final(const ScanParams p) {
+    if (wid >= p.workers) return;
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t Rp = P >> kLog2Row;
-    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < p.workers;
-         j += (uint64_t)gridDim.x * blockDim.x) {
-        for (int s = 1; s >= 0; s--) {
-            const Piece pc = p.pieces[2 * j + s];
-            if (pc.page == ~0ull) continue;
-            const AllocDev *al = p.allocs + pc.alloc;
-            const uint64_t pi = pc.page - __ldg(&al->page0);
-            const uint32_t n_pages = __ldg(&al->n_pages);
-            const bool tail = pi == (uint64_t)n_pages - 1;
-            const uint32_t len = tail ? __ldg(&al->tail_len) : P;
-            const uint32_t r0 = (P - len) >> kLog2Row;
-            if (pc.vr_begin != r0) continue;  // not the page's first piece
-            uint32_t raw = p.contrib[2 * j + s];
-            bool nz = pc.nz != 0;
-            uint32_t end = pc.vr_end;
-            for (uint64_t k = j + 1; end < Rp && k < p.workers; k++) {
-                raw ^= p.contrib[2 * k];
-                nz |= p.pieces[2 * k].nz != 0;
-                end = p.pieces[2 * k].vr_end;
+    for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
+        ChunkCtx cc;
+        cc.rb = p.chunk_rows[ch];
+        cc.rows = p.chunk_rows[ch + 1] - cc.rb;
+        cc.fx = p.fold.x + (uint64_t)ch * p.workers;
+        cc.fc = p.fold.c + (uint64_t)ch * p.workers;
+        const uint64_t r = cc.rb + cc.rows * wid / p.workers;
+        const uint64_t rend = cc.rb + cc.rows * (wid + 1) / p.workers;
+        if (r < rend) {
+            const uint32_t a = alloc_of_row(p.allocs, p.n_allocs, r, lane);
+            // position of row r: a full page, or the short tail page
+            ProcCursor pc;
+            pc.a = a;
+            pc.al = load_alloc(p.allocs + a, P);
+            const uint64_t lr = r - __ldg(&p.allocs[a].row0);
+            uint32_t pad0 = 0;  // padding of the first page (non-zero only for a short tail page)
+            if (lr < ((uint64_t)pc.al.nfull << (lg - kLog2Row))) {
+                pc.pi = (uint32_t)(lr >> (lg - kLog2Row));
+                pc.r0 = 0;
+                pc.vr = (uint32_t)(lr & (Rp - 1));
+            } else {
+                pc.pi = pc.al.n_pages - 1;
+                pad0 = P - pc.al.tail_len;
+                pc.r0 = pad0 >> kLog2Row;
+                pc.vr = (uint32_t)(lr - ((uint64_t)pc.al.nfull << (lg - kLog2Row))) + pc.r0;
             }
-            finalize_page(p, pc.page, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
-                          tail ? __ldg(&al->z_tail) : p.z_page, raw, nz);
+            pc.vstart = pc.vr;
+            LoadCursor lc;
+            lc.a = a;
+            lc.pi = pc.pi;
+            lc.vr = pc.vr;
+            lc.base = pc.al.base;
+            lc.n_pages = pc.al.n_pages;
+            lc.tail_len = pc.al.tail_len;
+            lc.addr = reinterpret_cast<const char *>(pc.al.base + ((uint64_t)pc.pi << lg)) - pad0 +
+                      (pc.vr << kLog2Row) + lane * 16u;
+            lc.mask = pc.vr == pc.r0 && (pc.r0 << kLog2Row) + lane * 16u < pad0;
+
+            constexpr int U = kScanUnroll;
+            int to_load = (int)(rend - r), to_proc = to_load;
+            uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u;
+            uint4 wa[U], wb[U];
+            load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
+            while (to_proc > 0) {
+                if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane);
+                process_rows<U>(p, cc, pc, wa, to_proc, x, acc, small, lane4, sb, lane);
+                if (to_proc <= 0) break;
+                if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
+                process_rows<U>(p, cc, pc, wb, to_proc, x, acc, small, lane4, sb, lane);
+            }
+            // the range ended inside a page: advance the piece to the page end
+            // (d = Rp - vr rows) and arrive at the page's owner slot
+            if (pc.vr != pc.vstart) {
+                const uint32_t raw = __shfl_sync(kFull, warp_raw(small, x), 0);
+                const bool nz = __any_sync(kFull, acc != 0);
+                const uint32_t contrib = warp_mulmod(__ldg(&p.tables->fold_m[Rp - pc.vr]), raw, lane);
+                if (lane == 0)
+                    fold_arrive(p, cc, pc.al.page0 + pc.pi, pc.a, pc.pi, pc.r0, pc.vr - pc.vstart, contrib, nz);
+            }
         }
+        // this warp is done with chunk ch; the last one publishes it for K2
+        if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(p.chunk_arrive + ch, 1u) == (uint32_t)p.workers - 1u) {
+                atomicExch(p.chunk_arrive + ch, 0u);
+                __threadfence();
+                atomicExch(p.chunk_done + ch, p.epoch);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -589,60 +631,89 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
         *reinterpret_cast<uint4 *>(dst + off) = ldg_stream(src + off);
 }
 
-// K4: gather PRESENT pages of the tiles [tb, te) into the staging slot.
-__global__ void __launch_bounds__(1024) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
-                                              const uint8_t *cls, const uint32_t *tile_off,
-                                              uint64_t tb, uint64_t te, uint32_t P, uint32_t lg,
-                                              uint8_t *slot, const uint8_t *pack_flags) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t t = tb + (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < te;
-         t += nwarps) {
-        if (pack_flags && !pack_flags[t - tb]) continue;  // moved by a direct DMA
-        const uint32_t a = __ldg(tile_alloc + t);
-        const AllocDev *al = allocs + a;
-        const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), tile0 = __ldg(&al->tile0);
-        const uint32_t n_pages = __ldg(&al->n_pages), tail_len = __ldg(&al->tail_len);
-        const uint64_t lt = t - tile0;
-        if (P <= kTileBytes) {
-            const uint32_t ppt = kTileBytes >> lg;
-            const uint64_t pi0 = lt * ppt;
-            // lane j < ppt looks at page pi0 + j
-            uint32_t my_len = 0;
-            const uint64_t pi = pi0 + lane;
-            if (lane < ppt && pi < n_pages && (cls[page0 + pi] & 3u) == kClsPresent)
-                my_len = pi == (uint64_t)n_pages - 1 ? tail_len : P;
-            uint32_t inc = my_len;
+// K4: gather the PRESENT bytes of the chunk's staged tiles into the staging
+// slot.  The host lists the staged tiles, each with the slot offset of its
+// first PRESENT byte (from K2's records), in MAPPED pinned memory: no H2D sits
+// in a copy-engine queue behind the drain.  A CTA stages a batch of items in
+// shared memory with coalesced PCIe reads; a warp unit is one 4 KiB slice of
+// a tile (8 rows of 512 B: every load in flight at once), so the work spreads
+// evenly over all warps whatever the dirty pattern.  Within a row every byte
+// lies in one page (pages are >= 4 KiB and row aligned): the row's page j and
+// the PRESENT bytes before it in the tile come from a lane-parallel scan of
+// the tile's page classes.
+constexpr int kPackThreads = 1024;
+constexpr uint32_t kPackBatch = 1024;                     // items staged per CTA round
+constexpr uint32_t kPackSlice = 4096, kPackSliceRows = kPackSlice >> kLog2Row;
+constexpr uint32_t kSlicesPerTile = kTileBytes / kPackSlice;  // 16
+
+__global__ void __launch_bounds__(kPackThreads) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
+                                                       const uint8_t *cls, uint64_t tb, uint32_t P, uint32_t lg,
+                                                       uint8_t *slot, const StageItem *items, uint32_t n_items) {
+    __shared__ StageItem si[kPackBatch];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t i0 = (uint32_t)((uint64_t)n_items * blockIdx.x / gridDim.x);
+    const uint32_t i1 = (uint32_t)((uint64_t)n_items * (blockIdx.x + 1) / gridDim.x);
+    for (uint32_t b0 = i0; b0 < i1; b0 += kPackBatch) {
+        const uint32_t nb = min(kPackBatch, i1 - b0);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+            const uint2 v = __ldcv(reinterpret_cast<const uint2 *>(items + b0 + i));  // host-written: never cached
+            si[i] = StageItem{v.x, v.y};
+        }
+        __syncthreads();
+        for (uint32_t u = warp; u < nb * kSlicesPerTile; u += nw) {
+            const StageItem it = si[u / kSlicesPerTile];
+            const uint32_t so = (u % kSlicesPerTile) * kPackSlice;  // slice offset in the tile
+            const uint64_t t = tb + it.tile;
+            const AllocDev *al = allocs + __ldg(tile_alloc + t);
+            const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), lt = t - __ldg(&al->tile0);
+            const uint32_t n_pages = __ldg(&al->n_pages), tail_len = __ldg(&al->tail_len);
+            const uint8_t *src;
+            uint8_t *dst;
+            uint32_t plen, pref;  // lane j: PRESENT length of the tile's page j, PRESENT bytes before it
+            uint32_t rlg = lg;    // row offset -> page-in-tile shift
+            if (P <= kTileBytes) {
+                const uint32_t ppt = kTileBytes >> lg;
+                const uint64_t pi = lt * ppt + lane;
+                plen = 0;
+                if (lane < ppt && pi < n_pages && (cls[page0 + pi] & 3u) == kClsPresent)
+                    plen = pi == (uint64_t)n_pages - 1 ? tail_len : P;
+                uint32_t inc = plen;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-                if (lane >= (uint32_t)d) inc += o;
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(kFull, inc, d);
+                    if (lane >= (uint32_t)d) inc += o;
+                }
+                pref = inc - plen;
+                src = reinterpret_cast<const uint8_t *>(base + (lt << kLog2Tile));
+                dst = slot + it.dst;
+            } else {  // one 64 KiB slice of a page; the item's dst is the slice's own offset
+                const uint32_t tpp = P >> kLog2Tile;
+                const uint64_t pi = lt / tpp;
+                const uint32_t s = (uint32_t)(lt % tpp);
+                const uint32_t len = pi == (uint64_t)n_pages - 1 ? tail_len : P;
+                const bool present = (cls[page0 + pi] & 3u) == kClsPresent;
+                plen = present && s * kTileBytes < len ? min(len - s * kTileBytes, kTileBytes) : 0u;
+                plen = __shfl_sync(kFull, plen, 0);
+                pref = 0;
+                src = reinterpret_cast<const uint8_t *>(base + (pi << lg) + (uint64_t)s * kTileBytes);
+                dst = slot + it.dst;
+                rlg = kLog2Tile;  // the slice is the tile's only "page"
             }
-            const uint32_t my_off = inc - my_len;
-            uint8_t *dst0 = slot + tile_off[t];
-            unsigned present = __ballot_sync(0xFFFFFFFFu, my_len != 0);
-            while (present) {
-                // merge consecutive present pages into one contiguous copy
-                const int j = __ffs(present) - 1;
-                int k = j;
-                while (k + 1 < 32 && ((present >> (k + 1)) & 1u)) k++;
-                const uint32_t off_j = __shfl_sync(0xFFFFFFFFu, my_off, j);
-                const uint32_t end_k = __shfl_sync(0xFFFFFFFFu, my_off + my_len, k);
-                warp_copy(dst0 + off_j, reinterpret_cast<const uint8_t *>(base + ((pi0 + j) << lg)),
-                          end_k - off_j, lane);
-                present &= (k + 1 < 32) ? ~((2u << k) - 1u) : 0u;
+            uint4 v[kPackSliceRows];
+            uint32_t doff[kPackSliceRows];  // slot offset of this lane's 16 B, ~0 = not PRESENT
+#pragma unroll
+            for (uint32_t r = 0; r < kPackSliceRows; r++) {
+                const uint32_t off = so + r * kRowBytes;  // row offset in the tile
+                const uint32_t j = off >> rlg;
+                const uint32_t pl = __shfl_sync(kFull, plen, j), pr = __shfl_sync(kFull, pref, j);
+                const uint32_t w = off - (j << rlg) + lane * 16u;  // byte offset in page j
+                doff[r] = w < pl ? pr + w : ~0u;
+                if (doff[r] != ~0u) v[r] = ldg_stream(src + off + lane * 16u);
             }
-        } else {
-            const uint32_t tpp = P >> kLog2Tile;
-            const uint64_t pi = lt / tpp;
-            const uint32_t s = (uint32_t)(lt % tpp);
-            if ((cls[page0 + pi] & 3u) != kClsPresent) continue;
-            const uint32_t len = pi == (uint64_t)n_pages - 1 ? tail_len : P;
-            const uint32_t lo = s * kTileBytes;
-            if (lo >= len) continue;
-            const uint32_t hi = min(len, lo + kTileBytes);
-            warp_copy(slot + tile_off[t - s] + lo, reinterpret_cast<const uint8_t *>(base + (pi << lg) + lo),
-                      hi - lo, lane);
+#pragma unroll
+            for (uint32_t r = 0; r < kPackSliceRows; r++)
+                if (doff[r] != ~0u) *reinterpret_cast<uint4 *>(dst + doff[r]) = v[r];
         }
     }
 }
@@ -777,17 +848,11 @@ constexpr int kPackCtas = 8;
 
 static int scan_sms(int n_sms) { return n_sms > 4 * kFreeSMs ? n_sms - kFreeSMs : n_sms; }
 
-uint64_t scan_workers(uint64_t rows, int n_sms) {
-    // every warp streams >= 8 rows (4 KiB); at most all warps of a full grid
-    const uint64_t full = (uint64_t)scan_sms(n_sms) * (kScanThreads / 32);
-    uint64_t w = rows / 8;
-    if (w < 1) w = 1;
-    return w < full ? w : full;
-}
+uint64_t scan_workers(int n_sms) { return (uint64_t)scan_sms(n_sms) * (kScanThreads / 32); }
 
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     // once per device: setting a function attribute can serialise with work in
-    // flight, which would leave the GPU idle between pipelined chunk launches
+    // flight, which would leave the GPU idle between pipelined launches
     static bool attr_done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -796,37 +861,16 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
             return -1;
         attr_done[dev] = true;
     }
-    if (p.row_end == p.row_begin) return 0;
+    if (p.n_chunks == 0) return 0;
     const uint64_t wpb = kScanThreads / 32;
     const uint64_t grid = (p.workers + wpb - 1) / wpb;
     k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
     return launched(1);
 }
 
-int launch_fold(const ScanParams &p, int n_sms, cudaStream_t st) {
-    if (p.row_end == p.row_begin) return 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static bool fold_attr[64] = {};
-    if (dev < 64 && !fold_attr[dev]) {
-        if (cudaFuncSetAttribute(k_fold_contrib, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kFoldTables * 4096u)) != cudaSuccess)
-            return -1;
-        fold_attr[dev] = true;
-    }
-    // the fold may run beside the next chunk's scan: stay on the SMs K1 leaves free
-    const uint64_t cap = n_sms > 4 * kFreeSMs ? kFreeSMs - 1 : n_sms;
-    uint64_t gc = (2 * p.workers + 255) / 256;
-    if (gc > cap) gc = cap;
-    k_fold_contrib<<<(unsigned)gc, 256, kFoldTables * 4096u, st>>>(p);
-    uint64_t g2 = (p.workers + 255) / 256;
-    if (g2 > cap) g2 = cap;
-    k_fold_final<<<(unsigned)g2, 256, 0, st>>>(p);
-    return launched(2);
-}
-
-int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *tile_off, TileRec *host_rec,
-                     unsigned long long *rec_count, ChunkTotals *totals_host, cudaStream_t st) {
+int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, const uint32_t *chunk_done, uint32_t chunk,
+                     uint32_t epoch, TileRec *host_rec, unsigned long long *rec_count, ChunkTotals *totals_host,
+                     cudaStream_t st) {
     const size_t smem = (size_t)(te - tb) * 4;
     static bool attr_done[64] = {};
     int dev = 0;
@@ -836,21 +880,19 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, uint32_t *ti
             return -1;
         attr_done[dev] = true;
     }
-    k_tile_scan<<<1, kTileScanThreads, smem, st>>>(tile_info, tb, te, tile_off, host_rec, rec_count, totals_host);
+    k_tile_scan<<<1, kTileScanThreads, smem, st>>>(tile_info, tb, te, chunk_done, chunk, epoch, host_rec, rec_count,
+                                                   totals_host);
     return launched(1);
 }
 
-int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, const uint32_t *tile_off,
-                uint64_t tb, uint64_t te, uint32_t P, uint32_t lg, uint8_t *slot, const uint8_t *pack_flags, int n_sms,
-                cudaStream_t st) {
-    const uint64_t tiles = te - tb;
-    if (tiles == 0) return 0;
-    // the pack runs beside the next chunk's scan: stay on the SMs K1 leaves free,
-    // with 32 warps each (4 KiB of loads in flight per warp) to fill them
-    uint64_t grid = (tiles + 31) / 32;
-    const uint64_t cap = n_sms > 4 * kFreeSMs ? kPackCtas : (uint64_t)n_sms * 4;
+int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tb, uint32_t P,
+                uint32_t lg, uint8_t *slot, const StageItem *items, uint32_t n_items, int n_sms, cudaStream_t st) {
+    if (n_items == 0) return 0;
+    // the pack runs beside the next chunk's scan: stay on the SMs K1 leaves free
+    uint64_t grid = ((uint64_t)n_items * kSlicesPerTile + kPackThreads / 32 - 1) / (kPackThreads / 32);
+    const uint64_t cap = n_sms > 4 * kFreeSMs ? kPackCtas : (uint64_t)n_sms * 2;
     if (grid > cap) grid = cap;
-    k_pack<<<(unsigned)grid, 1024, 0, st>>>(allocs, tile_alloc, cls, tile_off, tb, te, P, lg, slot, pack_flags);
+    k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items);
     return launched(1);
 }
 
