@@ -182,7 +182,7 @@ def run_ours(args):
     ts = w.materialize()
     torch.cuda.synchronize()
     ctx = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20,
-                      n_copy_streams=args.streams,
+                      n_copy_streams=args.streams, n_staging_slots=args.slots,
                       direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
     for t in ts:
         ctx.register_tensor(t)
@@ -334,7 +334,7 @@ def run_ours(args):
         "config": {"workload": _workload_desc(args.config + ("i" if incremental and args.config == "C4" else ""), w),
                    "dirty_fraction": args.dirty if incremental else None, "registered_bytes_per_rank": R,
                    "allocations": len(w.allocs), "page_size": w.page_size, "chunk_bytes": args.chunk_mb << 20,
-                   "copy_streams": args.streams, "direct_min_bytes": int(args.direct_min_mb * (1 << 20)) if args.direct_min_mb >= 0 else None,
+                   "copy_streams": args.streams, "staging_slots": args.slots or args.streams, "direct_min_bytes": int(args.direct_min_mb * (1 << 20)) if args.direct_min_mb >= 0 else None,
                    "parallelism": f"independent ranks x{world} (gloo control plane)",
                    "l2": "inputs larger than L2 (registered state >> 126 MB; no flush needed)"},
         "per_gpu": {"checkpoint_GBps": round(ck_gbs, 3), "restore_GBps": round(rs_gbs, 3),
@@ -450,6 +450,7 @@ def main():
     ap.add_argument("--gib", type=int, default=None, help="C4/C5 GiB per GPU")
     ap.add_argument("--chunk-mb", type=int, default=256)
     ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--slots", type=int, default=0, help="staging slots (0 = one per copy stream)")
     ap.add_argument("--direct-min-mb", type=float, default=None,
                     help="runs >= this go by direct DMA (default: the library's); -1 = always staged")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -75,10 +75,13 @@ typedef enum { GCR_FULL = 0, GCR_INCREMENTAL = 1 } gcr_mode;
 
 typedef struct {
     uint32_t page_size;       /* power of two in [4096, 2097152]; default 65536 (R-1) */
-    uint32_t n_copy_streams;  /* copy streams = staging slots for drain/restore; default 2, 1..8 */
+    uint32_t n_copy_streams;  /* copy streams for drain/restore; default 2, 1..8 */
     uint64_t chunk_bytes;     /* registry bytes scanned per pipeline chunk, also the staging slot
                                  size; default 256 MiB; multiple of page_size, <= 2 GiB */
-    uint32_t n_staging_slots; /* kept for ABI stability: must be 0 or == n_copy_streams */
+    uint32_t n_staging_slots; /* device staging slots of chunk_bytes each; 0 (default) = one per
+                                 copy stream, else n_copy_streams..16.  Checkpoint chunk i packs
+                                 into slot i mod n, so its pack waits only for chunk i - n's
+                                 drain; more slots let packs run further ahead of the drain. */
     uint32_t verify;          /* 1 (default) = restore re-reads every page and checks its digest
                                  (reading R-11); 0 = no verify pass (then restore never returns
                                  GCR_E_VERIFY) */

@@ -7,6 +7,7 @@
 // v * x^(8d) mod P, represented as a 32x32 bit matrix (one column per input
 // bit) and raised to the d-th power by repeated squaring; byte tables are
 // then read off by linearity: tab[k][e] = adv_d(e << 8k).
+#include <algorithm>
 #include <cstring>
 #include <nmmintrin.h>
 
@@ -102,14 +103,44 @@ static uint32_t mulmod(uint32_t m, uint32_t v) {
     return r;
 }
 
+uint32_t crc_shift(uint32_t reg, uint64_t nbytes) { return mat_vec(adv_matrix(nbytes), reg); }
+
 uint32_t zero_digest(uint64_t n) { return mat_vec(adv_matrix(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu; }
 
 // Raw register update over host bytes for image metadata (meta_crc32c).  The
 // x86 SSE4.2 crc32 instruction implements exactly this register update for
 // the Castagnoli polynomial; a table path covers CPUs without it.
+constexpr uint64_t kCrcSplitMin = 64 * 1024;  // below this one chain is as fast as the join
+
 uint32_t host_crc32c_update(uint32_t state, const void *p, uint64_t n) {
     const uint8_t *b = static_cast<const uint8_t *>(p);
     static const bool have_sse42 = __builtin_cpu_supports("sse4.2");
+    if (have_sse42 && n >= kCrcSplitMin) {
+        // three independent crc32 chains (the instruction has 3-cycle latency
+        // and 1-cycle throughput), joined by linearity:
+        // reg(s, A|B|C) = adv_k(adv_k(reg(s, A)) ^ reg(0, B)) ^ reg(0, C)
+        const uint64_t k = (n / 3) & ~7ull;
+        const uint8_t *b1 = b + k, *b2 = b + 2 * k;
+        uint64_t s0 = state, s1 = 0, s2 = 0;
+        for (uint64_t i = 0; i < k; i += 8) {
+            uint64_t w0, w1, w2;
+            std::memcpy(&w0, b + i, 8);
+            std::memcpy(&w1, b1 + i, 8);
+            std::memcpy(&w2, b2 + i, 8);
+            s0 = _mm_crc32_u64(s0, w0);
+            s1 = _mm_crc32_u64(s1, w1);
+            s2 = _mm_crc32_u64(s2, w2);
+        }
+        // (the shift matrix is cached: a drain CRCs equal-sized digest batches)
+        thread_local uint64_t mk = 0;
+        thread_local Mat m;
+        if (mk != k) {
+            m = adv_matrix(k);
+            mk = k;
+        }
+        const uint32_t joined = mat_vec(m, mat_vec(m, (uint32_t)s0) ^ (uint32_t)s1) ^ (uint32_t)s2;
+        return host_crc32c_update(joined, b + 3 * k, n - 3 * k);
+    }
     if (have_sse42) {
         uint64_t s = state;
         while (n >= 8) {
@@ -152,6 +183,20 @@ bool crc_self_test() {
     // braid table consistency: adv_512 == (adv_4)^128 on a probe value
     uint32_t v = 0x12345678u, w = v;
     for (int k = 0; k < 128; k++) w = apply4(t->t4, w);
+    // the 3-chain split path against the one-chain path on a long buffer
+    {
+        const uint64_t n = 3 * kCrcSplitMin + 40;
+        uint8_t *buf = new uint8_t[n];
+        for (uint64_t i = 0; i < n; i++) buf[i] = (uint8_t)(i * 2654435761u >> 13);
+        uint32_t one = 0xFFFFFFFFu;
+        for (uint64_t i = 0; i < n; i += 4096) one = host_crc32c_update(one, buf + i, std::min<uint64_t>(4096, n - i));
+        const bool split_ok = host_crc32c_update(0xFFFFFFFFu, buf, n) == one;
+        delete[] buf;
+        if (!split_ok) {
+            delete t;
+            return false;
+        }
+    }
     // fold products: fold_m[d] (*) v == adv_{512 d}(v) by an independent matrix power
     bool ok = a == 0xE3069283u && b == 0xE3069283u && apply4(t->braid, v) == w &&
               zero_digest(65536) == 0x72C0C4A4u && mulmod(t->fold_m[1], v) == w;

@@ -444,13 +444,18 @@ void destroy_image(gcr_ctx *c, gcr_image *img) {
     delete img;
 }
 
-uint32_t meta_crc(const gcr_image *img) {
+// meta_crc32c = CRC32C(header with the field 0 | alloc table | pagemap |
+// digests).  digests_reg, if given, is reg(0, digests) computed earlier (the
+// checkpoint CRCs digest batches while the drain runs); it is joined by
+// linearity: reg(s, X|D) = adv_|D|(reg(s, X)) ^ reg(0, D).
+uint32_t meta_crc(const gcr_image *img, const uint32_t *digests_reg = nullptr) {
     gcr_image_hdr h = img->hdr;
     h.meta_crc32c = 0;
     uint32_t s = host_crc32c_update(0xFFFFFFFFu, &h, sizeof h);
     s = host_crc32c_update(s, img->allocs.data(), sizeof(gcr_alloc_rec) * img->allocs.size());
     s = host_crc32c_update(s, img->pagemap, sizeof(gcr_pagemap_entry) * img->hdr.n_entries);
-    s = host_crc32c_update(s, img->digests, 4ull * img->hdr.n_pages);
+    if (digests_reg) s = crc_shift(s, 4ull * img->hdr.n_pages) ^ *digests_reg;
+    else s = host_crc32c_update(s, img->digests, 4ull * img->hdr.n_pages);
     return s ^ 0xFFFFFFFFu;
 }
 
@@ -524,7 +529,8 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     if (cfg_in) cfg = *cfg_in;
     if (!valid_page_size(cfg.page_size) || cfg.n_copy_streams < 1 || cfg.n_copy_streams > 8 ||
         cfg.chunk_bytes == 0 || cfg.chunk_bytes % cfg.page_size != 0 || cfg.chunk_bytes % kTileBytes != 0 ||
-        cfg.chunk_bytes > kMaxChunk || (cfg.n_staging_slots != 0 && cfg.n_staging_slots != cfg.n_copy_streams))
+        cfg.chunk_bytes > kMaxChunk ||
+        (cfg.n_staging_slots != 0 && (cfg.n_staging_slots < cfg.n_copy_streams || cfg.n_staging_slots > 16)))
         return GCR_E_INVAL;
     if (!crc_self_test()) return GCR_E_INVAL;
     int ndev = 0;
@@ -550,6 +556,8 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
         cudaStream_t s;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
         c->copy.push_back(s);
+    }
+    for (uint32_t i = 0; i < (cfg.n_staging_slots ? cfg.n_staging_slots : cfg.n_copy_streams); i++) {
         void *slot = nullptr;
         if (cudaMalloc(&slot, cfg.chunk_bytes) != cudaSuccess) {
             cudaGetLastError();
@@ -779,7 +787,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // staging slot and copied out in contiguous ranges.
     uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0;
     Clock::time_point drain0;
-    const size_t S = c->copy.size();
+    const size_t S = c->copy.size(), NS = c->slots.size();
     const uint64_t direct_min = c->cfg.direct_min_bytes;
     uint64_t direct_bytes = 0, staged_bytes = 0;
     struct Run {
@@ -788,6 +796,24 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     std::vector<Run> direct;
     std::vector<std::pair<uint64_t, uint64_t>> staged;  // chunk-local image ranges [lo, hi)
     size_t dg0 = 0;                                     // first chunk of the pending digest D2H
+    // digest batches in page order: CRC'd on the host as their D2H completes
+    struct DigestBatch {
+        uint64_t pb, pe;
+        cudaEvent_t done;
+    };
+    std::vector<DigestBatch> dbatch;
+    size_t dnext = 0;
+    uint32_t dreg = 0;  // reg(0, digests of the batches CRC'd so far)
+    auto crc_batches = [&](bool wait) -> gcr_status {
+        for (; dnext < dbatch.size(); dnext++) {
+            const DigestBatch &b = dbatch[dnext];
+            if (wait) CUDA_TRY(c, cudaEventSynchronize(b.done));
+            else if (cudaEventQuery(b.done) != cudaSuccess) break;
+            dreg = host_crc32c_update(dreg, img->digests + b.pb, 4 * (b.pe - b.pb));
+        }
+        cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error
+        return GCR_OK;
+    };
     for (size_t i = 0; i < nch; i++) {
         const Chunk &ch = c->chunks[i];
         CUDA_TRY(c, cudaEventSynchronize(tot[i]));
@@ -899,10 +925,10 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         pks[i] = c->ev();
         pke[i] = c->ev();
         CUDA_TRY(c, cudaStreamWaitEvent(c->packs, tot[i], 0));
-        if (any_staged) {
-            if (i >= S) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - S], 0));
+        if (any_staged) {  // slot i mod NS was last drained by chunk i - NS
+            if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
-            LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, ch.tile_begin, P, c->lg, c->slots[i % S],
+            LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, ch.tile_begin, P, c->lg, c->slots[i % NS],
                                       c->stage_map + ch.tile_begin, n_items, c->n_sms, c->packs));
         } else {
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
@@ -910,7 +936,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         CUDA_TRY(c, cudaEventRecord(pke[i], c->packs));
         CUDA_TRY(c, cudaStreamWaitEvent(cs, pke[i], 0));
         for (const auto &rg : staged) {
-            CUDA_TRY(c, cudaMemcpyAsync(img->data + base + rg.first, c->slots[i % S] + rg.first, rg.second - rg.first,
+            CUDA_TRY(c, cudaMemcpyAsync(img->data + base + rg.first, c->slots[i % NS] + rg.first, rg.second - rg.first,
                                         cudaMemcpyDeviceToHost, cs));
             staged_bytes += rg.second - rg.first;
         }
@@ -926,9 +952,17 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             if (pe > pb)
                 CUDA_TRY(c, cudaMemcpyAsync(img->digests + pb, Dnew + pb, 4 * (pe - pb), cudaMemcpyDeviceToHost, cs));
             dg0 = i + 1;
+            dde[i] = c->ev();
+            CUDA_TRY(c, cudaEventRecord(dde[i], cs));
+            if (pe > pb) dbatch.push_back(DigestBatch{pb, pe, dde[i]});
+        } else {
+            dde[i] = c->ev();
+            CUDA_TRY(c, cudaEventRecord(dde[i], cs));
         }
-        dde[i] = c->ev();
-        CUDA_TRY(c, cudaEventRecord(dde[i], cs));
+        {
+            gcr_status cs_ = crc_batches(false);  // digests that already landed (the host is idle here)
+            if (cs_ != GCR_OK) return cs_;
+        }
         base += T.image_bytes;
     }
     if (direct_bytes + staged_bytes != base) return fail(c, GCR_E_CUDA, "checkpoint: drain plan does not cover the image");
@@ -958,6 +992,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     }
     CUDA_TRY(c, cudaStreamSynchronize(c->compute));
     st.drain_ns = ns_since(drain0);
+    const double host_synced = ns_since(host0) * 1e-6;
 
     // stats from the events
     float ms;
@@ -971,6 +1006,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     }
     CUDA_TRY(c, cudaEventElapsedTime(&ms, pm0, pm1));
     st.compact_dev_ns = (uint64_t)(ms * 1e6);
+    const double host_stats = ns_since(host0) * 1e-6;
     if (trace) {  // GCR_TRACE=1: per-chunk timeline (ms from the checkpoint's first event) on stderr
         auto rel = [&](cudaEvent_t e) {
             float m = 0;
@@ -1014,7 +1050,17 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     h.reserved = 0;
     img->allocs.clear();
     for (const RegEntry &r : c->reg) img->allocs.push_back(gcr_alloc_rec{r.dptr, r.bytes, r.id, 0});
-    h.meta_crc32c = meta_crc(img);
+    const double host_model = ns_since(host0) * 1e-6;
+    {
+        gcr_status cs_ = crc_batches(true);
+        if (cs_ != GCR_OK) return cs_;
+    }
+    h.meta_crc32c = meta_crc(img, &dreg);
+    if (trace)
+        std::fprintf(stderr,
+                     "{\"gcr_trace\": \"checkpoint_host\", \"synced_ms\": %.3f, \"stats_ms\": %.3f, \"model_ms\": %.3f, "
+                     "\"meta_crc_done_ms\": %.3f}\n",
+                     host_synced, host_stats, host_model, ns_since(host0) * 1e-6);
     if (n_present + n_zero + n_parent != c->n_pages)
         return fail(c, GCR_E_CUDA, "checkpoint: class counts do not cover every page");
     c->next_gen++;

@@ -158,6 +158,7 @@ size_t scan_smem_bytes();
 // ---- host CRC32C math (crc_host.cpp), independent of oracle/ --------------
 void build_tables(CrcTables *out);
 uint32_t zero_digest(uint64_t n);                 // Z(n)
+uint32_t crc_shift(uint32_t reg, uint64_t nbytes);  // adv_nbytes(reg): reg(s, A|B) = crc_shift(reg(s, A), |B|) ^ reg(0, B)
 uint32_t host_crc32c_update(uint32_t state, const void *p, uint64_t n);  // raw register update
 bool crc_self_test();                            // "123456789" -> 0xE3069283 through the tables
 

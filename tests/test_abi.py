@@ -54,7 +54,8 @@ def test_invalid_config_rejected_before_touching_cuda(built):
     from paper_2502_16631_b200 import gcr
     h = C.c_void_p()
     for over in (dict(page_size=3000), dict(page_size=2048), dict(page_size=1 << 22), dict(n_copy_streams=0),
-                 dict(chunk_bytes=65536 + 4096), dict(chunk_bytes=4 << 30), dict(n_staging_slots=5)):
+                 dict(chunk_bytes=65536 + 4096), dict(chunk_bytes=4 << 30),
+                 dict(n_staging_slots=1), dict(n_staging_slots=17)):  # slots: 0 or n_copy_streams..16
         cfg = gcr.default_config(**over)
         assert gcr.gcr_create(0, C.byref(cfg), C.byref(h)) == gcr.GCR_E_INVAL, over
 

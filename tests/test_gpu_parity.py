@@ -55,10 +55,11 @@ ALWAYS_STAGED = (1 << 64) - 1
 DIRECT_MINS = [0, 1 << 20, ALWAYS_STAGED]   # every run direct / 1 MiB / every run staged
 
 
-def _ckpt_restore_parity(G, orc, sizes, P, zero_pages=(), chunk=None, streams=2, seed=99, direct_min=1 << 20):
+def _ckpt_restore_parity(G, orc, sizes, P, zero_pages=(), chunk=None, streams=2, seed=99, direct_min=1 << 20,
+                         slots=0):
     gcr, synth = G
     ts = _mk(G, sizes, seed, zero_pages=zero_pages, P=P)
-    cfg = dict(page_size=P, n_copy_streams=streams, direct_min_bytes=direct_min)
+    cfg = dict(page_size=P, n_copy_streams=streams, direct_min_bytes=direct_min, n_staging_slots=slots)
     if chunk:
         cfg["chunk_bytes"] = chunk
     ctx = gcr.Context(0, **cfg)
@@ -153,6 +154,19 @@ def test_chunking_and_copy_streams(G, orc, chunk, streams, direct_min):
     zp = [(a, int(p)) for a in range(4) for p in rng.choice((sizes[a] + P - 1) // P, min(3, (sizes[a] + P - 1) // P), replace=False)]
     _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=max(chunk, P), streams=streams, seed=chunk,
                          direct_min=direct_min)
+
+
+@pytest.mark.parametrize("streams,slots", [(1, 3), (2, 5), (3, 16)])
+def test_more_staging_slots_than_streams(G, orc, streams, slots):
+    """Chunk i packs into slot i mod n_slots (its pack waits for chunk i - n_slots's
+    drain); 30+ chunks, all staged, so every slot is reused many times and the
+    digests arrive in many batches (meta CRC joined from them)."""
+    P = 65536
+    sizes = [(9 << 20) + 4096, 3 << 20, (6 << 20) + 512, 16 + 4096]
+    rng = np.random.default_rng(slots)
+    zp = [(a, int(p)) for a in range(3) for p in rng.choice((sizes[a] + P - 1) // P, 5, replace=False)]
+    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=1 << 19, streams=streams, seed=slots,
+                         direct_min=ALWAYS_STAGED, slots=slots)
 
 
 def test_chunking_small_pages_many_chunks(G, orc):
