@@ -928,8 +928,10 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         if (any_staged) {  // slot i mod NS was last drained by chunk i - NS
             if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
+            // narrowed to the SMs K1 leaves free while the scan's last chunk is unpublished
             LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, ch.tile_begin, P, c->lg, c->slots[i % NS],
-                                      c->stage_map + ch.tile_begin, n_items, c->n_sms, c->packs));
+                                      c->stage_map + ch.tile_begin, n_items, c->n_sms, sp.chunk_done + (nch - 1),
+                                      sp.epoch, c->packs));
         } else {
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
         }

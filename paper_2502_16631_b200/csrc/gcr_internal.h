@@ -142,7 +142,7 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end
                      ChunkTotals *totals_host, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tile_begin,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, const StageItem *items, uint32_t n_items,
-                int n_sms, cudaStream_t st);
+                int n_sms, const uint32_t *scan_done, uint32_t epoch, cudaStream_t st);
 // Pagemap over all pages: phase 1 counts run starts per block and scans them,
 // writing the entry count to *n_entries_dev; phase 2 writes the entries.
 int launch_pagemap_count(const uint8_t *cls, uint64_t n_pages, uint32_t *blk_cnt, uint32_t *blk_off,

@@ -631,6 +631,13 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
         *reinterpret_cast<uint4 *>(dst + off) = ldg_stream(src + off);
 }
 
+// K1 leaves kFreeSMs SMs unoccupied so that K2/K4 (and the restore's K6)
+// start the moment they are enqueued instead of waiting
+// for the persistent scan to release an SM (measured: a pack queued behind
+// two scan launches delayed its chunk's drain by ~0.5 ms).
+constexpr int kFreeSMs = 10;   // = pack CTAs (8) + K2 (1) + 1 spare
+constexpr int kPackCtas = 8;
+
 // K4: gather the PRESENT bytes of the chunk's staged tiles into the staging
 // slot.  The host lists the staged tiles, each with the slot offset of its
 // first PRESENT byte (from K2's records), in MAPPED pinned memory: no H2D sits
@@ -648,11 +655,19 @@ constexpr uint32_t kSlicesPerTile = kTileBytes / kPackSlice;  // 16
 
 __global__ void __launch_bounds__(kPackThreads) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
                                                        const uint8_t *cls, uint64_t tb, uint32_t P, uint32_t lg,
-                                                       uint8_t *slot, const StageItem *items, uint32_t n_items) {
+                                                       uint8_t *slot, const StageItem *items, uint32_t n_items,
+                                                       const uint32_t *scan_done, uint32_t epoch) {
     __shared__ StageItem si[kPackBatch];
+    // Launched wide; while the persistent scan still runs (its last chunk not
+    // yet published) only the first kPackCtas CTAs work -- the SMs K1 leaves
+    // free -- and the rest exit at once.  Decided when the pack RUNS: packs
+    // are enqueued long before their slot frees up.
+    const bool wide = scan_done == nullptr || *reinterpret_cast<const volatile uint32_t *>(scan_done) == epoch;
+    const uint32_t G = wide ? gridDim.x : min(gridDim.x, (uint32_t)kPackCtas);
+    if (blockIdx.x >= G) return;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const uint32_t i0 = (uint32_t)((uint64_t)n_items * blockIdx.x / gridDim.x);
-    const uint32_t i1 = (uint32_t)((uint64_t)n_items * (blockIdx.x + 1) / gridDim.x);
+    const uint32_t i0 = (uint32_t)((uint64_t)n_items * blockIdx.x / G);
+    const uint32_t i1 = (uint32_t)((uint64_t)n_items * (blockIdx.x + 1) / G);
     for (uint32_t b0 = i0; b0 < i1; b0 += kPackBatch) {
         const uint32_t nb = min(kPackBatch, i1 - b0);
         __syncthreads();
@@ -839,12 +854,6 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
     return launched(1);
 }
 
-// K1 leaves kFreeSMs SMs unoccupied so that the previous chunk's K2/K4 (and
-// the restore's K6) start the moment they are enqueued instead of waiting
-// for the persistent scan to release an SM (measured: a pack queued behind
-// two scan launches delayed its chunk's drain by ~0.5 ms).
-constexpr int kFreeSMs = 10;   // = pack CTAs (8) + K2 (1) + 1 spare
-constexpr int kPackCtas = 8;
 
 static int scan_sms(int n_sms) { return n_sms > 4 * kFreeSMs ? n_sms - kFreeSMs : n_sms; }
 
@@ -886,13 +895,16 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, const uint32
 }
 
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tb, uint32_t P,
-                uint32_t lg, uint8_t *slot, const StageItem *items, uint32_t n_items, int n_sms, cudaStream_t st) {
+                uint32_t lg, uint8_t *slot, const StageItem *items, uint32_t n_items, int n_sms,
+                const uint32_t *scan_done, uint32_t epoch, cudaStream_t st) {
     if (n_items == 0) return 0;
-    // the pack runs beside the next chunk's scan: stay on the SMs K1 leaves free
+    // up to 2 CTAs of 1024 per SM; narrowed on the device while the scan runs
     uint64_t grid = ((uint64_t)n_items * kSlicesPerTile + kPackThreads / 32 - 1) / (kPackThreads / 32);
-    const uint64_t cap = n_sms > 4 * kFreeSMs ? kPackCtas : (uint64_t)n_sms * 2;
+    const uint64_t cap = (uint64_t)n_sms * 2;
     if (grid > cap) grid = cap;
-    k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items);
+    if (n_sms <= 4 * kFreeSMs) scan_done = nullptr;  // small GPUs: K1 leaves no SMs free anyway
+    k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items,
+                                                    scan_done, epoch);
     return launched(1);
 }
 
