@@ -179,11 +179,14 @@ def run_ours(args):
     from paper_2502_16631_b200 import gcr, synth
 
     w = synth.make_workload(args.config, rank=rank, page_size=args.page_size, gib=args.gib)
-    ts = w.materialize()
-    torch.cuda.synchronize()
     ctx = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20,
                       n_copy_streams=args.streams, n_staging_slots=args.slots,
                       direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
+    # --release: the state lives in one releasable gcr_mem_alloc block, carved
+    # into the workload's allocations (f2: checkpoint frees the HBM, restore
+    # re-backs the same addresses)
+    ts = w.materialize(region=ctx.alloc_tensor(w.total_bytes, local) if args.release else None)
+    torch.cuda.synchronize()
     for t in ts:
         ctx.register_tensor(t)
     R0 = w.total_bytes
@@ -229,6 +232,8 @@ def run_ours(args):
             ctx.lock()
         img = ctx.checkpoint(gcr.GCR_INCREMENTAL if incremental else gcr.GCR_FULL)
         s_ck = ctx.stats()
+        if args.release:
+            ctx.release()
         if not incremental:
             ctx.restore([img])
         ctx.unlock()
@@ -367,6 +372,11 @@ def run_ours(args):
         "mode": args.mode,
         "chain_restore": chain_restore,
         "probes": probes,
+        "release": {"release_ms": round(sum(r[1]["release_ns"] for r in recs) / K * 1e-6, 3),
+                    "remap_ms": round(sum(r[1]["remap_ns"] for r in recs) / K * 1e-6, 3),
+                    "released_bytes": recs[-1][1]["released_bytes"],
+                    "what": "f2: checkpoint -> gcr_release (HBM returned to the driver) -> restore re-maps the same VAs"}
+        if args.release else None,
     }
     result["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -465,7 +475,12 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--release", action="store_true",
+                    help="full mode: state in releasable gcr_mem_alloc memory; each step releases the HBM after "
+                         "the checkpoint and the restore re-maps the same addresses (SURVEY f2)")
     args = ap.parse_args()
+    if args.release and args.mode != "full":
+        ap.error("--release needs --mode full (the restore re-maps the released memory)")
     if args.direct_min_mb is None:
         from paper_2502_16631_b200 import gcr as _g
         args.direct_min_mb = _g.default_config().direct_min_bytes / (1 << 20)

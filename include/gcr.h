@@ -27,8 +27,9 @@
  *        register/unregister/watch_stream/reserve_host : RUNNING
  *        lock       : RUNNING -> LOCKED           (TIMEOUT: stays RUNNING)
  *        checkpoint : LOCKED -> CHECKPOINTED      (failure: stays LOCKED)
- *        restore    : LOCKED|CHECKPOINTED -> LOCKED
- *        unlock     : LOCKED|CHECKPOINTED -> RUNNING
+ *        release    : CHECKPOINTED -> RELEASED   (device memory freed, VAs kept)
+ *        restore    : LOCKED|CHECKPOINTED|RELEASED -> LOCKED
+ *        unlock     : LOCKED|CHECKPOINTED -> RUNNING   (not from RELEASED)
  *    Any other (phase, call) pair returns GCR_E_STATE and changes nothing.
  */
 #ifndef GCR_H
@@ -64,7 +65,7 @@ typedef enum {
     GCR_E_CUDA = 11     /* a CUDA runtime call failed; message in gcr_last_error */
 } gcr_status;
 
-typedef enum { GCR_RUNNING = 0, GCR_LOCKED = 1, GCR_CHECKPOINTED = 2 } gcr_phase;
+typedef enum { GCR_RUNNING = 0, GCR_LOCKED = 1, GCR_CHECKPOINTED = 2, GCR_RELEASED = 3 } gcr_phase;
 typedef enum { GCR_FULL = 0, GCR_INCREMENTAL = 1 } gcr_mode;
 
 /* Page classes and pagemap flags.  PARENT/PRESENT
@@ -128,6 +129,10 @@ typedef struct {
                                                     the allocations (the rest was packed) */
     uint64_t restore_direct_bytes;               /* last restore: image bytes copied straight into
                                                     the allocations (the rest was scattered) */
+    uint64_t release_ns;                         /* host: last gcr_release (unmap + release) */
+    uint64_t remap_ns;                           /* host: last restore's re-create + re-map (0 if
+                                                    the memory was resident) */
+    uint64_t released_bytes;                     /* last gcr_release: physical bytes returned */
 } gcr_stats;
 
 /* gcr_image_hdr -- 96 bytes, offsets: magic 0, version 8, page_size 12,
@@ -221,14 +226,53 @@ gcr_status gcr_lock(gcr_ctx *ctx);
  * returned and the parent digest state is unchanged. */
 gcr_status gcr_checkpoint(gcr_ctx *ctx, gcr_mode mode, gcr_image **out);
 
-/* LOCKED|CHECKPOINTED -> LOCKED: apply images chain[0..n) in order into the
+/* ---- releasable device memory ----------------------------
+ * The paper's checkpoint action leaves the process "releasing all GPU
+ * resources" and its restore maps device memory "back to the GPU,
+ * memory mappings to their original addresses".  Memory from
+ * gcr_mem_alloc is built from CUDA virtual-memory-management pieces (a
+ * reserved VA range + a physical allocation mapped into it), so the library
+ * can return the physical memory to the driver while keeping the VA range
+ * reserved, and later back the SAME addresses with fresh physical memory:
+ * pointers held by the application (tensors, pointer tables) stay valid. */
+
+/* Allocate `bytes` (> 0) of device memory on the ctx's device, rounded up to
+ * the driver's allocation granularity (2 MiB on B200), readable and writable
+ * from the ctx's device (RUNNING only).  *dptr_out gets the address (2 MiB
+ * aligned).  It is NOT registered: call gcr_register on it (or on sub-ranges)
+ * as with any allocation.  Owned by the ctx: freed by gcr_mem_free or
+ * gcr_destroy.  GCR_E_INVAL (null, bytes == 0), GCR_E_STATE, GCR_E_NOMEM,
+ * GCR_E_CUDA (driver VMM entry points unavailable). */
+gcr_status gcr_mem_alloc(gcr_ctx *ctx, uint64_t bytes, uint64_t *dptr_out);
+
+/* Free memory from gcr_mem_alloc (RUNNING only).  GCR_E_INVAL if dptr is not
+ * the start of such a block or any registered allocation lies inside it. */
+gcr_status gcr_mem_free(gcr_ctx *ctx, uint64_t dptr);
+
+/* CHECKPOINTED -> RELEASED: return the physical memory behind every registered
+ * allocation to the driver, keeping the virtual address ranges reserved
+ * (P:162-164).  Every registered allocation must lie in a gcr_mem_alloc block
+ * and every block that holds one must be covered completely by registered
+ * allocations (bytes outside the registry would be lost): otherwise
+ * GCR_E_INVAL and nothing changes.  From RELEASED only gcr_restore (which first
+ * re-backs the same addresses, then applies the chain) and gcr_destroy are
+ * legal; unlock returns GCR_E_STATE (the memory is gone: SPEC S:180).
+ * GCR_E_CUDA if the driver refuses an unmap (the phase is then RELEASED if any
+ * block was released). */
+gcr_status gcr_release(gcr_ctx *ctx);
+
+/* LOCKED|CHECKPOINTED|RELEASED -> LOCKED: apply images chain[0..n) in order into the
  * registered allocations: PRESENT pages copied H2D and scattered (K6),
  * ZERO pages filled (K7), PARENT pages skipped; entries map to allocations by
  * index, so allocations may live at new addresses (R-14).  Then every page's
  * CRC32C is recomputed and compared with chain[n-1]'s digests (K8, R-11).
  * Validation happens before any write, in order: meta CRC (CORRUPT), version
  * (VERSION), layout vs registry (LAYOUT), chain order (CHAIN).  After a
- * successful restore the ctx's parent digest state is chain[n-1]'s.
+ * successful restore the ctx's parent digest state is chain[n-1]'s.  From
+ * RELEASED, after validation, every released block is backed again at its
+ * original address (GCR_E_NOMEM leaves the phase RELEASED) before the
+ * chain is applied -- the chain starts with a full image, which writes every
+ * page.
  * GCR_E_VERIFY: counts in gcr_get_stats (verify_failures, first_bad_page);
  * memory content is then undefined, as after GCR_E_CUDA once writes began. */
 gcr_status gcr_restore(gcr_ctx *ctx, gcr_image *const *chain, uint32_t n);

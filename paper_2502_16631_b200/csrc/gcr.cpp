@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include <cuda.h>  // VMM types only: entry points come from cudaGetDriverEntryPoint (no -lcuda)
+
 #include "../../include/gcr.h"
 #include "gcr_internal.h"
 
@@ -140,6 +142,89 @@ struct RegEntry {
     uint64_t dptr, bytes;
 };
 
+// A gcr_mem_alloc block (f2): reserved VA range + physical backing.
+struct MemBlock {
+    uint64_t va, user_bytes, size;  // size: user_bytes rounded up to the granularity
+    CUmemGenericAllocationHandle h;
+    bool mapped;
+};
+
+// Driver VMM entry points, resolved once through the runtime.
+struct Vmm {
+    decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemAddressFree) addr_free = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) set_access = nullptr;
+    bool ok = false;
+};
+
+const Vmm &vmm() {
+    static const Vmm v = [] {
+        Vmm r;
+        auto get = [](const char *name, void *fp) {
+            cudaDriverEntryPointQueryResult q{};
+            return cudaGetDriverEntryPoint(name, reinterpret_cast<void **>(fp), cudaEnableDefault, &q) ==
+                       cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess;
+        };
+        r.ok = get("cuMemGetAllocationGranularity", &r.granularity) && get("cuMemAddressReserve", &r.reserve) &&
+               get("cuMemAddressFree", &r.addr_free) && get("cuMemCreate", &r.create) &&
+               get("cuMemRelease", &r.release) && get("cuMemMap", &r.map) && get("cuMemUnmap", &r.unmap) &&
+               get("cuMemSetAccess", &r.set_access);
+        cudaGetLastError();
+        return r;
+    }();
+    return v;
+}
+
+CUmemAllocationProp mem_prop(int device) {
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    return prop;
+}
+
+// Back [b.va, b.va + b.size) with new physical memory (cuMemCreate + Map + SetAccess).
+CUresult map_block(int device, MemBlock &b) {
+    const Vmm &v = vmm();
+    const CUmemAllocationProp prop = mem_prop(device);
+    CUmemGenericAllocationHandle h{};
+    CUresult r = v.create(&h, b.size, &prop, 0);
+    if (r != CUDA_SUCCESS) return r;
+    r = v.map(b.va, b.size, 0, h, 0);
+    if (r != CUDA_SUCCESS) {
+        v.release(h);
+        return r;
+    }
+    CUmemAccessDesc ad{};
+    ad.location = prop.location;
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = v.set_access(b.va, b.size, &ad, 1);
+    if (r != CUDA_SUCCESS) {
+        v.unmap(b.va, b.size);
+        v.release(h);
+        return r;
+    }
+    b.h = h;
+    b.mapped = true;
+    return CUDA_SUCCESS;
+}
+
+// Return the physical memory (the VA range stays reserved).
+CUresult unmap_block(MemBlock &b) {
+    const Vmm &v = vmm();
+    CUresult r = v.unmap(b.va, b.size);
+    if (r != CUDA_SUCCESS) return r;
+    r = v.release(b.h);
+    b.mapped = false;
+    return r;
+}
+
 struct Chunk {
     uint64_t tile_begin, tile_end, page_begin, page_end, row_begin, row_end;
 };
@@ -168,6 +253,7 @@ struct gcr_ctx {
 
     std::vector<RegEntry> reg;
     uint32_t next_id = 1;
+    std::vector<MemBlock> blocks;  // gcr_mem_alloc (f2)
     std::vector<cudaStream_t> watched;
 
     cudaStream_t compute = nullptr;
@@ -191,7 +277,8 @@ struct gcr_ctx {
     uint8_t *cls = nullptr;
     TileInfo *tile_info = nullptr;
     uint64_t *chunk_rows_d = nullptr;  // chunk row boundaries (nch + 1), then {0, n_rows} for verify
-    uint32_t *chunk_sync_d = nullptr;  // per chunk: K1 arrival counter [0, nch), chunk_done [nch, 2 nch)
+    uint32_t *chunk_sync_d = nullptr;  // per chunk: K1 arrival counter [0, nch), chunk_done [nch, 2 nch),
+                                       // K4 width decision [2 nch, 3 nch)
     uint32_t epoch = 0;                // K1 launch id published in chunk_done
     uint32_t *fold_slots = nullptr;  // K1's cut-page fold: 2 words per K1 warp, zero between launches
     FoldSlots fold{};
@@ -381,11 +468,11 @@ gcr_status build_layout(gcr_ctx *c) {
         CUDA_TRY(c, cudaMalloc(&c->chunk_rows_d, 8 * cr.size()));
         CUDA_TRY(c, cudaMemcpy(c->chunk_rows_d, cr.data(), 8 * cr.size(), cudaMemcpyHostToDevice));
         const uint64_t ns = std::max<uint64_t>(nch, 1);
-        CUDA_TRY(c, cudaMalloc(&c->chunk_sync_d, 2 * 4 * ns));
-        CUDA_TRY(c, cudaMemset(c->chunk_sync_d, 0, 2 * 4 * ns));
+        CUDA_TRY(c, cudaMalloc(&c->chunk_sync_d, 3 * 4 * ns));
+        CUDA_TRY(c, cudaMemset(c->chunk_sync_d, 0, 3 * 4 * ns));
         // fold slots: one pair per K1 warp per chunk (warps run ahead into later
         // chunks independently, so chunks never share slots)
-        const uint64_t w = scan_workers(c->n_sms) * ns;
+        const uint64_t w = scan_workers(c->n_sms, false) * ns;  // the verify K8 uses every SM
         CUDA_TRY(c, cudaMalloc(&c->fold_slots, 2 * 4 * w));
         CUDA_TRY(c, cudaMemset(c->fold_slots, 0, 2 * 4 * w));
         c->fold = FoldSlots{c->fold_slots, c->fold_slots + w};
@@ -584,6 +671,10 @@ gcr_status gcr_destroy(gcr_ctx *c) {
     sync_all(c);
     while (!c->images.empty()) destroy_image(c, c->images.back());
     free_layout(c);
+    for (MemBlock &b : c->blocks) {
+        if (b.mapped) unmap_block(b);
+        vmm().addr_free(b.va, b.size);
+    }
     for (uint8_t *s : c->slots) cudaFree(s);
     for (cudaStream_t s : c->copy) cudaStreamDestroy(s);
     if (c->compute) cudaStreamDestroy(c->compute);
@@ -697,6 +788,7 @@ gcr_status gcr_lock(gcr_ctx *c) {
 
 gcr_status gcr_unlock(gcr_ctx *c) {
     if (!c) return GCR_E_INVAL;
+    if (c->phase == GCR_RELEASED) return fail(c, GCR_E_STATE, "unlock: device memory is released; restore first");
     if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "unlock: not locked");
     auto t0 = Clock::now();
     c->phase = GCR_RUNNING;
@@ -737,6 +829,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.cls = c->cls;
     sp.tile_info = c->tile_info;
     sp.tables = c->tables_d;
+    sp.prefetch = scan_prefetch_bytes();
 
     const size_t nch = c->chunks.size();
     // One persistent K1 for the whole registry, walking the chunks in order;
@@ -931,7 +1024,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             // narrowed to the SMs K1 leaves free while the scan's last chunk is unpublished
             LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, ch.tile_begin, P, c->lg, c->slots[i % NS],
                                       c->stage_map + ch.tile_begin, n_items, c->n_sms, sp.chunk_done + (nch - 1),
-                                      sp.epoch, c->packs));
+                                      sp.epoch, c->chunk_sync_d + 2 * std::max<size_t>(nch, 1) + i, c->packs));
         } else {
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
         }
@@ -1098,8 +1191,8 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
         cudaMemset(c->tile_info, 0, sizeof(TileInfo) * c->n_tiles);
         {
             const uint64_t ns = std::max<size_t>(c->chunks.size(), 1);
-            cudaMemset(c->chunk_sync_d, 0, 2 * 4 * ns);
-            cudaMemset(c->fold_slots, 0, 2 * 4 * scan_workers(c->n_sms) * ns);
+            cudaMemset(c->chunk_sync_d, 0, 3 * 4 * ns);
+            cudaMemset(c->fold_slots, 0, 2 * 4 * scan_workers(c->n_sms, false) * ns);
         }
         cudaGetLastError();
         image_free_buffers(img);
@@ -1132,7 +1225,8 @@ static gcr_status ensure_desc(gcr_ctx *c, uint64_t bytes) {
 
 gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
     if (!c) return GCR_E_INVAL;
-    if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "restore: not locked");
+    if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED && c->phase != GCR_RELEASED)
+        return fail(c, GCR_E_STATE, "restore: not locked");
     if (!chain || n == 0) return fail(c, GCR_E_INVAL, "restore: empty chain");
     for (uint32_t k = 0; k < n; k++)
         if (!chain[k] || chain[k]->ctx != c) return fail(c, GCR_E_INVAL, "restore: image of another ctx or NULL");
@@ -1163,6 +1257,19 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
             return fail(c, GCR_E_CHAIN, "restore: parent_generation link broken");
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
+    st.remap_ns = 0;
+    if (c->phase == GCR_RELEASED) {  // back the same VAs again, then apply the chain
+        const auto r0 = Clock::now();
+        for (MemBlock &b : c->blocks) {
+            if (b.mapped) continue;
+            const CUresult r = map_block(c->device, b);
+            if (r != CUDA_SUCCESS)
+                return fail(c, r == CUDA_ERROR_OUT_OF_MEMORY ? GCR_E_NOMEM : GCR_E_CUDA,
+                            "restore: re-mapping released memory failed (driver error " + std::to_string((int)r) + ")");
+        }
+        st.remap_ns = ns_since(r0);
+        c->phase = GCR_LOCKED;  // memory is back (content undefined until the chain is applied)
+    }
     gcr_status s = build_layout(c);
     if (s != GCR_OK) return s;
     c->ev_used = 0;
@@ -1318,7 +1425,8 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;
         sp.chunk_arrive = c->chunk_sync_d;
         sp.chunk_done = c->chunk_sync_d + std::max<size_t>(nch, 1);
-        sp.workers = scan_workers(c->n_sms);
+        sp.workers = scan_workers(c->n_sms, false);  // nothing runs beside the verify: every SM
+        sp.prefetch = scan_prefetch_bytes();
         sp.page_size = P;
         sp.log2_page = c->lg;
         sp.z_page = c->z_page;
@@ -1364,6 +1472,94 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
     c->have_parent = true;
     c->next_gen = std::max(c->next_gen, last->hdr.generation + 1);
     return GCR_OK;
+}
+
+gcr_status gcr_mem_alloc(gcr_ctx *c, uint64_t bytes, uint64_t *dptr_out) {
+    if (!c) return GCR_E_INVAL;
+    if (!dptr_out || bytes == 0) return fail(c, GCR_E_INVAL, "mem_alloc: null or empty");
+    *dptr_out = 0;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "mem_alloc: not RUNNING");
+    const Vmm &v = vmm();
+    if (!v.ok) return fail(c, GCR_E_CUDA, "mem_alloc: driver VMM entry points unavailable");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const CUmemAllocationProp prop = mem_prop(c->device);
+    size_t gran = 0;
+    if (v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || gran == 0)
+        return fail(c, GCR_E_CUDA, "mem_alloc: cuMemGetAllocationGranularity failed");
+    MemBlock b{};
+    b.user_bytes = bytes;
+    b.size = (bytes + gran - 1) / gran * gran;
+    CUdeviceptr va = 0;
+    if (v.reserve(&va, b.size, gran, 0, 0) != CUDA_SUCCESS)
+        return fail(c, GCR_E_NOMEM, "mem_alloc: cuMemAddressReserve failed");
+    b.va = va;
+    const CUresult r = map_block(c->device, b);
+    if (r != CUDA_SUCCESS) {
+        v.addr_free(b.va, b.size);
+        return fail(c, r == CUDA_ERROR_OUT_OF_MEMORY ? GCR_E_NOMEM : GCR_E_CUDA,
+                    "mem_alloc: cuMemCreate/Map failed (driver error " + std::to_string((int)r) + ")");
+    }
+    c->blocks.push_back(b);
+    *dptr_out = b.va;
+    return GCR_OK;
+}
+
+gcr_status gcr_mem_free(gcr_ctx *c, uint64_t dptr) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "mem_free: not RUNNING");
+    for (size_t i = 0; i < c->blocks.size(); i++) {
+        MemBlock &b = c->blocks[i];
+        if (b.va != dptr) continue;
+        for (const RegEntry &r : c->reg)
+            if (r.dptr < b.va + b.size && b.va < r.dptr + r.bytes)
+                return fail(c, GCR_E_INVAL, "mem_free: a registered allocation lies in the block");
+        CUDA_TRY(c, cudaSetDevice(c->device));
+        CUDA_TRY(c, cudaDeviceSynchronize());  // no kernel may still touch it
+        if (b.mapped && unmap_block(b) != CUDA_SUCCESS) return fail(c, GCR_E_CUDA, "mem_free: cuMemUnmap failed");
+        vmm().addr_free(b.va, b.size);
+        c->blocks.erase(c->blocks.begin() + i);
+        return GCR_OK;
+    }
+    return fail(c, GCR_E_INVAL, "mem_free: not a gcr_mem_alloc block");
+}
+
+gcr_status gcr_release(gcr_ctx *c) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "release: not CHECKPOINTED");
+    // every registered allocation inside a block; every touched block fully registered
+    std::vector<uint64_t> covered(c->blocks.size(), 0);
+    for (const RegEntry &r : c->reg) {
+        size_t k = 0;
+        for (; k < c->blocks.size(); k++) {
+            const MemBlock &b = c->blocks[k];
+            if (r.dptr >= b.va && r.dptr + r.bytes <= b.va + b.user_bytes) break;
+        }
+        if (k == c->blocks.size())
+            return fail(c, GCR_E_INVAL, "release: a registered allocation is not gcr_mem_alloc memory");
+        covered[k] += r.bytes;
+    }
+    for (size_t k = 0; k < c->blocks.size(); k++)
+        if (covered[k] != 0 && covered[k] != c->blocks[k].user_bytes)
+            return fail(c, GCR_E_INVAL, "release: a block is only partly registered (its other bytes would be lost)");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    sync_all(c);
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    const auto t0 = Clock::now();
+    uint64_t freed = 0;
+    gcr_status s = GCR_OK;
+    for (size_t k = 0; k < c->blocks.size(); k++) {
+        MemBlock &b = c->blocks[k];
+        if (covered[k] == 0 || !b.mapped) continue;
+        if (unmap_block(b) != CUDA_SUCCESS) {
+            s = fail(c, GCR_E_CUDA, "release: cuMemUnmap/cuMemRelease failed");
+            if (b.mapped) break;  // still mapped: stop here
+        }
+        freed += b.size;
+    }
+    c->stats.release_ns = ns_since(t0);
+    c->stats.released_bytes = freed;
+    if (freed) c->phase = GCR_RELEASED;
+    return s;
 }
 
 gcr_status gcr_get_phase(const gcr_ctx *c, gcr_phase *out) {

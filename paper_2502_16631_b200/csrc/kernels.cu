@@ -39,6 +39,7 @@
 // (one GF(2) product with fold_m[d], lane-parallel) and XORed into the page's
 // owner slot; the piece that completes the page's rows finalizes it.
 #include <cstdio>
+#include <cstdlib>
 
 #include "gcr_internal.h"
 
@@ -59,6 +60,10 @@ constexpr int kScanThreads = GCR_SCAN_THREADS;
 #endif
 constexpr int kScanUnroll = GCR_SCAN_UNROLL;
 constexpr unsigned kFull = 0xFFFFFFFFu;
+#ifndef GCR_SCAN_PREFETCH_DEFAULT
+#define GCR_SCAN_PREFETCH_DEFAULT 4096
+#endif
+constexpr uint32_t kScanPrefetchDefault = GCR_SCAN_PREFETCH_DEFAULT;
 
 enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3, kA128 = 4, kA256 = 5 };
 
@@ -75,6 +80,11 @@ __device__ __forceinline__ uint4 ldg_stream(const void *p) {
         : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
         : "l"(p));
     return r;
+}
+
+// Request [p, p + bytes) into L2 (one bulk async prefetch; no completion to wait on).
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 template <int kOff>
@@ -113,8 +123,11 @@ __device__ __forceinline__ void row_step(uint32_t lane4, uint32_t sb, uint32_t (
     x[3] = braid(x[3], lane4, sb) ^ w.w;
 }
 
-// raw() of the warp's 512-byte Y block; valid in lane 0.
-__device__ __forceinline__ uint32_t warp_raw(const uint32_t *small, const uint32_t (&x)[4]) {
+// raw() of the warp's 512-byte Y block; valid in lane 0.  Tree level j only
+// needs the lanes that are multiples of 2^(j+1): the others skip the lookups,
+// which also thins the bank conflicts of these unreplicated tables (this
+// per-page cost is what small pages pay on top of the braid lookups).
+__device__ __forceinline__ uint32_t warp_raw(const uint32_t *small, const uint32_t (&x)[4], uint32_t lane) {
     const uint32_t *t4 = small + kT4 * 1024u;
     uint32_t v = apply_tab(t4, x[0]);
     v = apply_tab(t4, v ^ x[1]);
@@ -123,7 +136,7 @@ __device__ __forceinline__ uint32_t warp_raw(const uint32_t *small, const uint32
 #pragma unroll
     for (int j = 0; j < 5; j++) {
         const uint32_t o = __shfl_down_sync(kFull, v, 1 << j);
-        v = apply_tab(small + (kA16 + j) * 1024u, v) ^ o;
+        if ((lane & ((2u << j) - 1u)) == 0u) v = apply_tab(small + (kA16 + j) * 1024u, v) ^ o;
     }
     return v;
 }
@@ -381,7 +394,7 @@ __device__ __forceinline__ AllocView load_alloc(const AllocDev *al, uint32_t P) 
 struct LoadCursor {
     const char *addr;
     uint32_t a, pi, vr;
-    uint64_t base;
+    uint64_t base, end;  // the current allocation's [base, end)
     uint32_t n_pages, tail_len;
     bool mask;  // next row is the first row of a short page and this lane's 16 B lie in its padding
 };
@@ -391,6 +404,7 @@ __device__ __forceinline__ void lc_next_page(LoadCursor &lc, const AllocDev *all
     if (++lc.pi == lc.n_pages) {
         const AllocDev *al = allocs + (++lc.a);
         lc.base = __ldg(&al->base);
+        lc.end = lc.base + __ldg(&al->bytes);
         lc.n_pages = __ldg(&al->n_pages);
         lc.tail_len = __ldg(&al->tail_len);
         lc.pi = 0;
@@ -405,10 +419,18 @@ __device__ __forceinline__ void lc_next_page(LoadCursor &lc, const AllocDev *all
 
 template <int U>
 __device__ __forceinline__ void load_rows(uint4 (&w)[U], int &left, LoadCursor &lc, const AllocDev *allocs,
-                                          uint32_t P, uint32_t lg, uint32_t lane) {
+                                          uint32_t P, uint32_t lg, uint32_t lane, uint32_t pf) {
     const uint32_t Rp = P >> kLog2Row;
     if (lc.vr == Rp) lc_next_page(lc, allocs, P, lg, lane);
     const int cnt = min(min(U, left), (int)(Rp - lc.vr));
+    // keep the stream requested pf bytes ahead: the block pf bytes past this
+    // one, if it still lies in this warp's range and in this allocation (the
+    // real rows of an allocation are contiguous in memory)
+    if (pf != 0u && lane == 0u) {
+        const uint64_t a = reinterpret_cast<uint64_t>(lc.addr) + pf;
+        if ((uint64_t)left * kRowBytes >= pf + U * kRowBytes && a >= lc.base && a + U * kRowBytes <= lc.end)
+            prefetch_l2(reinterpret_cast<const void *>(a), U * kRowBytes);
+    }
     if (cnt == U && !lc.mask) {
 #pragma unroll
         for (int u = 0; u < U; u++) w[u] = ldg_stream(lc.addr + (u << kLog2Row));
@@ -441,7 +463,7 @@ __device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
 __device__ __forceinline__ void page_end(const ScanParams &p, const ChunkCtx &cc, ProcCursor &pc, uint32_t (&x)[4],
                                          uint32_t &acc, const uint32_t *small, uint32_t lane) {
     const uint32_t P = p.page_size, lg = p.log2_page;
-    const uint32_t raw = warp_raw(small, x);
+    const uint32_t raw = warp_raw(small, x, lane);
     const bool nz = __any_sync(kFull, acc != 0);
     const bool whole = pc.vstart == pc.r0;
     if (lane == 0) {
@@ -566,6 +588,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             lc.pi = pc.pi;
             lc.vr = pc.vr;
             lc.base = pc.al.base;
+            lc.end = pc.al.base + __ldg(&p.allocs[a].bytes);
             lc.n_pages = pc.al.n_pages;
             lc.tail_len = pc.al.tail_len;
             lc.addr = reinterpret_cast<const char *>(pc.al.base + ((uint64_t)pc.pi << lg)) - pad0 +
@@ -574,20 +597,25 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
 
             constexpr int U = kScanUnroll;
             int to_load = (int)(rend - r), to_proc = to_load;
+            if (p.prefetch != 0u && lane == 0u) {  // the range's first pf bytes (clamped to the allocation)
+                const uint64_t a0 = max(reinterpret_cast<uint64_t>(lc.addr), lc.base);  // a short page's row may start before it
+                const uint64_t e = min(min(a0 + p.prefetch, lc.end), a0 + (uint64_t)to_load * kRowBytes);
+                if (e > a0) prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(e - a0));
+            }
             uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u;
             uint4 wa[U], wb[U];
-            load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
+            load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
             while (to_proc > 0) {
-                if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane);
+                if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
                 process_rows<U>(p, cc, pc, wa, to_proc, x, acc, small, lane4, sb, lane);
                 if (to_proc <= 0) break;
-                if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane);
+                if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
                 process_rows<U>(p, cc, pc, wb, to_proc, x, acc, small, lane4, sb, lane);
             }
             // the range ended inside a page: advance the piece to the page end
             // (d = Rp - vr rows) and arrive at the page's owner slot
             if (pc.vr != pc.vstart) {
-                const uint32_t raw = __shfl_sync(kFull, warp_raw(small, x), 0);
+                const uint32_t raw = __shfl_sync(kFull, warp_raw(small, x, lane), 0);
                 const bool nz = __any_sync(kFull, acc != 0);
                 const uint32_t contrib = warp_mulmod(__ldg(&p.tables->fold_m[Rp - pc.vr]), raw, lane);
                 if (lane == 0)
@@ -656,14 +684,35 @@ constexpr uint32_t kSlicesPerTile = kTileBytes / kPackSlice;  // 16
 __global__ void __launch_bounds__(kPackThreads) k_pack(const AllocDev *allocs, const uint32_t *tile_alloc,
                                                        const uint8_t *cls, uint64_t tb, uint32_t P, uint32_t lg,
                                                        uint8_t *slot, const StageItem *items, uint32_t n_items,
-                                                       const uint32_t *scan_done, uint32_t epoch) {
+                                                       const uint32_t *scan_done, uint32_t epoch,
+                                                       uint32_t *decision) {
     __shared__ StageItem si[kPackBatch];
+    __shared__ uint32_t s_wide;
     // Launched wide; while the persistent scan still runs (its last chunk not
     // yet published) only the first kPackCtas CTAs work -- the SMs K1 leaves
-    // free -- and the rest exit at once.  Decided when the pack RUNS: packs
-    // are enqueued long before their slot frees up.
-    const bool wide = scan_done == nullptr || *reinterpret_cast<const volatile uint32_t *>(scan_done) == epoch;
-    const uint32_t G = wide ? gridDim.x : min(gridDim.x, (uint32_t)kPackCtas);
+    // free -- and the rest exit at once.  Decided when the pack RUNS (packs
+    // are enqueued long before their slot frees up), ONCE per launch: the
+    // first CTA to get here publishes its reading in this chunk's decision
+    // word (tagged with the epoch) and every CTA uses that one -- CTAs reading
+    // scan_done on their own could straddle the scan's end and split the items
+    // with different grid widths (some packed twice, some never).
+    if (threadIdx.x == 0) {
+        uint32_t w = 1u;
+        if (scan_done != nullptr) {
+            const uint32_t tag = (epoch & 0x7FFFFFFFu) << 1;
+            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(decision);
+            if ((cur & ~1u) == tag) {
+                w = cur & 1u;
+            } else {
+                const uint32_t mine = *reinterpret_cast<const volatile uint32_t *>(scan_done) == epoch ? 1u : 0u;
+                const uint32_t prev = atomicCAS(decision, cur, tag | mine);
+                w = prev == cur ? mine : (prev & 1u);  // lost the race: the winner's reading
+            }
+        }
+        s_wide = w;
+    }
+    __syncthreads();
+    const uint32_t G = s_wide ? gridDim.x : min(gridDim.x, (uint32_t)kPackCtas);
     if (blockIdx.x >= G) return;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t i0 = (uint32_t)((uint64_t)n_items * blockIdx.x / G);
@@ -855,9 +904,23 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
 }
 
 
-static int scan_sms(int n_sms) { return n_sms > 4 * kFreeSMs ? n_sms - kFreeSMs : n_sms; }
+static int scan_sms(int n_sms, bool leave_free) {
+    return leave_free && n_sms > 4 * kFreeSMs ? n_sms - kFreeSMs : n_sms;
+}
 
-uint64_t scan_workers(int n_sms) { return (uint64_t)scan_sms(n_sms) * (kScanThreads / 32); }
+uint64_t scan_workers(int n_sms, bool leave_free) { return (uint64_t)scan_sms(n_sms, leave_free) * (kScanThreads / 32); }
+
+// K1 keeps each warp's stream requested into L2 this many bytes ahead of its
+// register loads (cp.async.bulk.prefetch.L2: no registers, no shared memory),
+// so the ~50 KiB of register double buffers per SM only have to cover L2
+// latency, not HBM latency.  GCR_SCAN_PREFETCH overrides (0 = off).
+uint32_t scan_prefetch_bytes() {
+    static const uint32_t v = [] {
+        const char *e = std::getenv("GCR_SCAN_PREFETCH");
+        return e ? (uint32_t)std::strtoul(e, nullptr, 0) & ~15u : kScanPrefetchDefault;
+    }();
+    return v;
+}
 
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     // once per device: setting a function attribute can serialise with work in
@@ -896,7 +959,7 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, const uint32
 
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tb, uint32_t P,
                 uint32_t lg, uint8_t *slot, const StageItem *items, uint32_t n_items, int n_sms,
-                const uint32_t *scan_done, uint32_t epoch, cudaStream_t st) {
+                const uint32_t *scan_done, uint32_t epoch, uint32_t *decision, cudaStream_t st) {
     if (n_items == 0) return 0;
     // up to 2 CTAs of 1024 per SM; narrowed on the device while the scan runs
     uint64_t grid = ((uint64_t)n_items * kSlicesPerTile + kPackThreads / 32 - 1) / (kPackThreads / 32);
@@ -904,7 +967,7 @@ int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_
     if (grid > cap) grid = cap;
     if (n_sms <= 4 * kFreeSMs) scan_done = nullptr;  // small GPUs: K1 leaves no SMs free anyway
     k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items,
-                                                    scan_done, epoch);
+                                                    scan_done, epoch, decision);
     return launched(1);
 }
 

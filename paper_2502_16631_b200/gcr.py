@@ -23,7 +23,7 @@ GCR_OK, GCR_E_INVAL, GCR_E_STATE, GCR_E_TIMEOUT, GCR_E_PEER, GCR_E_LAYOUT, GCR_E
     GCR_E_CORRUPT, GCR_E_VERSION, GCR_E_VERIFY, GCR_E_NOMEM, GCR_E_CUDA = range(12)
 STATUS_NAMES = ["OK", "E_INVAL", "E_STATE", "E_TIMEOUT", "E_PEER", "E_LAYOUT", "E_CHAIN", "E_CORRUPT",
                 "E_VERSION", "E_VERIFY", "E_NOMEM", "E_CUDA"]
-GCR_RUNNING, GCR_LOCKED, GCR_CHECKPOINTED = 0, 1, 2
+GCR_RUNNING, GCR_LOCKED, GCR_CHECKPOINTED, GCR_RELEASED = 0, 1, 2, 3
 GCR_FULL, GCR_INCREMENTAL = 0, 1
 GCR_PE_PARENT, GCR_PE_PRESENT, GCR_PE_ZERO = 1, 4, 8
 
@@ -38,7 +38,8 @@ _STAT_FIELDS = ["lock_ns", "unlock_ns", "checkpoint_ns", "restore_ns", "scan_dev
                 "compact_dev_ns", "pack_dev_ns", "drain_ns", "restore_h2d_ns", "scatter_dev_ns", "verify_dev_ns",
                 "verify_launches", "pages_scanned", "pages_zero", "pages_parent", "pages_written", "image_bytes",
                 "n_entries", "verify_failures", "first_bad_page", "restore_h2d_bytes", "kernel_launches",
-                "pinned_alloc_ns", "direct_bytes", "restore_direct_bytes"]
+                "pinned_alloc_ns", "direct_bytes", "restore_direct_bytes", "release_ns", "remap_ns",
+                "released_bytes"]
 
 
 class gcr_stats(C.Structure):
@@ -83,6 +84,9 @@ _SIGS = {
     "gcr_get_phase": [_vp, _P(C.c_int)],
     "gcr_get_stats": [_vp, _P(gcr_stats)],
     "gcr_ctx_stream": [_vp, _P(_vp)],
+    "gcr_mem_alloc": [_vp, _u64, _P(_u64)],
+    "gcr_mem_free": [_vp, _u64],
+    "gcr_release": [_vp],
     "gcr_image_header": [_vp, _P(gcr_image_hdr)],
     "gcr_image_allocs": [_vp, _P(_P(gcr_alloc_rec)), _P(_u32)],
     "gcr_image_pagemap": [_vp, _P(_P(gcr_pagemap_entry)), _P(_u64)],
@@ -237,6 +241,37 @@ class Context:
 
     def unlock(self):
         self._check(gcr_unlock(self.h))
+
+    def mem_alloc(self, nbytes: int) -> int:
+        """Releasable device memory (gcr_mem_alloc): returns its device address."""
+        p = C.c_uint64()
+        self._check(gcr_mem_alloc(self.h, nbytes, C.byref(p)))
+        return p.value
+
+    def mem_free(self, dptr: int):
+        self._check(gcr_mem_free(self.h, dptr))
+
+    def alloc_tensor(self, nbytes: int, device: int = 0):
+        """A torch uint8 CUDA tensor over fresh gcr_mem_alloc memory (zero-copy,
+        via __cuda_array_interface__).  The tensor does not own the memory: it
+        stays valid until mem_free / close, and across release -> restore (the
+        address does not change)."""
+        import torch
+        dptr = self.mem_alloc(nbytes)
+
+        class _Mem:
+            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (dptr, False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(_Mem(), device=f"cuda:{device}")
+
+    def release(self):
+        self._check(gcr_release(self.h))
+
+    def try_release(self) -> int:
+        return gcr_release(self.h)
+
+    def try_unlock(self) -> int:
+        return gcr_unlock(self.h)
 
     def phase(self) -> int:
         p = C.c_int()

@@ -174,13 +174,17 @@ class Workload:
             v ^= np.uint32(mx)
         return out
 
-    def materialize(self, device="cuda"):
+    def materialize(self, device="cuda", region=None):
         """Allocate device tensors (torch, plumbing only) and fill them with
-        the GPU generator; returns the list of uint8 tensors."""
+        the GPU generator; returns the list of uint8 tensors.  `region`: a
+        uint8 device tensor of total_bytes to carve the allocations from in
+        order (e.g. releasable gcr_mem_alloc memory)."""
         import torch
         st = torch.cuda.current_stream().cuda_stream
-        if self.contiguous:
-            region = torch.empty(self.total_bytes, dtype=torch.uint8, device=device)
+        if self.contiguous or region is not None:
+            if region is None:
+                region = torch.empty(self.total_bytes, dtype=torch.uint8, device=device)
+            assert region.numel() >= self.total_bytes
             ts, o = [], 0
             for s in self.allocs:
                 ts.append(region[o:o + s.nbytes])

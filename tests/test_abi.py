@@ -23,7 +23,7 @@ def built():
 
 def test_gcr_exports_every_declared_symbol(built):
     names = _declared("gcr.h")
-    assert len(names) == 24
+    assert len(names) == 27
     lib = ctypes.CDLL(built["libgcr.so"])
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
@@ -65,3 +65,6 @@ def test_null_handles(built):
     assert gcr.gcr_destroy(None) == gcr.GCR_E_INVAL
     assert gcr.gcr_lock(None) == gcr.GCR_E_INVAL
     assert gcr.gcr_image_free(None) == gcr.GCR_E_INVAL
+    assert gcr.gcr_release(None) == gcr.GCR_E_INVAL
+    assert gcr.gcr_mem_free(None, 0) == gcr.GCR_E_INVAL
+    assert gcr.gcr_mem_alloc(None, 1 << 20, None) == gcr.GCR_E_INVAL
