@@ -212,6 +212,7 @@ def run_ours(args):
         base_img = ctx.checkpoint(gcr.GCR_FULL)
         ctx.unlock()
     step_no = [0]
+    io_times = []
 
     def step(timed):
         if incremental:  # the "training step": dirty a fresh seeded set of pages (untimed harness work)
@@ -234,6 +235,15 @@ def run_ours(args):
         s_ck = ctx.stats()
         if args.release:
             ctx.release()
+        if args.storage:  # f3: the image goes to a file (durable), comes back from it, then restores
+            path = os.path.join(args.storage, f"gcr_bench_rank{rank}.img")
+            s0 = time.perf_counter()
+            img.write_file(path)
+            s1 = time.perf_counter()
+            img.free()
+            img = ctx.read_file(path)
+            s2 = time.perf_counter()
+            io_times.append((s1 - s0, s2 - s1))
         if not incremental:
             ctx.restore([img])
         ctx.unlock()
@@ -377,6 +387,10 @@ def run_ours(args):
                     "released_bytes": recs[-1][1]["released_bytes"],
                     "what": "f2: checkpoint -> gcr_release (HBM returned to the driver) -> restore re-maps the same VAs"}
         if args.release else None,
+        "storage": {"dir": args.storage, "write_GBps": round(img_b * len(io_times) / max(sum(t[0] for t in io_times), 1e-9) / 1e9, 3),
+                    "read_GBps": round(img_b * len(io_times) / max(sum(t[1] for t in io_times), 1e-9) / 1e9, 3),
+                    "what": "f3: pinned image -> file (parallel pwrite + fdatasync + drop cache) -> pinned image (parallel pread)"}
+        if args.storage else None,
     }
     result["clocks"] = clk.summary()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -463,7 +477,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--page-size", type=int, default=None)
     ap.add_argument("--gib", type=int, default=None, help="C4/C5 GiB per GPU")
-    ap.add_argument("--chunk-mb", type=int, default=256)
+    ap.add_argument("--chunk-mb", type=int, default=1024)
     ap.add_argument("--streams", type=int, default=2)
     ap.add_argument("--slots", type=int, default=0, help="staging slots (0 = one per copy stream)")
     ap.add_argument("--direct-min-mb", type=float, default=None,
@@ -475,10 +489,13 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--storage", default=None, help="full mode: directory for the f3 storage tier round trip")
     ap.add_argument("--release", action="store_true",
                     help="full mode: state in releasable gcr_mem_alloc memory; each step releases the HBM after "
                          "the checkpoint and the restore re-maps the same addresses (SURVEY f2)")
     args = ap.parse_args()
+    if args.storage and args.mode != "full":
+        ap.error("--storage needs --mode full")
     if args.release and args.mode != "full":
         ap.error("--release needs --mode full (the restore re-maps the released memory)")
     if args.direct_min_mb is None:

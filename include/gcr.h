@@ -62,7 +62,9 @@ typedef enum {
     GCR_E_VERSION = 8,  /* unknown image format version */
     GCR_E_VERIFY = 9,   /* restore: at least one page digest differs after the scatter */
     GCR_E_NOMEM = 10,   /* device or pinned host allocation failed */
-    GCR_E_CUDA = 11     /* a CUDA runtime call failed; message in gcr_last_error */
+    GCR_E_CUDA = 11,    /* a CUDA runtime call failed; message in gcr_last_error */
+    GCR_E_IO = 12       /* storage tier: open/read/write/sync of an image file failed (errno
+                           text in gcr_last_error) */
 } gcr_status;
 
 typedef enum { GCR_RUNNING = 0, GCR_LOCKED = 1, GCR_CHECKPOINTED = 2, GCR_RELEASED = 3 } gcr_phase;
@@ -78,7 +80,7 @@ typedef struct {
     uint32_t page_size;       /* power of two in [4096, 2097152]; default 65536 (R-1) */
     uint32_t n_copy_streams;  /* copy streams for drain/restore; default 2, 1..8 */
     uint64_t chunk_bytes;     /* registry bytes scanned per pipeline chunk, also the staging slot
-                                 size; default 256 MiB; multiple of page_size, <= 2 GiB */
+                                 size; default 1 GiB; multiple of page_size, <= 2 GiB */
     uint32_t n_staging_slots; /* device staging slots of chunk_bytes each; 0 (default) = one per
                                  copy stream, else n_copy_streams..16.  Checkpoint chunk i packs
                                  into slot i mod n, so its pack waits only for chunk i - n's
@@ -310,6 +312,26 @@ gcr_status gcr_image_serialize(const gcr_image *img, void *dst, uint64_t cap);
 /* Copy a stream into a new ctx-owned image in pinned memory after checking
  * framing, meta CRC (CORRUPT) and version (VERSION).  Usable in any phase. */
 gcr_status gcr_image_import(gcr_ctx *ctx, const void *stream, uint64_t bytes, gcr_image **out);
+
+/* ---- storage tier: the paper's "memory write time -- the
+ * time to save the memory state to persistent storage" and restore
+ * "from storage".  The file holds exactly the canonical stream
+ * (gcr_image_serialize); it is written and read by n_threads threads (0 = 8)
+ * with positional I/O on disjoint ranges, straight from / into the image's
+ * pinned buffers (no staging copy of the whole stream). ------------------- */
+#define GCR_IO_SYNC 1u  /* fdatasync before returning (durable), then drop the file's page cache so a
+                           later read comes from the device */
+
+/* Create/truncate `path` and write img's canonical stream.  GCR_E_INVAL (null
+ * arguments), GCR_E_IO (errno text in gcr_last_error of the image's ctx). */
+gcr_status gcr_image_write_file(const gcr_image *img, const char *path, uint32_t n_threads, uint32_t flags);
+
+/* Read a stream file into a new ctx-owned image in pinned memory (any phase):
+ * framing, meta CRC (GCR_E_CORRUPT) and version (GCR_E_VERSION) are checked
+ * as in gcr_image_import; the file size must equal the stream size
+ * (GCR_E_CORRUPT otherwise).  GCR_E_IO if the file cannot be opened/read,
+ * GCR_E_NOMEM if pinning fails. */
+gcr_status gcr_image_read_file(gcr_ctx *ctx, const char *path, uint32_t n_threads, gcr_image **out);
 
 #ifdef __cplusplus
 }

@@ -6,7 +6,13 @@
 // overlapped with K1 of the next chunk), the pagemap (K3), the
 // restore pipeline (H2D -> K6 scatter, K7 zero fill, K8 verify; §3.4), the
 // pinned-host pool and the image model.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
 #include <chrono>
 #include <cstddef>
 #include <cstdio>
@@ -600,7 +606,7 @@ gcr_status gcr_config_default(gcr_config *out) {
     if (!out) return GCR_E_INVAL;
     out->page_size = 65536;
     out->n_copy_streams = 2;
-    out->chunk_bytes = 256ull << 20;
+    out->chunk_bytes = 1ull << 30;
     out->n_staging_slots = 0;
     out->verify = 1;
     out->lock_timeout_ms = 10000;
@@ -1693,6 +1699,181 @@ gcr_status gcr_image_import(gcr_ctx *c, const void *stream, uint64_t bytes, gcr_
     std::memcpy(img->digests, o, 4ull * h.n_pages);
     o += 4ull * h.n_pages;
     std::memcpy(img->data, o, h.image_bytes);
+    c->images.push_back(img);
+    *out = img;
+    return GCR_OK;
+}
+
+// ---- storage tier (f3) ------------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+constexpr uint64_t kIoPiece = 64ull << 20;  // bytes per positional read/write unit
+
+struct IoSeg {
+    uint64_t file_off;
+    uint8_t *buf;
+    uint64_t len;
+};
+
+// Positional I/O of every segment, split into kIoPiece units handed out to
+// n threads; returns 0 or the first errno.
+int parallel_io(int fd, const std::vector<IoSeg> &segs, uint32_t n_threads, bool write) {
+    struct Unit {
+        uint64_t off;
+        uint8_t *buf;
+        uint64_t len;
+    };
+    std::vector<Unit> units;
+    for (const IoSeg &sg : segs)
+        for (uint64_t o = 0; o < sg.len; o += kIoPiece)
+            units.push_back(Unit{sg.file_off + o, sg.buf + o, std::min(kIoPiece, sg.len - o)});
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{0};
+    auto work = [&]() {
+        for (size_t i; (i = next.fetch_add(1)) < units.size() && err.load() == 0;) {
+            const Unit &u = units[i];
+            uint64_t done = 0;
+            while (done < u.len) {
+                const ssize_t r = write ? pwrite(fd, u.buf + done, u.len - done, (off_t)(u.off + done))
+                                        : pread(fd, u.buf + done, u.len - done, (off_t)(u.off + done));
+                if (r < 0 && errno == EINTR) continue;
+                if (r <= 0) {
+                    int e0 = 0;
+                    err.compare_exchange_strong(e0, r < 0 ? errno : EIO);
+                    return;
+                }
+                done += (uint64_t)r;
+            }
+        }
+    };
+    const uint32_t T = std::max<uint32_t>(1, std::min<uint32_t>(n_threads ? n_threads : 8, 64));
+    std::vector<std::thread> th;
+    for (uint32_t t = 1; t < T && t < units.size(); t++) th.emplace_back(work);
+    work();
+    for (auto &x : th) x.join();
+    return err.load();
+}
+
+}  // namespace
+
+extern "C" {
+
+gcr_status gcr_image_write_file(const gcr_image *img, const char *path, uint32_t n_threads, uint32_t flags) {
+    if (!img || !path) return GCR_E_INVAL;
+    gcr_ctx *c = img->ctx;
+    const gcr_image_hdr &h = img->hdr;
+    uint64_t total = 0;
+    gcr_image_stream_size(img, &total);
+    const int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+    if (fd < 0) return fail(c, GCR_E_IO, std::string("write_file: open: ") + std::strerror(errno));
+    auto io_fail = [&](const char *what, int e) {
+        close(fd);
+        return fail(c, GCR_E_IO, std::string("write_file: ") + what + ": " + std::strerror(e));
+    };
+    if (ftruncate(fd, (off_t)total) != 0) return io_fail("ftruncate", errno);
+    // header + alloc table are small host vectors: one contiguous prefix
+    std::vector<uint8_t> prefix(96 + 24ull * h.n_allocs);
+    std::memcpy(prefix.data(), &h, 96);
+    if (h.n_allocs) std::memcpy(prefix.data() + 96, img->allocs.data(), 24ull * h.n_allocs);
+    uint64_t o = 0;
+    std::vector<IoSeg> segs;
+    segs.push_back(IoSeg{o, prefix.data(), prefix.size()});
+    o += prefix.size();
+    segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->pagemap), 16ull * h.n_entries});
+    o += 16ull * h.n_entries;
+    segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->digests), 4ull * h.n_pages});
+    o += 4ull * h.n_pages;
+    segs.push_back(IoSeg{o, img->data, h.image_bytes});
+    const int e = parallel_io(fd, segs, n_threads, true);
+    if (e) return io_fail("pwrite", e);
+    if (flags & GCR_IO_SYNC) {
+        if (fdatasync(fd) != 0) return io_fail("fdatasync", errno);
+        posix_fadvise(fd, 0, 0, POSIX_FADV_DONTNEED);  // the next read comes from the device
+    }
+    if (close(fd) != 0) return fail(c, GCR_E_IO, std::string("write_file: close: ") + std::strerror(errno));
+    return GCR_OK;
+}
+
+gcr_status gcr_image_read_file(gcr_ctx *c, const char *path, uint32_t n_threads, gcr_image **out) {
+    if (!c) return GCR_E_INVAL;
+    if (!path || !out) return fail(c, GCR_E_INVAL, "read_file: null argument");
+    *out = nullptr;
+    const int fd = open(path, O_RDONLY | O_CLOEXEC);
+    if (fd < 0) return fail(c, GCR_E_IO, std::string("read_file: open: ") + std::strerror(errno));
+    struct stat sb {};
+    if (fstat(fd, &sb) != 0) {
+        const int e = errno;
+        close(fd);
+        return fail(c, GCR_E_IO, std::string("read_file: fstat: ") + std::strerror(e));
+    }
+    const uint64_t bytes = (uint64_t)sb.st_size;
+    gcr_image_hdr h{};
+    if (bytes < 96 || pread(fd, &h, 96, 0) != 96) {
+        close(fd);
+        return fail(c, GCR_E_CORRUPT, "read_file: shorter than a header");
+    }
+    // framing checks as in gcr_image_import, before allocating anything
+    if (std::memcmp(h.magic, kMagic, 8) != 0 || h.n_pages > bytes / 4 || h.n_entries > bytes / 16 ||
+        h.n_allocs > bytes / 24) {
+        close(fd);
+        return fail(c, GCR_E_CORRUPT, "read_file: bad magic or section sizes exceed the file");
+    }
+    const uint64_t meta = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages;
+    if (meta > bytes || bytes - meta != h.image_bytes) {
+        close(fd);
+        return fail(c, GCR_E_CORRUPT, "read_file: framing mismatch (file size != stream size)");
+    }
+    gcr_image *img = new (std::nothrow) gcr_image;
+    if (!img) {
+        close(fd);
+        return fail(c, GCR_E_NOMEM, "read_file: out of host memory");
+    }
+    auto bail = [&](gcr_status s, const std::string &m) {
+        close(fd);
+        image_free_buffers(img);
+        delete img;
+        return fail(c, s, m);
+    };
+    if (cudaSetDevice(c->device) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(GCR_E_CUDA, "read_file: cudaSetDevice failed");
+    }
+    img->ctx = c;
+    img->hdr = h;
+    img->allocs.resize(h.n_allocs);
+    img->pagemap_cap = 16ull * h.n_entries;
+    img->digests_cap = 4ull * h.n_pages;
+    img->data_cap = h.image_bytes;
+    img->pagemap = static_cast<gcr_pagemap_entry *>(c->pool.alloc(img->pagemap_cap));
+    img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
+    img->data = static_cast<uint8_t *>(c->pool.alloc(img->data_cap));
+    c->stats.pinned_alloc_ns = c->pool.pin_ns;
+    if ((img->pagemap_cap && !img->pagemap) || (img->digests_cap && !img->digests) || (img->data_cap && !img->data))
+        return bail(GCR_E_NOMEM, "read_file: pinned allocation failed");
+    std::vector<IoSeg> segs;
+    uint64_t o = 96;
+    segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->allocs.data()), 24ull * h.n_allocs});
+    o += 24ull * h.n_allocs;
+    segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->pagemap), 16ull * h.n_entries});
+    o += 16ull * h.n_entries;
+    segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->digests), 4ull * h.n_pages});
+    o += 4ull * h.n_pages;
+    segs.push_back(IoSeg{o, img->data, h.image_bytes});
+    const int e = parallel_io(fd, segs, n_threads, false);
+    if (e) return bail(GCR_E_IO, std::string("read_file: pread: ") + std::strerror(e));
+    close(fd);
+    if (meta_crc(img) != h.meta_crc32c) {
+        image_free_buffers(img);
+        delete img;
+        return fail(c, GCR_E_CORRUPT, "read_file: meta_crc32c mismatch");
+    }
+    if (h.version != 1) {
+        image_free_buffers(img);
+        delete img;
+        return fail(c, GCR_E_VERSION, "read_file: unknown version");
+    }
     c->images.push_back(img);
     *out = img;
     return GCR_OK;

@@ -663,8 +663,16 @@ __device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint
 // start the moment they are enqueued instead of waiting
 // for the persistent scan to release an SM (measured: a pack queued behind
 // two scan launches delayed its chunk's drain by ~0.5 ms).
-constexpr int kFreeSMs = 10;   // = pack CTAs (8) + K2 (1) + 1 spare
-constexpr int kPackCtas = 8;
+constexpr int kFreeSMsDefault = 10;  // = pack CTAs (8) + K2 (1) + 1 spare
+// GCR_FREE_SMS overrides (>= 3): pack CTAs = free - 2
+static int free_sms() {
+    static const int v = [] {
+        const char *e = std::getenv("GCR_FREE_SMS");
+        const int f = e ? std::atoi(e) : kFreeSMsDefault;
+        return f < 3 ? 3 : f;
+    }();
+    return v;
+}
 
 // K4: gather the PRESENT bytes of the chunk's staged tiles into the staging
 // slot.  The host lists the staged tiles, each with the slot offset of its
@@ -685,11 +693,11 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const AllocDev *allocs, c
                                                        const uint8_t *cls, uint64_t tb, uint32_t P, uint32_t lg,
                                                        uint8_t *slot, const StageItem *items, uint32_t n_items,
                                                        const uint32_t *scan_done, uint32_t epoch,
-                                                       uint32_t *decision) {
+                                                       uint32_t *decision, uint32_t pack_ctas) {
     __shared__ StageItem si[kPackBatch];
     __shared__ uint32_t s_wide;
     // Launched wide; while the persistent scan still runs (its last chunk not
-    // yet published) only the first kPackCtas CTAs work -- the SMs K1 leaves
+    // yet published) only the first pack_ctas CTAs work -- the SMs K1 leaves
     // free -- and the rest exit at once.  Decided when the pack RUNS (packs
     // are enqueued long before their slot frees up), ONCE per launch: the
     // first CTA to get here publishes its reading in this chunk's decision
@@ -712,7 +720,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const AllocDev *allocs, c
         s_wide = w;
     }
     __syncthreads();
-    const uint32_t G = s_wide ? gridDim.x : min(gridDim.x, (uint32_t)kPackCtas);
+    const uint32_t G = s_wide ? gridDim.x : min(gridDim.x, pack_ctas);
     if (blockIdx.x >= G) return;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const uint32_t i0 = (uint32_t)((uint64_t)n_items * blockIdx.x / G);
@@ -905,7 +913,7 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
 
 
 static int scan_sms(int n_sms, bool leave_free) {
-    return leave_free && n_sms > 4 * kFreeSMs ? n_sms - kFreeSMs : n_sms;
+    return leave_free && n_sms > 4 * free_sms() ? n_sms - free_sms() : n_sms;
 }
 
 uint64_t scan_workers(int n_sms, bool leave_free) { return (uint64_t)scan_sms(n_sms, leave_free) * (kScanThreads / 32); }
@@ -965,9 +973,9 @@ int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_
     uint64_t grid = ((uint64_t)n_items * kSlicesPerTile + kPackThreads / 32 - 1) / (kPackThreads / 32);
     const uint64_t cap = (uint64_t)n_sms * 2;
     if (grid > cap) grid = cap;
-    if (n_sms <= 4 * kFreeSMs) scan_done = nullptr;  // small GPUs: K1 leaves no SMs free anyway
+    if (n_sms <= 4 * free_sms()) scan_done = nullptr;  // small GPUs: K1 leaves no SMs free anyway
     k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items,
-                                                    scan_done, epoch, decision);
+                                                    scan_done, epoch, decision, (uint32_t)(free_sms() - 2));
     return launched(1);
 }
 

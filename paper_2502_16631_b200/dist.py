@@ -96,6 +96,22 @@ def restore_all(ctx, chain, group=None) -> int:
     return st if st != GCR_OK else GCR_E_PEER
 
 
+def release_all(ctx, group=None) -> int:
+    """f2 on every rank after checkpoint_all: barrier, local gcr_release,
+    outcome vote.  A release cannot be rolled back (the HBM is gone): ranks
+    whose release succeeded stay RELEASED and leave it only through restore, so
+    a failed vote is reported (GCR_E_PEER on the ranks that succeeded) for the
+    caller to restore everywhere."""
+    dist = _pg()
+    dist.barrier(group=group)
+    st = ctx.try_release()
+    ok = _vote(st == GCR_OK, group)
+    dist.barrier(group=group)
+    if ok:
+        return GCR_OK
+    return st if st != GCR_OK else GCR_E_PEER
+
+
 def unlock_all(ctx, group=None) -> None:
     ctx.unlock()
     _pg().barrier(group=group)

@@ -20,9 +20,10 @@ _lib = C.CDLL(LIB_PATH)
 
 # ---- enums -------------------------------------------------------------------
 GCR_OK, GCR_E_INVAL, GCR_E_STATE, GCR_E_TIMEOUT, GCR_E_PEER, GCR_E_LAYOUT, GCR_E_CHAIN, \
-    GCR_E_CORRUPT, GCR_E_VERSION, GCR_E_VERIFY, GCR_E_NOMEM, GCR_E_CUDA = range(12)
+    GCR_E_CORRUPT, GCR_E_VERSION, GCR_E_VERIFY, GCR_E_NOMEM, GCR_E_CUDA, GCR_E_IO = range(13)
 STATUS_NAMES = ["OK", "E_INVAL", "E_STATE", "E_TIMEOUT", "E_PEER", "E_LAYOUT", "E_CHAIN", "E_CORRUPT",
-                "E_VERSION", "E_VERIFY", "E_NOMEM", "E_CUDA"]
+                "E_VERSION", "E_VERIFY", "E_NOMEM", "E_CUDA", "E_IO"]
+GCR_IO_SYNC = 1
 GCR_RUNNING, GCR_LOCKED, GCR_CHECKPOINTED, GCR_RELEASED = 0, 1, 2, 3
 GCR_FULL, GCR_INCREMENTAL = 0, 1
 GCR_PE_PARENT, GCR_PE_PRESENT, GCR_PE_ZERO = 1, 4, 8
@@ -96,6 +97,8 @@ _SIGS = {
     "gcr_image_stream_size": [_vp, _P(_u64)],
     "gcr_image_serialize": [_vp, _vp, _u64],
     "gcr_image_import": [_vp, _vp, _u64, _P(_vp)],
+    "gcr_image_write_file": [_vp, C.c_char_p, _u32, _u32],
+    "gcr_image_read_file": [_vp, C.c_char_p, _u32, _P(_vp)],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -166,6 +169,10 @@ class Image:
         if n.value == 0:
             return np.zeros(0, np.uint8)
         return np.ctypeslib.as_array(p, shape=(n.value,))
+
+    def write_file(self, path: str, threads: int = 0, sync: bool = True):
+        """Storage tier (f3): write the canonical stream to `path`."""
+        self.ctx._check(gcr_image_write_file(self.handle, os.fsencode(path), threads, GCR_IO_SYNC if sync else 0))
 
     def free(self):
         if self.handle:
@@ -292,6 +299,12 @@ class Context:
         out = C.c_void_p()
         buf = C.create_string_buffer(data, len(data))
         self._check(gcr_image_import(self.h, buf, len(data), C.byref(out)))
+        return Image(self, out.value)
+
+    def read_file(self, path: str, threads: int = 0) -> Image:
+        """Storage tier (f3): a new image from a stream file."""
+        out = C.c_void_p()
+        self._check(gcr_image_read_file(self.h, os.fsencode(path), threads, C.byref(out)))
         return Image(self, out.value)
 
     def last_error(self) -> str:

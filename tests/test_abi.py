@@ -23,7 +23,7 @@ def built():
 
 def test_gcr_exports_every_declared_symbol(built):
     names = _declared("gcr.h")
-    assert len(names) == 27
+    assert len(names) == 29
     lib = ctypes.CDLL(built["libgcr.so"])
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
@@ -44,7 +44,7 @@ def test_config_defaults_without_gpu(built):
     from paper_2502_16631_b200 import gcr
     cfg = gcr.default_config()
     assert (cfg.page_size, cfg.n_copy_streams, cfg.chunk_bytes, cfg.verify, cfg.lock_timeout_ms) == \
-        (65536, 2, 256 << 20, 1, 10000)   # lock timeout: "10 seconds by default"
+        (65536, 2, 1 << 30, 1, 10000)   # chunk: SURVEY §8(b) default 1 GiB; lock timeout: "10 seconds by default"
     assert cfg.direct_min_bytes == 16 << 20
     assert gcr.gcr_config_default(None) == gcr.GCR_E_INVAL
 

@@ -32,8 +32,9 @@ class FakeImage:
 class FakeCtx:
     """Phase machine of include/gcr.h without a GPU (RUNNING/LOCKED/CHECKPOINTED)."""
 
-    def __init__(self, rank, lock_status=0, restore_status=0, nbytes=1000):
+    def __init__(self, rank, lock_status=0, restore_status=0, nbytes=1000, release_status=0):
         self.rank, self.lock_status, self.restore_status, self.nbytes = rank, lock_status, restore_status, nbytes
+        self.release_status = release_status
         self.phase, self.gen, self.log = 0, 0, []
 
     def try_lock(self):
@@ -55,8 +56,16 @@ class FakeCtx:
         return FakeImage(FakeHeader(self.gen, 10, self.nbytes * (self.rank + 1)))
 
     def try_restore(self, chain):
+        assert self.phase in (1, 2, 3)
         self.phase = 1
         return self.restore_status
+
+    def try_release(self):  # f2: CHECKPOINTED -> RELEASED (3)
+        self.log.append("release")
+        assert self.phase == 2
+        if self.release_status == 0:
+            self.phase = 3
+        return self.release_status
 
 
 def _worker(rank, world, port, scenario, q):
@@ -77,6 +86,15 @@ def _worker(rank, world, port, scenario, q):
             ctx = FakeCtx(rank, lock_status=3 if rank == 1 else 0)
             st = gd.lock_all(ctx)
             q.put((rank, st, ctx.phase, ctx.log))
+        elif scenario == "release":
+            ctx = FakeCtx(rank, release_status=2 if (rank == 1 and world == 3) else 0)
+            gd.lock_all(ctx)
+            img, _ = gd.checkpoint_all(ctx)
+            rl = gd.release_all(ctx)
+            ph = ctx.phase
+            rs = gd.restore_all(ctx, [img])  # the only way out of RELEASED, everywhere
+            gd.unlock_all(ctx)
+            q.put((rank, rl, ph, rs, ctx.phase, ctx.log))
         elif scenario == "verify_on_0":
             ctx = FakeCtx(rank, restore_status=9 if rank == 0 else 0)
             gd.lock_all(ctx)
@@ -123,3 +141,16 @@ def test_lock_timeout_on_one_rank_rolls_back_every_rank():
 def test_restore_failure_on_one_rank_is_reported_everywhere():
     out = _run("verify_on_0")
     assert out == [(0, 9), (1, 4)]
+
+
+def test_release_all_then_restore_all():
+    out = _run("release")
+    for rank, rl, ph, rs, ph_end, log in out:
+        assert rl == 0 and ph == 3 and rs == 0 and ph_end == 0
+        assert log == ["lock", "release", "unlock"]
+
+
+def test_release_failure_on_one_rank_is_reported_everywhere():
+    out = _run("release", world=3)
+    assert [(r, rl, ph) for r, rl, ph, *_ in out] == [(0, 4, 3), (1, 2, 2), (2, 4, 3)]
+    assert all(rs == 0 and ph_end == 0 for _, _, _, rs, ph_end, _ in out)

@@ -1,5 +1,5 @@
 """-m gpu, BASELINE.json's full sizes in the launch configuration bench.py times
-(256 MiB chunks, 2 copy streams, default direct_min): every sampled output is
+(default 1 GiB chunks, 2 copy streams, default direct_min): every sampled output is
 recomputed by the oracle one page at a time from the CPU twin of the
 generator, and whole-image properties that hold at any
 size are checked exactly (counts, Σ nr_pages, framing, meta CRC, restore)."""

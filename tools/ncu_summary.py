@@ -23,6 +23,10 @@ KEYS = [
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
     "launch__shared_mem_per_block_dynamic", "smsp__average_warp_latency_per_inst_issued.ratio",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_lsu_wavefronts.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lts__t_sectors_srcunit_tex_op_read.sum",
+    "sm__memory_throughput.avg.pct_of_peak_sustained_active",
 ]
 STALLS = ["long_scoreboard", "short_scoreboard", "mio_throttle", "wait", "math_pipe_throttle", "barrier",
           "lg_throttle", "not_selected", "selected", "branch_resolving", "no_instruction", "drain", "membar"]
