@@ -283,6 +283,7 @@ struct gcr_ctx {
     uint8_t *cls = nullptr;
     TileInfo *tile_info = nullptr;
     uint64_t *chunk_rows_d = nullptr;  // chunk row boundaries (nch + 1), then {0, n_rows} for verify
+    uint64_t *chunk_groups_d = nullptr;  // K1g (4/8 KiB pages): the same in page groups, else null
     uint32_t *chunk_sync_d = nullptr;  // per chunk: K1 arrival counter [0, nch), chunk_done [nch, 2 nch),
                                        // K4 width decision [2 nch, 3 nch)
     uint32_t epoch = 0;                // K1 launch id published in chunk_done
@@ -358,8 +359,8 @@ bool valid_page_size(uint32_t P) { return P >= 4096u && P <= 2097152u && (P & (P
 
 void free_layout(gcr_ctx *c) {
     void *ptrs[] = {c->allocs_d, c->page_alloc, c->tile_alloc, c->D[0], c->D[1], c->cls, c->tile_info,
-                    c->chunk_rows_d, c->chunk_sync_d, c->fold_slots, c->pm_blk_cnt, c->pm_blk_off, c->run_start,
-                    c->entries_d, c->misc_d};
+                    c->chunk_rows_d, c->chunk_groups_d, c->chunk_sync_d, c->fold_slots, c->pm_blk_cnt,
+                    c->pm_blk_off, c->run_start, c->entries_d, c->misc_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (c->totals_h) cudaFreeHost(c->totals_h);
@@ -380,6 +381,7 @@ void free_layout(gcr_ctx *c) {
     c->cls = nullptr;
     c->tile_info = nullptr;
     c->chunk_rows_d = nullptr;
+    c->chunk_groups_d = nullptr;
     c->chunk_sync_d = nullptr;
     c->fold_slots = nullptr;
     c->pm_blk_cnt = c->pm_blk_off = c->run_start = nullptr;
@@ -398,7 +400,9 @@ gcr_status build_layout(gcr_ctx *c) {
     c->P = P;
     c->lg = lg;
     c->allocs_h.clear();
-    uint64_t g = 0, t = 0, rows = 0;
+    uint64_t g = 0, t = 0, rows = 0, groups = 0;
+    const bool grp = scan_uses_groups(P);
+    const uint64_t G = grp ? kGroupBytes / P : 1;
     for (const RegEntry &r : c->reg) {
         AllocDev a{};
         a.base = r.dptr;
@@ -413,6 +417,8 @@ gcr_status build_layout(gcr_ctx *c) {
         a.row0 = rows;
         a.n_rows = (uint64_t)(a.n_pages - 1) * (P / kRowBytes) + (a.tail_len + kRowBytes - 1) / kRowBytes;
         rows += a.n_rows;
+        a.grp0 = groups;
+        groups += (a.n_pages + G - 1) / G;
         g += a.n_pages;
         t += a.n_tiles;
         c->allocs_h.push_back(a);
@@ -473,6 +479,24 @@ gcr_status build_layout(gcr_ctx *c) {
         cr.push_back(rows);
         CUDA_TRY(c, cudaMalloc(&c->chunk_rows_d, 8 * cr.size()));
         CUDA_TRY(c, cudaMemcpy(c->chunk_rows_d, cr.data(), 8 * cr.size(), cudaMemcpyHostToDevice));
+        if (grp) {  // K1g: chunk boundaries in page groups (tile-aligned chunks are group-aligned)
+            auto group_of_page = [&](uint64_t page) -> uint64_t {
+                if (page >= g) return groups;
+                size_t lo = 0, hi = c->allocs_h.size();
+                while (hi - lo > 1) {
+                    size_t mid = (lo + hi) / 2;
+                    if (c->allocs_h[mid].page0 <= page) lo = mid; else hi = mid;
+                }
+                return c->allocs_h[lo].grp0 + (page - c->allocs_h[lo].page0) / G;
+            };
+            std::vector<uint64_t> cg;
+            for (const Chunk &ch : c->chunks) cg.push_back(group_of_page(ch.page_begin));
+            cg.push_back(groups);
+            cg.push_back(0);
+            cg.push_back(groups);
+            CUDA_TRY(c, cudaMalloc(&c->chunk_groups_d, 8 * cg.size()));
+            CUDA_TRY(c, cudaMemcpy(c->chunk_groups_d, cg.data(), 8 * cg.size(), cudaMemcpyHostToDevice));
+        }
         const uint64_t ns = std::max<uint64_t>(nch, 1);
         CUDA_TRY(c, cudaMalloc(&c->chunk_sync_d, 3 * 4 * ns));
         CUDA_TRY(c, cudaMemset(c->chunk_sync_d, 0, 3 * 4 * ns));
@@ -845,6 +869,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // saturated D2H every launch or event the GPU front-end fetches from host
     // memory costs tens of us).
     sp.chunk_rows = c->chunk_rows_d;
+    sp.chunk_groups = c->chunk_groups_d;  // K1g for 4/8 KiB pages (null: K1)
     sp.n_chunks = (uint32_t)nch;
     sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;  // never 0 (the flags' initial value)
     sp.chunk_arrive = c->chunk_sync_d;
@@ -1427,6 +1452,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.fold = c->fold;
         const size_t nch = c->chunks.size();
         sp.chunk_rows = c->chunk_rows_d + nch + 1;  // one chunk: every real row
+        sp.chunk_groups = c->chunk_groups_d ? c->chunk_groups_d + nch + 1 : nullptr;
         sp.n_chunks = 1;
         sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;
         sp.chunk_arrive = c->chunk_sync_d;

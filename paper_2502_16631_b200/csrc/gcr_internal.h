@@ -33,7 +33,13 @@ struct AllocDev {
     uint32_t z_tail;    // Z(tail_len) = CRC32C of tail_len zero bytes
     uint64_t row0;      // global index of its first REAL 512-byte row
     uint64_t n_rows;    // (n_pages-1)*P/512 + ceil(tail_len/512)
+    uint64_t grp0;      // small pages (K1g): global index of its first page group
 };
+
+// Small pages (P = 4 KiB / 8 KiB): K1g scans G = 16 KiB / P consecutive pages
+// of one allocation (a page GROUP, 16 KiB) at once, one page per 32/G lanes,
+// so the per-page lane tree is shared by G pages.
+constexpr uint32_t kGroupBytes = 16384;
 
 // A page cut by K1 warp-range boundaries is folded inside K1: every warp
 // holding a piece of it XORs the piece's contribution into the page's owner
@@ -116,6 +122,7 @@ struct ScanParams {
     unsigned long long *first_bad;
     const CrcTables *tables;
     uint32_t prefetch;         // bytes: each warp keeps [cursor + prefetch, + block) requested into L2
+    const uint64_t *chunk_groups;  // K1g: n_chunks + 1 global page-group boundaries (device)
 };
 
 struct ScatterDesc {
@@ -137,7 +144,8 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
                             cudaStream_t st);
 uint64_t scan_workers(int n_sms, bool leave_free = true);          // K1 warps (a full persistent grid)
 uint32_t scan_prefetch_bytes();                                     // K1 L2 prefetch distance (GCR_SCAN_PREFETCH)
-int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1
+int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1 (K1g when p.chunk_groups is set)
+bool scan_uses_groups(uint32_t page_size);                          // K1g for this page size?
 // K2 of one chunk: first waits (bounded) until chunk_done[chunk] == epoch.
 int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, const uint32_t *chunk_done,
                      uint32_t chunk, uint32_t epoch, TileRec *host_rec, unsigned long long *rec_count,

@@ -505,49 +505,51 @@ __device__ __forceinline__ void process_rows(const ScanParams &p, const ChunkCtx
     if (pc.vr == Rp) page_end(p, cc, pc, x, acc, small, lane);
 }
 
+// Stage the tables in shared memory: the braid table `gb` (adv_{row}) into
+// all 32 lane-private replicas (word (k>>1)*16384 + e*64 + (k&1)*32 + l) and
+// the small tables (t4, a16 .. a256) once.  Each thread loads a few table
+// words (all loads issued before any store).
+__device__ __forceinline__ void stage_tables(uint32_t *sm, const CrcTables *tables, const uint32_t *gb) {
+    const uint32_t *gs = &tables->t4[0][0];  // t4, a16, ..., a256 are contiguous
+    constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
+    constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
+    uint32_t bv[kPer], sv[kPerS];
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; j++) {
+        const uint32_t ke = threadIdx.x + j * kScanThreads;
+        bv[j] = ke < 1024u ? __ldg(gb + ke) : 0u;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kPerS; j++) {
+        const uint32_t i = threadIdx.x + j * kScanThreads;
+        sv[j] = i < kSmallTables * 1024u ? __ldg(gs + i) : 0u;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; j++) {
+        const uint32_t ke = threadIdx.x + j * kScanThreads;
+        if (ke < 1024u) {
+            const uint32_t k = ke >> 8, e = ke & 255u;
+            uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
+            const uint4 v4 = make_uint4(bv[j], bv[j], bv[j], bv[j]);
+#pragma unroll
+            for (int l = 0; l < 8; l++) dst[l] = v4;
+        }
+    }
+    uint32_t *ss = sm + kBraidSmem / 4;
+#pragma unroll
+    for (uint32_t j = 0; j < kPerS; j++) {
+        const uint32_t i = threadIdx.x + j * kScanThreads;
+        if (i < kSmallTables * 1024u) ss[i] = sv[j];
+    }
+}
+
 // K1.
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
     const uint32_t *small = sm + kBraidSmem / 4;
 
-    // Stage the tables.  Each thread loads a few table words once (all loads
-    // issued before any store) and writes the braid words to all 32 lane-private
-    // replicas: word (k>>1)*16384 + e*64 + (k&1)*32 + l.
-    {
-        const uint32_t *gb = &p.tables->braid[0][0];
-        const uint32_t *gs = &p.tables->t4[0][0];  // t4, a16, ..., a256 are contiguous
-        constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
-        constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
-        uint32_t bv[kPer], sv[kPerS];
-#pragma unroll
-        for (uint32_t j = 0; j < kPer; j++) {
-            const uint32_t ke = threadIdx.x + j * kScanThreads;
-            bv[j] = ke < 1024u ? __ldg(gb + ke) : 0u;
-        }
-#pragma unroll
-        for (uint32_t j = 0; j < kPerS; j++) {
-            const uint32_t i = threadIdx.x + j * kScanThreads;
-            sv[j] = i < kSmallTables * 1024u ? __ldg(gs + i) : 0u;
-        }
-#pragma unroll
-        for (uint32_t j = 0; j < kPer; j++) {
-            const uint32_t ke = threadIdx.x + j * kScanThreads;
-            if (ke < 1024u) {
-                const uint32_t k = ke >> 8, e = ke & 255u;
-                uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
-                const uint4 v4 = make_uint4(bv[j], bv[j], bv[j], bv[j]);
-#pragma unroll
-                for (int l = 0; l < 8; l++) dst[l] = v4;
-            }
-        }
-        uint32_t *ss = sm + kBraidSmem / 4;
-#pragma unroll
-        for (uint32_t j = 0; j < kPerS; j++) {
-            const uint32_t i = threadIdx.x + j * kScanThreads;
-            if (i < kSmallTables * 1024u) ss[i] = sv[j];
-        }
-    }
+    stage_tables(sm, p.tables, &p.tables->braid[0][0]);
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u;
@@ -625,6 +627,167 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         // this warp is done with chunk ch; the last one publishes it for K2
         if (lane == 0) {
             __threadfence();
+            if (atomicAdd(p.chunk_arrive + ch, 1u) == (uint32_t)p.workers - 1u) {
+                atomicExch(p.chunk_arrive + ch, 0u);
+                __threadfence();
+                atomicExch(p.chunk_done + ch, p.epoch);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1g: the scan for small pages (P = 4 KiB: G = 4; 8 KiB: G = 2).  At 4 KiB
+// K1 finalizes a page every 8 rows and the per-page raw16 + lane tree (through
+// unreplicated, bank-conflicting tables) costs as much as the page's braid
+// lookups.  K1g streams a GROUP of G consecutive pages of one allocation (16
+// KiB) as 32 rows of 512 bytes in which lanes [q*QL, (q+1)*QL) (QL = 32/G) read
+// page q's next 512/G bytes: the braid step is adv_{512/G} (the a128 / a256
+// table, staged lane-private), each page's 512/G-byte Y block sits in its own
+// lane group, and ONE raw16 + log2(QL)-level tree finalizes all G pages.
+// Warps take whole groups (equal split of the chunk's groups), so no page is
+// ever cut between warps: no fold.  Loads stay full 128-byte lines.  A short
+// tail page is front-padded with zeros as in K1; a last group with fewer than
+// G pages masks the missing pages' lanes.
+template <int G>
+struct GroupLane {  // this lane's page in the current group
+    const char *ptr;  // address of row 0 for this lane (front padding included)
+    uint32_t pad;     // front padding bytes of a short tail page (0 otherwise)
+    uint32_t pi;      // page index in the allocation
+    bool valid;       // the page exists (partial last group)
+};
+
+template <int G>
+__device__ __forceinline__ GroupLane<G> group_lane(const AllocView &al, uint64_t gi, uint32_t P, uint32_t lg,
+                                                   uint32_t q, uint32_t m) {
+    GroupLane<G> gl;
+    gl.pi = (uint32_t)(gi * G + q);
+    gl.valid = gl.pi < al.n_pages;
+    const bool tail = gl.valid && gl.pi == al.n_pages - 1 && al.tail_len < P;
+    gl.pad = tail ? P - al.tail_len : 0u;
+    gl.ptr = reinterpret_cast<const char *>(al.base + ((uint64_t)gl.pi << lg)) - gl.pad + m * 16u;
+    return gl;
+}
+
+__device__ __forceinline__ uint32_t alloc_of_group(const AllocDev *al, uint32_t n, uint64_t g, uint32_t lane) {
+    uint32_t lo = 0, hi = n;  // al[lo].grp0 <= g < al[hi].grp0
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t probe = lo + lane * step;
+        const bool le = probe < hi && __ldg(&al[probe].grp0) <= g;
+        const uint32_t qm = 31 - __clz(__ballot_sync(kFull, le));
+        lo = lo + qm * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p) {
+    constexpr uint32_t QL = 32 / G, Wr = kRowBytes / G, Rg = 32, U = 4, NB = Rg / U;
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
+    const uint32_t *small = sm + kBraidSmem / 4;
+    stage_tables(sm, p.tables, G == 4 ? &p.tables->a128[0][0] : &p.tables->a256[0][0]);
+    __syncthreads();
+
+    const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
+    const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (wid >= p.workers) return;
+    const uint32_t P = p.page_size, lg = p.log2_page;
+    for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
+        const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
+        const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
+        if (g0 < g1) {
+            // load cursor (group gl_g, block lb) runs one block ahead of the process cursor
+            uint32_t la = alloc_of_group(p.allocs, p.n_allocs, g0, lane);
+            AllocView lal = load_alloc(p.allocs + la, P);
+            uint64_t lgi = g0 - __ldg(&p.allocs[la].grp0), lgg = g0;
+            GroupLane<G> lgl = group_lane<G>(lal, lgi, P, lg, q, m);
+            uint32_t lb = 0;
+            uint32_t pa = la;
+            AllocView pal = lal;
+            GroupLane<G> pgl = lgl;
+            const uint64_t ngr = g1 - g0;
+            uint64_t done = 0;  // groups finalized
+            auto load_block = [&](uint4 (&w)[U]) {
+                if (lb == 0 && p.prefetch != 0u && lane == 0u && lgg + 1 < g1 &&
+                    lgi + 1 < (lal.n_pages + G - 1) / G) {  // the next group of this allocation
+                    const uint64_t nx = lal.base + ((lgi + 1) * G << lg);
+                    const uint64_t e = min(nx + (uint64_t)G * P, lal.base + __ldg(&p.allocs[la].bytes));
+                    if (e > nx) prefetch_l2(reinterpret_cast<const void *>(nx), (uint32_t)(e - nx));
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < U; u++) {
+                    const uint32_t off = (lb * U + u) * Wr;
+                    w[u] = lgl.valid && off + m * 16u >= lgl.pad ? ldg_stream(lgl.ptr + off) : make_uint4(0, 0, 0, 0);
+                }
+                if (++lb == NB) {  // next group
+                    lb = 0;
+                    lgg++;
+                    if (lgg < g1) {
+                        if (++lgi == (lal.n_pages + G - 1) / G) {
+                            la++;
+                            lal = load_alloc(p.allocs + la, P);
+                            lgi = 0;
+                        }
+                        lgl = group_lane<G>(lal, lgi, P, lg, q, m);
+                    }
+                }
+            };
+            uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u, pb = 0;
+            auto process_block = [&](const uint4 (&w)[U]) {
+#pragma unroll
+                for (uint32_t u = 0; u < U; u++) row_step(lane4, sb, x, acc, w[u]);
+                if (++pb < NB) return;
+                // group complete: one raw16 + tree for all G pages
+                const uint32_t *t4 = small + kT4 * 1024u;
+                uint32_t v = apply_tab(t4, x[0]);
+                v = apply_tab(t4, v ^ x[1]);
+                v = apply_tab(t4, v ^ x[2]);
+                v = apply_tab(t4, v ^ x[3]);
+#pragma unroll
+                for (uint32_t j = 0; (1u << j) < QL; j++) {
+                    const uint32_t o = __shfl_down_sync(kFull, v, 1u << j);
+                    if ((m & ((2u << j) - 1u)) == 0u) v = apply_tab(small + (kA16 + j) * 1024u, v) ^ o;
+                }
+                const uint32_t bal = __ballot_sync(kFull, acc != 0u);
+                const uint32_t nzq = QL == 32 ? bal : (bal >> (q * QL)) & ((1u << QL) - 1u);
+                if (m == 0u && pgl.valid) {
+                    const bool tail = pgl.pi == pal.n_pages - 1;
+                    finalize_page(p, pal.page0 + pgl.pi, tile_of_page(pal.tile0, pgl.pi, P, lg), pgl.pi == 0,
+                                  tail ? pal.tail_len : P, tail ? pal.z_tail : p.z_page, v, nzq != 0u);
+                }
+                x[0] = x[1] = x[2] = x[3] = 0u;
+                acc = 0u;
+                pb = 0;
+                if (++done < ngr) {
+                    const uint64_t pgi = (uint64_t)pgl.pi / G + 1;
+                    if (pgi == (pal.n_pages + G - 1) / G) {
+                        pa++;
+                        pal = load_alloc(p.allocs + pa, P);
+                        pgl = group_lane<G>(pal, 0, P, lg, q, m);
+                    } else {
+                        pgl = group_lane<G>(pal, pgi, P, lg, q, m);
+                    }
+                }
+            };
+            const uint64_t nblk = ngr * NB;
+            uint4 wa[U], wb[U];
+            load_block(wa);
+            for (uint64_t bk = 0; bk < nblk; bk += 2) {
+                if (bk + 1 < nblk) load_block(wb);
+                process_block(wa);
+                if (bk + 1 >= nblk) break;
+                if (bk + 2 < nblk) load_block(wa);
+                process_block(wb);
+            }
+        }
+        // every leader lane's page results visible before lane 0 publishes
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
             if (atomicAdd(p.chunk_arrive + ch, 1u) == (uint32_t)p.workers - 1u) {
                 atomicExch(p.chunk_arrive + ch, 0u);
                 __threadfence();
@@ -930,6 +1093,15 @@ uint32_t scan_prefetch_bytes() {
     return v;
 }
 
+// K1g for 4 KiB / 8 KiB pages unless GCR_SMALL_GROUPS=0
+bool scan_uses_groups(uint32_t page_size) {
+    static const bool on = [] {
+        const char *e = std::getenv("GCR_SMALL_GROUPS");
+        return !(e && e[0] == '0');
+    }();
+    return on && (page_size == kGroupBytes / 4 || page_size == kGroupBytes / 2);
+}
+
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     // once per device: setting a function attribute can serialise with work in
     // flight, which would leave the GPU idle between pipelined launches
@@ -937,14 +1109,23 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_done[dev]) {
-        if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(k_scan_grp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_scan_grp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) !=
+                cudaSuccess)
             return -1;
         attr_done[dev] = true;
     }
     if (p.n_chunks == 0) return 0;
     const uint64_t wpb = kScanThreads / 32;
     const uint64_t grid = (p.workers + wpb - 1) / wpb;
-    k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 4)
+        k_scan_grp<4><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    else if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 2)
+        k_scan_grp<2><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    else
+        k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
     return launched(1);
 }
 

@@ -169,9 +169,11 @@ def test_more_staging_slots_than_streams(G, orc, streams, slots):
                          direct_min=ALWAYS_STAGED, slots=slots)
 
 
-def test_chunking_small_pages_many_chunks(G, orc):
-    _ckpt_restore_parity(G, orc, [1 << 20, (1 << 20) + 4096 + 512, 12288], 4096, chunk=65536, streams=3,
-                         zero_pages=[(0, 3), (0, 4), (1, 0), (2, 2)], seed=5)
+@pytest.mark.parametrize("P", [4096, 8192])
+def test_chunking_small_pages_many_chunks(G, orc, P):
+    """Small pages (K1g page groups) over many chunks, partial last groups, tails."""
+    _ckpt_restore_parity(G, orc, [1 << 20, (1 << 20) + 4096 + 512, 12288, 5 * P + 16], P, chunk=65536, streams=3,
+                         zero_pages=[(0, 3), (0, 4), (1, 0), (2, 1), (3, 5)], seed=5)
 
 
 def test_large_page_chunking(G, orc):
@@ -197,7 +199,7 @@ def _mutate(ts, rng, k, P):
 
 
 @pytest.mark.parametrize("direct_min", [0, ALWAYS_STAGED])
-@pytest.mark.parametrize("P", [4096, 65536, 262144])
+@pytest.mark.parametrize("P", [4096, 8192, 65536, 262144])
 def test_incremental_chain_parity(G, orc, P, direct_min):
     """Full, then two incrementals with exact dirty counts; every stream equals
     the oracle's; restore(I0, I1, I2) into poison == state at I2."""
