@@ -4,6 +4,7 @@
 //  K0  build_page_table  A1: page -> allocation, tile -> allocation maps
 //  K1  scan              A2+A3+A4 (+A9 in verify mode): per-page CRC32C,
 //                        all-zero test, dirty diff, class, tile counters
+//  K1g scan_grp<G>       the same for 4 / 8 KiB pages: G pages per 16 KiB group
 //  K2  tile_scan         A5: chunk-local exclusive scan of PRESENT bytes per
 //                        tile (the pack's destination offsets) and chunk totals
 //  K3  pagemap_*         A5: maximal runs -> CRIU-style pagemap entries
