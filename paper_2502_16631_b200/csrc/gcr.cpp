@@ -287,7 +287,7 @@ struct gcr_ctx {
     uint32_t *chunk_sync_d = nullptr;  // per chunk: K1 arrival counter [0, nch), chunk_done [nch, 2 nch),
                                        // K4 width decision [2 nch, 3 nch)
     uint32_t epoch = 0;                // K1 launch id published in chunk_done
-    uint32_t *fold_slots = nullptr;  // K1's cut-page fold: 2 words per K1 warp, zero between launches
+    unsigned long long *fold_slots = nullptr;  // K1's cut-page fold: one u64 per K1 warp and chunk, zero between launches
     FoldSlots fold{};
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
@@ -503,9 +503,9 @@ gcr_status build_layout(gcr_ctx *c) {
         // fold slots: one pair per K1 warp per chunk (warps run ahead into later
         // chunks independently, so chunks never share slots)
         const uint64_t w = scan_workers(c->n_sms, false) * ns;  // the verify K8 uses every SM
-        CUDA_TRY(c, cudaMalloc(&c->fold_slots, 2 * 4 * w));
-        CUDA_TRY(c, cudaMemset(c->fold_slots, 0, 2 * 4 * w));
-        c->fold = FoldSlots{c->fold_slots, c->fold_slots + w};
+        CUDA_TRY(c, cudaMalloc(&c->fold_slots, 8 * w));
+        CUDA_TRY(c, cudaMemset(c->fold_slots, 0, 8 * w));
+        c->fold = FoldSlots{c->fold_slots};
     }
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_cnt, 4 * nblk));
     CUDA_TRY(c, cudaMalloc(&c->pm_blk_off, 4 * nblk));
@@ -870,6 +870,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // memory costs tens of us).
     sp.chunk_rows = c->chunk_rows_d;
     sp.chunk_groups = c->chunk_groups_d;  // K1g for 4/8 KiB pages (null: K1)
+    sp.grp_pf_block = grp_prefetch_block();
     sp.n_chunks = (uint32_t)nch;
     sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;  // never 0 (the flags' initial value)
     sp.chunk_arrive = c->chunk_sync_d;
@@ -1223,7 +1224,7 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
         {
             const uint64_t ns = std::max<size_t>(c->chunks.size(), 1);
             cudaMemset(c->chunk_sync_d, 0, 3 * 4 * ns);
-            cudaMemset(c->fold_slots, 0, 2 * 4 * scan_workers(c->n_sms, false) * ns);
+            cudaMemset(c->fold_slots, 0, 8 * scan_workers(c->n_sms, false) * ns);
         }
         cudaGetLastError();
         image_free_buffers(img);
@@ -1453,6 +1454,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         const size_t nch = c->chunks.size();
         sp.chunk_rows = c->chunk_rows_d + nch + 1;  // one chunk: every real row
         sp.chunk_groups = c->chunk_groups_d ? c->chunk_groups_d + nch + 1 : nullptr;
+        sp.grp_pf_block = grp_prefetch_block();
         sp.n_chunks = 1;
         sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;
         sp.chunk_arrive = c->chunk_sync_d;
@@ -1467,9 +1469,41 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.verify_count = c->misc_d + 1;
         sp.first_bad = c->misc_d + 2;
         sp.tables = c->tables_d;
+        // GCR_SCAN_TIMES=1: per-warp {entry, first chunk done, exit} globaltimer
+        // stamps of this verify launch, summarised on stderr (diagnostics)
+        static const bool stamps = std::getenv("GCR_SCAN_TIMES") != nullptr;
+        unsigned long long *wt = nullptr;
+        if (stamps && cudaMalloc(&wt, 24 * sp.workers) == cudaSuccess) {
+            cudaMemsetAsync(wt, 0, 24 * sp.workers, c->compute);
+            sp.warp_times = wt;
+        }
         CUDA_TRY(c, cudaEventRecord(v0, c->compute));
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
         CUDA_TRY(c, cudaEventRecord(v1, c->compute));
+        if (wt) {
+            std::vector<unsigned long long> h(3 * sp.workers);
+            cudaMemcpy(h.data(), wt, 24 * sp.workers, cudaMemcpyDeviceToHost);
+            cudaFree(wt);
+            std::vector<double> st0, en;
+            unsigned long long t0 = ~0ull;
+            for (uint64_t w = 0; w < sp.workers; w++) t0 = std::min(t0, h[3 * w]);
+            for (uint64_t w = 0; w < sp.workers; w++) {
+                st0.push_back((h[3 * w] - t0) * 1e-3);
+                en.push_back((h[3 * w + 2] - t0) * 1e-3);
+            }
+            std::vector<double> a = st0, b = en;
+            std::sort(a.begin(), a.end());
+            std::sort(b.begin(), b.end());
+            auto pct = [](const std::vector<double> &v, double q) { return v[(size_t)(q * (v.size() - 1))]; };
+            float kms = 0;
+            cudaEventSynchronize(v1);
+            cudaEventElapsedTime(&kms, v0, v1);
+            std::fprintf(stderr,
+                         "{\"gcr_scan_times\": \"verify\", \"warps\": %llu, \"event_us\": %.1f, \"start_us\": [%.2f, %.2f, "
+                         "%.2f, %.2f], \"end_us\": [%.1f, %.1f, %.1f, %.1f, %.1f]}\n",
+                         (unsigned long long)sp.workers, kms * 1e3, pct(a, 0), pct(a, 0.5), pct(a, 0.99), pct(a, 1),
+                         pct(b, 0), pct(b, 0.1), pct(b, 0.5), pct(b, 0.9), pct(b, 1));
+        }
         CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));
         verify_launches = 1;
     }

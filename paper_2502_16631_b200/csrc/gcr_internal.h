@@ -42,14 +42,15 @@ struct AllocDev {
 constexpr uint32_t kGroupBytes = 16384;
 
 // A page cut by K1 warp-range boundaries is folded inside K1: every warp
-// holding a piece of it XORs the piece's contribution into the page's owner
-// slot (owner = the warp whose range holds the page's first real row), then
-// adds its row count (low 16 bits) and non-zero flag (<< 16) to the owner's
-// counter; the warp whose add completes the page's rows finalizes it and
-// re-zeroes both slots.  One slot pair per K1 warp.
+// holding a piece of it folds the piece's contribution into the page's owner
+// slot (owner = the warp whose range holds the page's first real row) with ONE
+// 64-bit compare-and-swap that XORs the contribution into the low word and
+// adds its row count (bits 32-47) and non-zero flag (bits 48-63) to the high
+// word; the CAS that completes the page's rows holds the full XOR in its own
+// result and finalizes the page (no fences, no second read), then re-zeroes the
+// slot for the next launch.  One slot per K1 warp and chunk.
 struct FoldSlots {
-    uint32_t *x;  // XOR of the contributions adv_{512 (Rp - vr_end)}(raw)
-    uint32_t *c;  // rows | n_nonzero_pieces << 16
+    unsigned long long *s;
 };
 
 // Per-tile result of the scan used by compaction (K2) and pack (K4).
@@ -123,6 +124,8 @@ struct ScanParams {
     const CrcTables *tables;
     uint32_t prefetch;         // bytes: each warp keeps [cursor + prefetch, + block) requested into L2
     const uint64_t *chunk_groups;  // K1g: n_chunks + 1 global page-group boundaries (device)
+    unsigned long long *warp_times;  // optional (GCR_SCAN_TIMES): per warp {start, end} globaltimer ns
+    uint32_t grp_pf_block;     // K1g: block of a group (0..7) at which the next group is prefetched
 };
 
 struct ScatterDesc {
@@ -144,6 +147,7 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
                             cudaStream_t st);
 uint64_t scan_workers(int n_sms, bool leave_free = true);          // K1 warps (a full persistent grid)
 uint32_t scan_prefetch_bytes();                                     // K1 L2 prefetch distance (GCR_SCAN_PREFETCH)
+uint32_t grp_prefetch_block();                                      // K1g prefetch trigger block (GCR_GRP_PF_BLOCK)
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1 (K1g when p.chunk_groups is set)
 bool scan_uses_groups(uint32_t page_size);                          // K1g for this page size?
 // K2 of one chunk: first waits (bounded) until chunk_done[chunk] == epoch.

@@ -197,14 +197,14 @@ __device__ __forceinline__ uint32_t warp_mulmod(uint32_t m, uint32_t v, uint32_t
 // The chunk a warp is scanning: its real rows and its fold slots.
 struct ChunkCtx {
     uint64_t rb, rows;  // first global real row, real rows
-    uint32_t *fx, *fc;  // fold slots of this chunk (one pair per warp)
+    unsigned long long *fs;  // fold slots of this chunk (one per warp)
 };
 
 // A piece of a cut page arrives at the page's owner slot (executed by one
-// lane).  The piece's contribution is already advanced to the page end.  The
-// arrival that completes the page's Rp - r0 real rows finalizes it.  Release:
-// the XOR is fenced before the counter add; acquire: fence after observing
-// the full count, then read-and-clear the XOR.
+// lane).  The piece's contribution is already advanced to the page end.  One
+// 64-bit CAS folds {XOR contribution, + rows, + non-zero} (FoldSlots); the
+// arrival that completes the page's Rp - r0 real rows finalizes it from its
+// own CAS result.
 __device__ __forceinline__ void fold_arrive(const ScanParams &p, const ChunkCtx &cc, uint64_t g, uint32_t a,
                                             uint32_t pi, uint32_t r0, uint32_t rows, uint32_t contrib, bool nz) {
     const uint32_t P = p.page_size, lg = p.log2_page, Rp = P >> kLog2Row;
@@ -213,18 +213,21 @@ __device__ __forceinline__ void fold_arrive(const ScanParams &p, const ChunkCtx 
     // real row; ranges are [rows*w/W, rows*(w+1)/W) relative to the chunk
     const uint64_t x = __ldg(&al->row0) + (uint64_t)pi * Rp - cc.rb;
     const uint64_t owner = ((x + 1) * p.workers - 1) / cc.rows;
-    atomicXor(cc.fx + owner, contrib);
-    __threadfence();
-    const uint32_t add = rows | (nz ? 1u << 16 : 0u);
-    const uint32_t tot = atomicAdd(cc.fc + owner, add) + add;
-    if ((tot & 0xFFFFu) != Rp - r0) return;
-    __threadfence();
-    const uint32_t raw = atomicExch(cc.fx + owner, 0u);
-    atomicExch(cc.fc + owner, 0u);
+    unsigned long long *slot = cc.fs + owner;
+    const unsigned long long add = ((unsigned long long)rows << 32) | (nz ? 1ull << 48 : 0ull);
+    unsigned long long old = 0ull, nv;
+    for (;;) {  // first guess: the slot is empty
+        nv = (old ^ contrib) + add;  // contrib < 2^32: the XOR only touches the low word
+        const unsigned long long seen = atomicCAS(slot, old, nv);
+        if (seen == old) break;
+        old = seen;
+    }
+    if (((nv >> 32) & 0xFFFFull) != Rp - r0) return;
+    *slot = 0ull;  // every piece arrived: the slot is free for the next launch
     const uint32_t n_pages = __ldg(&al->n_pages);
     const bool tail = pi == n_pages - 1;
     finalize_page(p, g, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, tail ? __ldg(&al->tail_len) : P,
-                  tail ? __ldg(&al->z_tail) : p.z_page, raw, (tot >> 16) != 0u);
+                  tail ? __ldg(&al->z_tail) : p.z_page, (uint32_t)nv, (nv >> 48) != 0ull);
 }
 
 // Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
@@ -550,6 +553,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
     const uint32_t *small = sm + kBraidSmem / 4;
 
+    const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     stage_tables(sm, p.tables, &p.tables->braid[0][0]);
     __syncthreads();
 
@@ -557,14 +561,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     const uint32_t lane4 = lane * 4u;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (wid >= p.workers) return;
+    if (p.warp_times && lane == 0) p.warp_times[3 * wid] = t_entry;
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t Rp = P >> kLog2Row;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
         ChunkCtx cc;
         cc.rb = p.chunk_rows[ch];
         cc.rows = p.chunk_rows[ch + 1] - cc.rb;
-        cc.fx = p.fold.x + (uint64_t)ch * p.workers;
-        cc.fc = p.fold.c + (uint64_t)ch * p.workers;
+        cc.fs = p.fold.s + (uint64_t)ch * p.workers;
         const uint64_t r = cc.rb + cc.rows * wid / p.workers;
         const uint64_t rend = cc.rb + cc.rows * (wid + 1) / p.workers;
         if (r < rend) {
@@ -635,7 +639,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             }
         }
         __syncwarp();
+        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[3 * wid + 1] = globaltimer_ns();
     }
+    if (p.warp_times && lane == 0) p.warp_times[3 * wid + 2] = globaltimer_ns();
 }
 
 // ---------------------------------------------------------------------------
@@ -690,12 +696,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t *small = sm + kBraidSmem / 4;
+    const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     stage_tables(sm, p.tables, G == 4 ? &p.tables->a128[0][0] : &p.tables->a256[0][0]);
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (wid >= p.workers) return;
+    if (p.warp_times && lane == 0) p.warp_times[3 * wid] = t_entry;
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
         const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
@@ -713,7 +721,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             const uint64_t ngr = g1 - g0;
             uint64_t done = 0;  // groups finalized
             auto load_block = [&](uint4 (&w)[U]) {
-                if (lb == 0 && p.prefetch != 0u && lane == 0u && lgg + 1 < g1 &&
+                if (lb == p.grp_pf_block && p.prefetch != 0u && lane == 0u && lgg + 1 < g1 &&
                     lgi + 1 < (lal.n_pages + G - 1) / G) {  // the next group of this allocation
                     const uint64_t nx = lal.base + ((lgi + 1) * G << lg);
                     const uint64_t e = min(nx + (uint64_t)G * P, lal.base + __ldg(&p.allocs[la].bytes));
@@ -796,7 +804,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             }
         }
         __syncwarp();
+        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[3 * wid + 1] = globaltimer_ns();
     }
+    if (p.warp_times && lane == 0) p.warp_times[3 * wid + 2] = globaltimer_ns();
 }
 
 // K0: page -> allocation and tile -> allocation (A1).  One CTA per allocation.
@@ -1086,6 +1096,19 @@ uint64_t scan_workers(int n_sms, bool leave_free) { return (uint64_t)scan_sms(n_
 // register loads (cp.async.bulk.prefetch.L2: no registers, no shared memory),
 // so the ~50 KiB of register double buffers per SM only have to cover L2
 // latency, not HBM latency.  GCR_SCAN_PREFETCH overrides (0 = off).
+// K1g requests the next group (16 KiB) into L2 when it loads block
+// GCR_GRP_PF_BLOCK (default 4, i.e. ~8 KiB ahead) of the current one.  At
+// block 0 (16 KiB ahead) 4-9 % of the prefetched lines were evicted before use
+// and re-read from DRAM (ncu: 1.56-1.62 GB read for 1.49 GB); at block 4 the
+// reads are 1.0010x the algorithmic bytes (profiles/r1n_grp_prefetch.jsonl).
+uint32_t grp_prefetch_block() {
+    static const uint32_t v = [] {
+        const char *e = std::getenv("GCR_GRP_PF_BLOCK");
+        return e ? (uint32_t)std::strtoul(e, nullptr, 0) % 8u : 4u;
+    }();
+    return v;
+}
+
 uint32_t scan_prefetch_bytes() {
     static const uint32_t v = [] {
         const char *e = std::getenv("GCR_SCAN_PREFETCH");
