@@ -502,7 +502,7 @@ gcr_status build_layout(gcr_ctx *c) {
         CUDA_TRY(c, cudaMemset(c->chunk_sync_d, 0, 3 * 4 * ns));
         // fold slots: one pair per K1 warp per chunk (warps run ahead into later
         // chunks independently, so chunks never share slots)
-        const uint64_t w = scan_workers(c->n_sms, false) * ns;  // the verify K8 uses every SM
+        const uint64_t w = scan_workers(c->n_sms, 0) * ns;  // the verify K8 uses every SM
         CUDA_TRY(c, cudaMalloc(&c->fold_slots, 8 * w));
         CUDA_TRY(c, cudaMemset(c->fold_slots, 0, 8 * w));
         c->fold = FoldSlots{c->fold_slots};
@@ -875,7 +875,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;  // never 0 (the flags' initial value)
     sp.chunk_arrive = c->chunk_sync_d;
     sp.chunk_done = c->chunk_sync_d + std::max<size_t>(nch, 1);
-    sp.workers = scan_workers(c->n_sms);
+    const int scan_free = scan_free_sms(mode == GCR_INCREMENTAL);
+    sp.workers = scan_workers(c->n_sms, scan_free);
     std::vector<cudaEvent_t> k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
     cudaEvent_t t0 = c->ev(), k1s = c->ev(), k1m = c->ev();
@@ -1055,7 +1056,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
             // narrowed to the SMs K1 leaves free while the scan's last chunk is unpublished
             LAUNCH_TRY(c, launch_pack(c->allocs_d, c->tile_alloc, c->cls, ch.tile_begin, P, c->lg, c->slots[i % NS],
-                                      c->stage_map + ch.tile_begin, n_items, c->n_sms, sp.chunk_done + (nch - 1),
+                                      c->stage_map + ch.tile_begin, n_items, c->n_sms, scan_free,
+                                      sp.chunk_done + (nch - 1),
                                       sp.epoch, c->chunk_sync_d + 2 * std::max<size_t>(nch, 1) + i, c->packs));
         } else {
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
@@ -1224,7 +1226,7 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
         {
             const uint64_t ns = std::max<size_t>(c->chunks.size(), 1);
             cudaMemset(c->chunk_sync_d, 0, 3 * 4 * ns);
-            cudaMemset(c->fold_slots, 0, 8 * scan_workers(c->n_sms, false) * ns);
+            cudaMemset(c->fold_slots, 0, 8 * scan_workers(c->n_sms, 0) * ns);
         }
         cudaGetLastError();
         image_free_buffers(img);
@@ -1459,7 +1461,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
         sp.epoch = ++c->epoch ? c->epoch : ++c->epoch;
         sp.chunk_arrive = c->chunk_sync_d;
         sp.chunk_done = c->chunk_sync_d + std::max<size_t>(nch, 1);
-        sp.workers = scan_workers(c->n_sms, false);  // nothing runs beside the verify: every SM
+        sp.workers = scan_workers(c->n_sms, 0);  // nothing runs beside the verify: every SM
         sp.prefetch = scan_prefetch_bytes();
         sp.page_size = P;
         sp.log2_page = c->lg;

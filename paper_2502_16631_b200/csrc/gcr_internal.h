@@ -145,7 +145,8 @@ struct ZeroDesc {
 int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t *page_alloc,
                             uint32_t *tile_alloc, uint32_t tiles_per_page, uint32_t pages_per_tile,
                             cudaStream_t st);
-uint64_t scan_workers(int n_sms, bool leave_free = true);          // K1 warps (a full persistent grid)
+int scan_free_sms(bool incremental);                                // SMs K1 leaves to K2 / K4
+uint64_t scan_workers(int n_sms, int free_sms);                      // K1 warps (a full persistent grid)
 uint32_t scan_prefetch_bytes();                                     // K1 L2 prefetch distance (GCR_SCAN_PREFETCH)
 uint32_t grp_prefetch_block();                                      // K1g prefetch trigger block (GCR_GRP_PF_BLOCK)
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1 (K1g when p.chunk_groups is set)
@@ -156,7 +157,8 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end
                      ChunkTotals *totals_host, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tile_begin,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, const StageItem *items, uint32_t n_items,
-                int n_sms, const uint32_t *scan_done, uint32_t epoch, uint32_t *decision, cudaStream_t st);
+                int n_sms, int scan_free, const uint32_t *scan_done, uint32_t epoch, uint32_t *decision,
+                cudaStream_t st);
 // Pagemap over all pages: phase 1 counts run starts per block and scans them,
 // writing the entry count to *n_entries_dev; phase 2 writes the entries.
 int launch_pagemap_count(const uint8_t *cls, uint64_t n_pages, uint32_t *blk_cnt, uint32_t *blk_off,

@@ -1086,11 +1086,16 @@ int launch_build_page_table(const AllocDev *allocs, uint32_t n_allocs, uint32_t 
 }
 
 
-static int scan_sms(int n_sms, bool leave_free) {
-    return leave_free && n_sms > 4 * free_sms() ? n_sms - free_sms() : n_sms;
-}
+// SMs K1 leaves free: an incremental checkpoint (scan about as long as the
+// drain) keeps K2 + 8 pack CTAs running beside it; a full checkpoint (drain
+// ~100x the scan) keeps only K2's SM, so the scan runs ~7 % faster and the
+// packs simply queue behind it (they start when it ends, wide); the verify
+// takes every SM.
+int scan_free_sms(bool incremental) { return incremental ? free_sms() : 1; }
 
-uint64_t scan_workers(int n_sms, bool leave_free) { return (uint64_t)scan_sms(n_sms, leave_free) * (kScanThreads / 32); }
+uint64_t scan_workers(int n_sms, int free) {
+    return (uint64_t)(free > 0 && n_sms > 4 * free ? n_sms - free : n_sms) * (kScanThreads / 32);
+}
 
 // K1 keeps each warp's stream requested into L2 this many bytes ahead of its
 // register loads (cp.async.bulk.prefetch.L2: no registers, no shared memory),
@@ -1171,16 +1176,17 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, const uint32
 }
 
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tb, uint32_t P,
-                uint32_t lg, uint8_t *slot, const StageItem *items, uint32_t n_items, int n_sms,
+                uint32_t lg, uint8_t *slot, const StageItem *items, uint32_t n_items, int n_sms, int scan_free,
                 const uint32_t *scan_done, uint32_t epoch, uint32_t *decision, cudaStream_t st) {
     if (n_items == 0) return 0;
     // up to 2 CTAs of 1024 per SM; narrowed on the device while the scan runs
     uint64_t grid = ((uint64_t)n_items * kSlicesPerTile + kPackThreads / 32 - 1) / (kPackThreads / 32);
     const uint64_t cap = (uint64_t)n_sms * 2;
     if (grid > cap) grid = cap;
-    if (n_sms <= 4 * free_sms()) scan_done = nullptr;  // small GPUs: K1 leaves no SMs free anyway
+    // narrow while the scan runs only if it left room for K2 + >= 1 pack CTA
+    if (scan_free < 3 || n_sms <= 4 * scan_free) scan_done = nullptr;
     k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items,
-                                                    scan_done, epoch, decision, (uint32_t)(free_sms() - 2));
+                                                    scan_done, epoch, decision, (uint32_t)(scan_free - 2));
     return launched(1);
 }
 
