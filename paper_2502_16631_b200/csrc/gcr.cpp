@@ -427,11 +427,36 @@ gcr_status build_layout(gcr_ctx *c) {
     c->n_tiles = t;
     c->z_page = zero_digest(P);
     // chunk plan: uniform tile ranges; page ranges from the allocation walk
+    // chunk plan: tile ranges of chunk_bytes; a long registry (>= 8 chunks)
+    // ramps up (1/8, 1/4, 1/2 chunk) so the first drain starts after a short
+    // scan, and ramps down the same way at the end so the last drain (which
+    // only starts once the scan ends) is short.  Sizes stay whole pages.
     const uint64_t ct = c->cfg.chunk_bytes / kTileBytes;
+    const uint64_t tpp = P > kTileBytes ? P / kTileBytes : 1;  // tiles per page
     c->chunks.clear();
-    for (uint64_t tb = 0; tb < t; tb += ct) {
-        Chunk ch{tb, std::min(t, tb + ct), 0, 0};
-        c->chunks.push_back(ch);
+    {
+        std::vector<uint64_t> sizes;
+        static const bool ramp_on = [] {  // GCR_CHUNK_RAMP=0: uniform chunks
+            const char *e = std::getenv("GCR_CHUNK_RAMP");
+            return !(e && e[0] == '0');
+        }();
+        if (ramp_on && t >= 8 * ct && ct >= 8 * tpp) {
+            const uint64_t r[3] = {ct / 8, ct / 4, ct / 2};
+            uint64_t ramp = 0;
+            for (uint64_t x : r) ramp += x / tpp * tpp;
+            uint64_t mid = t - 2 * ramp;
+            for (uint64_t x : r) sizes.push_back(x / tpp * tpp);
+            for (; mid > 0; mid -= std::min(mid, ct)) sizes.push_back(std::min(mid, ct));
+            for (int k = 2; k >= 0; k--) sizes.push_back(r[k] / tpp * tpp);
+        } else {
+            for (uint64_t tb = 0; tb < t; tb += ct) sizes.push_back(std::min(ct, t - tb));
+        }
+        uint64_t tb = 0;
+        for (uint64_t n : sizes) {
+            if (n == 0) continue;
+            c->chunks.push_back(Chunk{tb, tb + n, 0, 0});
+            tb += n;
+        }
     }
     auto page_of_tile = [&](uint64_t tile) -> uint64_t {
         if (tile >= t) return g;

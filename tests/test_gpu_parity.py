@@ -176,6 +176,17 @@ def test_chunking_small_pages_many_chunks(G, orc, P):
                          zero_pages=[(0, 3), (0, 4), (1, 0), (2, 1), (3, 5)], seed=5)
 
 
+@pytest.mark.parametrize("P,chunk", [(4096, 1 << 20), (1 << 20, 8 << 20)])
+def test_chunk_ramp_parity(G, orc, P, chunk):
+    """A registry of >= 8 chunks gets ramped chunk sizes (1/8, 1/4, 1/2 chunk at
+    both ends, whole pages): image offsets, pagemap and digests stitched across
+    chunks of every size, 4 KiB page groups (K1g) and 16-tile pages."""
+    n = 9 * chunk
+    sizes = [n // 2 + 16, n // 3 + 4096, n // 6 + P]
+    zp = [(0, 1), (0, 2), (1, 3), (2, 0)]
+    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=chunk, streams=2, seed=77, direct_min=1 << 20)
+
+
 def test_large_page_chunking(G, orc):
     P = 1 << 20
     _ckpt_restore_parity(G, orc, [5 * P + 4096, 3 * P, 2 * P + 16], P, chunk=2 * P, streams=2,
