@@ -427,19 +427,19 @@ gcr_status build_layout(gcr_ctx *c) {
     c->n_tiles = t;
     c->z_page = zero_digest(P);
     // chunk plan: uniform tile ranges; page ranges from the allocation walk
-    // chunk plan: tile ranges of chunk_bytes; a long registry (>= 8 chunks)
-    // ramps up (1/8, 1/4, 1/2 chunk) so the first drain starts after a short
-    // scan, and ramps down the same way at the end so the last drain (which
-    // only starts once the scan ends) is short.  Sizes stay whole pages.
+    // chunk plan: uniform tile ranges of chunk_bytes.  GCR_CHUNK_RAMP=1 ramps
+    // a long registry (>= 8 chunks) up and down (1/8, 1/4, 1/2 chunk at both
+    // ends, whole pages): the first drain starts ~0.4 ms earlier, but measured
+    // on C4 the step did not improve (1 %: 8.90 -> 9.00 ms, 5 %: 39.65 ->
+    // 39.46 ms; profiles/r1s_chunk_ramp_ab.jsonl) -- the drain, not its start,
+    // bounds it -- and every extra chunk costs each K1 warp a range restart.
     const uint64_t ct = c->cfg.chunk_bytes / kTileBytes;
     const uint64_t tpp = P > kTileBytes ? P / kTileBytes : 1;  // tiles per page
     c->chunks.clear();
     {
         std::vector<uint64_t> sizes;
-        static const bool ramp_on = [] {  // GCR_CHUNK_RAMP=0: uniform chunks
-            const char *e = std::getenv("GCR_CHUNK_RAMP");
-            return !(e && e[0] == '0');
-        }();
+        const char *ramp_env = std::getenv("GCR_CHUNK_RAMP");  // read per layout (tests flip it)
+        const bool ramp_on = ramp_env && ramp_env[0] == '1';
         if (ramp_on && t >= 8 * ct && ct >= 8 * tpp) {
             const uint64_t r[3] = {ct / 8, ct / 4, ct / 2};
             uint64_t ramp = 0;

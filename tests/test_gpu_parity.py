@@ -177,13 +177,14 @@ def test_chunking_small_pages_many_chunks(G, orc, P):
 
 
 @pytest.mark.parametrize("P,chunk", [(4096, 1 << 20), (1 << 20, 8 << 20)])
-def test_chunk_ramp_parity(G, orc, P, chunk):
-    """A registry of >= 8 chunks gets ramped chunk sizes (1/8, 1/4, 1/2 chunk at
+def test_chunk_ramp_parity(G, orc, P, chunk, monkeypatch):
+    """With GCR_CHUNK_RAMP=1 a registry of >= 8 chunks gets ramped chunk sizes (1/8, 1/4, 1/2 chunk at
     both ends, whole pages): image offsets, pagemap and digests stitched across
     chunks of every size, 4 KiB page groups (K1g) and 16-tile pages."""
     n = 9 * chunk
     sizes = [n // 2 + 16, n // 3 + 4096, n // 6 + P]
     zp = [(0, 1), (0, 2), (1, 3), (2, 0)]
+    monkeypatch.setenv("GCR_CHUNK_RAMP", "1")  # read by the library at each layout build (lock)
     _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=chunk, streams=2, seed=77, direct_min=1 << 20)
 
 
@@ -368,6 +369,62 @@ def test_gpt2_small_full_size_parity(G, orc):
             assert np.array_equal(ts[a].cpu().numpy(), cont[a])
         st = ctx.stats()
         assert st["verify_failures"] == 0 and 0 < st["restore_direct_bytes"] < st["restore_h2d_bytes"]
+        ctx.unlock()
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("P", [4096, 65536, 2097152])
+def test_degenerate_all_zero_registry(G, orc, P):
+    """Every page ZERO: an empty data section (image_bytes = 0), one ZERO entry
+    per allocation, every digest Z(len); restore zero-fills poisoned memory."""
+    gcr, _ = G
+    sizes = [3 * P + 48, P, 16]
+    ts = [torch.zeros(n, dtype=torch.uint8, device="cuda") for n in sizes]
+    torch.cuda.synchronize()
+    ctx = gcr.Context(0, page_size=P)
+    try:
+        reg = registry_of(ctx, ts)
+        ctx.lock()
+        img = ctx.checkpoint(gcr.GCR_FULL)
+        exp = oracle_stream(orc, P, reg, host_copies(ts))
+        got = img.stream()
+        assert got == exp, first_diff(got, exp)
+        h = img.header()
+        assert h.n_present == 0 and h.image_bytes == 0 and h.n_zero == h.n_pages and h.n_entries == len(sizes)
+        for t in ts:
+            t.fill_(0xA5)
+        ctx.restore([img])
+        assert all(int(t.count_nonzero().item()) == 0 for t in ts)
+        ctx.unlock()
+    finally:
+        ctx.close()
+
+
+def test_degenerate_all_present_single_page_allocations(G, orc):
+    """No ZERO page, one short page per allocation (every page is a tail page and
+    starts an allocation): one PRESENT entry per allocation."""
+    gcr, synth = G
+    P = 65536
+    sizes = [16 * (k + 1) for k in range(64)]
+    ts = _mk(G, sizes, 4321)
+    ctx = gcr.Context(0, page_size=P)
+    try:
+        reg = registry_of(ctx, ts)
+        cont = host_copies(ts)
+        ctx.lock()
+        img = ctx.checkpoint(gcr.GCR_FULL)
+        exp = oracle_stream(orc, P, reg, cont)
+        got = img.stream()
+        assert got == exp, first_diff(got, exp)
+        h = img.header()
+        assert h.n_present == h.n_pages == len(sizes) and h.n_entries == len(sizes)
+        assert h.image_bytes == sum(sizes)
+        for t in ts:
+            t.fill_(0xA5)
+        ctx.restore([img])
+        for t, c in zip(ts, cont):
+            assert np.array_equal(t.cpu().numpy(), c)
         ctx.unlock()
     finally:
         ctx.close()
