@@ -1124,11 +1124,8 @@ uint32_t scan_prefetch_bytes() {
 
 // K1g for 4 KiB / 8 KiB pages unless GCR_SMALL_GROUPS=0
 bool scan_uses_groups(uint32_t page_size) {
-    static const bool on = [] {
-        const char *e = std::getenv("GCR_SMALL_GROUPS");
-        return !(e && e[0] == '0');
-    }();
-    return on && (page_size == kGroupBytes / 4 || page_size == kGroupBytes / 2);
+    const char *e = std::getenv("GCR_SMALL_GROUPS");  // read per layout build (tests flip it)
+    return !(e && e[0] == '0') && (page_size == kGroupBytes / 4 || page_size == kGroupBytes / 2);
 }
 
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {

@@ -169,9 +169,12 @@ def test_more_staging_slots_than_streams(G, orc, streams, slots):
                          direct_min=ALWAYS_STAGED, slots=slots)
 
 
+@pytest.mark.parametrize("groups", ["1", "0"])
 @pytest.mark.parametrize("P", [4096, 8192])
-def test_chunking_small_pages_many_chunks(G, orc, P):
-    """Small pages (K1g page groups) over many chunks, partial last groups, tails."""
+def test_chunking_small_pages_many_chunks(G, orc, P, groups, monkeypatch):
+    """Small pages over many chunks, partial last groups, tails: K1g page groups
+    (default) and the plain K1 (GCR_SMALL_GROUPS=0) give the same stream."""
+    monkeypatch.setenv("GCR_SMALL_GROUPS", groups)  # read at each layout build (lock)
     _ckpt_restore_parity(G, orc, [1 << 20, (1 << 20) + 4096 + 512, 12288, 5 * P + 16], P, chunk=65536, streams=3,
                          zero_pages=[(0, 3), (0, 4), (1, 0), (2, 1), (3, 5)], seed=5)
 
