@@ -199,8 +199,9 @@ gcr_status gcr_unregister(gcr_ctx *ctx, uint32_t alloc_id);
 
 /* Add a CUDA stream (cudaStream_t, may be 0 = legacy default stream) that
  * lock must see idle (RUNNING only).  With no watched stream, lock waits for
- * the whole device (cudaDeviceSynchronize semantics, bounded by the timeout
- * through polling of the legacy stream).  Not owned by the library. */
+ * the whole device: every stream of the process, blocking or non-blocking
+ * (cudaDeviceSynchronize on a helper thread, bounded by lock_timeout_ms).
+ * Not owned by the library. */
 gcr_status gcr_watch_stream(gcr_ctx *ctx, void *cuda_stream);
 
 /* Pre-pin `bytes` of host memory for images (RUNNING only), so checkpoints do
@@ -227,6 +228,15 @@ gcr_status gcr_lock(gcr_ctx *ctx);
  * valid: chains).  On any failure the phase stays LOCKED, no image is
  * returned and the parent digest state is unchanged. */
 gcr_status gcr_checkpoint(gcr_ctx *ctx, gcr_mode mode, gcr_image **out);
+
+/* CHECKPOINTED -> LOCKED: undo the ctx's LAST checkpoint, whose image `img`
+ * is freed, and restore the parent digest state it replaced (the next
+ * incremental diffs against the previous parent again, generations are
+ * re-issued).  Used by the multi-rank helpers when another rank's checkpoint
+ * failed, so every rank is back where it was before the attempt (all or
+ * nothing).  GCR_E_STATE if not CHECKPOINTED (e.g. after release or
+ * unlock), GCR_E_INVAL if img is not the last checkpoint's image. */
+gcr_status gcr_checkpoint_abort(gcr_ctx *ctx, gcr_image *img);
 
 /* ---- releasable device memory ----------------------------
  * The paper's checkpoint action leaves the process "releasing all GPU
@@ -272,11 +282,15 @@ gcr_status gcr_release(gcr_ctx *ctx);
  * (VERSION), layout vs registry (LAYOUT), chain order (CHAIN).  After a
  * successful restore the ctx's parent digest state is chain[n-1]'s.  From
  * RELEASED, after validation, every released block is backed again at its
- * original address (GCR_E_NOMEM leaves the phase RELEASED) before the
- * chain is applied -- the chain starts with a full image, which writes every
- * page.
- * GCR_E_VERIFY: counts in gcr_get_stats (verify_failures, first_bad_page);
- * memory content is then undefined, as after GCR_E_CUDA once writes began. */
+ * original address before the chain is applied -- the chain starts
+ * with a full image, which writes every page.
+ * Failure: a validation error (CORRUPT, VERSION, LAYOUT, CHAIN, INVAL) changes
+ * nothing.  Once writes have begun, any failure (GCR_E_VERIFY with counts in
+ * gcr_get_stats verify_failures / first_bad_page, GCR_E_NOMEM, GCR_E_CUDA)
+ * leaves the memory content undefined and drops the parent digest state (an
+ * incremental then returns GCR_E_CHAIN); the phase becomes LOCKED, or stays
+ * RELEASED when the restore started from RELEASED (unlock refused until a
+ * restore succeeds). */
 gcr_status gcr_restore(gcr_ctx *ctx, gcr_image *const *chain, uint32_t n);
 
 /* LOCKED|CHECKPOINTED -> RUNNING.  CHECKPOINTED keeps memory resident,

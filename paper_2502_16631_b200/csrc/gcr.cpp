@@ -14,11 +14,14 @@
 #include <atomic>
 #include <cerrno>
 #include <chrono>
+#include <condition_variable>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -309,6 +312,12 @@ struct gcr_ctx {
     int parent_idx = 0;
     uint64_t parent_gen = 0;
     uint64_t next_gen = 1;
+    // the parent state before the last successful checkpoint, and its image:
+    // gcr_checkpoint_abort undoes that checkpoint (multi-rank all-or-nothing)
+    gcr_image *last_ckpt = nullptr;
+    bool prev_have_parent = false;
+    int prev_parent_idx = 0;
+    uint64_t prev_parent_gen = 0, prev_next_gen = 1;
 
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -580,6 +589,7 @@ void image_free_buffers(gcr_image *img) {
 }
 
 void destroy_image(gcr_ctx *c, gcr_image *img) {
+    if (c->last_ckpt == img) c->last_ckpt = nullptr;
     image_free_buffers(img);
     auto it = std::find(c->images.begin(), c->images.end(), img);
     if (it != c->images.end()) c->images.erase(it);
@@ -808,10 +818,39 @@ gcr_status gcr_lock(gcr_ctx *c) {
     auto t0 = Clock::now();
     CUDA_TRY(c, cudaSetDevice(c->device));
     // "waiting for active operations ... to complete" with a timeout
-    std::vector<cudaStream_t> ws = c->watched;
-    if (ws.empty()) ws.push_back(nullptr);
+    const std::vector<cudaStream_t> &ws = c->watched;
     const uint64_t limit = c->cfg.lock_timeout_ms * 1000000ull;
-    for (;;) {
+    if (ws.empty()) {
+        // Nothing watched: the whole device must be idle (every stream of the
+        // process, blocking or not).  cudaDeviceSynchronize has no timeout, so
+        // it runs on a helper thread that the lock waits for, bounded; on
+        // expiry the helper is left to finish on its own (it touches only its
+        // shared state) and the lock rolls back.
+        struct Waiter {
+            std::mutex m;
+            std::condition_variable cv;
+            bool done = false;
+            cudaError_t err = cudaSuccess;
+        };
+        auto w = std::make_shared<Waiter>();
+        const int dev = c->device;
+        std::thread([w, dev] {
+            cudaError_t e = cudaSetDevice(dev);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            std::lock_guard<std::mutex> g(w->m);
+            w->done = true;
+            w->err = e;
+            w->cv.notify_all();
+        }).detach();
+        std::unique_lock<std::mutex> g(w->m);
+        if (!w->cv.wait_for(g, std::chrono::nanoseconds(limit), [&] { return w->done; })) {
+            c->stats.lock_ns = ns_since(t0);
+            return fail(c, GCR_E_TIMEOUT, "lock: device not idle within lock_timeout_ms (rolled back)");
+        }
+        if (w->err != cudaSuccess)
+            return fail(c, GCR_E_CUDA, std::string("lock: cudaDeviceSynchronize: ") + cudaGetErrorString(w->err));
+    }
+    while (!ws.empty()) {
         bool idle = true;
         for (cudaStream_t s : ws) {
             cudaError_t e = cudaStreamQuery(s);
@@ -1264,7 +1303,31 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
     c->images.push_back(img);
     c->phase = GCR_CHECKPOINTED;
     c->stats.checkpoint_ns = ns_since(t0);
+    c->last_ckpt = img;
+    c->prev_have_parent = had_parent;
+    c->prev_parent_idx = pidx;
+    c->prev_parent_gen = pgen;
+    c->prev_next_gen = c->next_gen - 1;
     *out = img;
+    return GCR_OK;
+}
+
+gcr_status gcr_checkpoint_abort(gcr_ctx *c, gcr_image *img) {
+    if (!c) return GCR_E_INVAL;
+    if (c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "checkpoint_abort: not CHECKPOINTED");
+    if (!img || img != c->last_ckpt)
+        return fail(c, GCR_E_INVAL, "checkpoint_abort: not the image of the ctx's last checkpoint");
+    cudaSetDevice(c->device);
+    sync_all(c);
+    destroy_image(c, img);
+    c->last_ckpt = nullptr;
+    // the digest table the checkpoint wrote was the non-parent one: the old
+    // parent table is intact, so the previous state is restored exactly
+    c->have_parent = c->prev_have_parent;
+    c->parent_idx = c->prev_parent_idx;
+    c->parent_gen = c->prev_parent_gen;
+    c->next_gen = c->prev_next_gen;
+    c->phase = GCR_LOCKED;
     return GCR_OK;
 }
 
@@ -1282,8 +1345,7 @@ static gcr_status ensure_desc(gcr_ctx *c, uint64_t bytes) {
     return GCR_OK;
 }
 
-gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
-    if (!c) return GCR_E_INVAL;
+static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, bool &writes_began) {
     if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED && c->phase != GCR_RELEASED)
         return fail(c, GCR_E_STATE, "restore: not locked");
     if (!chain || n == 0) return fail(c, GCR_E_INVAL, "restore: empty chain");
@@ -1317,6 +1379,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
     st.remap_ns = 0;
+    writes_began = true;  // from here on a failure leaves the memory content undefined
     if (c->phase == GCR_RELEASED) {  // back the same VAs again, then apply the chain
         const auto r0 = Clock::now();
         for (MemBlock &b : c->blocks) {
@@ -1327,7 +1390,8 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
                             "restore: re-mapping released memory failed (driver error " + std::to_string((int)r) + ")");
         }
         st.remap_ns = ns_since(r0);
-        c->phase = GCR_LOCKED;  // memory is back (content undefined until the chain is applied)
+        // the phase stays RELEASED (content not valid: unlock refused) until
+        // the chain has been applied and verified
     }
     gcr_status s = build_layout(c);
     if (s != GCR_OK) return s;
@@ -1553,18 +1617,32 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
     }
     st.verify_launches = verify_launches;
     st.restore_h2d_bytes = h2d_bytes;
-    c->phase = GCR_LOCKED;
     st.restore_ns = ns_since(t0);
-    if (st.verify_failures) {
-        c->have_parent = false;
+    if (st.verify_failures)
         return fail(c, GCR_E_VERIFY, "restore: " + std::to_string(st.verify_failures) + " page digest(s) differ");
-    }
+    c->phase = GCR_LOCKED;
     // the next incremental diffs against the restored state (c.2 step 4)
     c->parent_idx = scratch;
     c->parent_gen = last->hdr.generation;
     c->have_parent = true;
     c->next_gen = std::max(c->next_gen, last->hdr.generation + 1);
     return GCR_OK;
+}
+
+gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
+    if (!c) return GCR_E_INVAL;
+    const gcr_phase ph0 = c->phase;
+    bool writes_began = false;
+    const gcr_status s = restore_impl(c, chain, n, writes_began);
+    if (s != GCR_OK && writes_began) {
+        // memory content undefined: no incremental may diff against it, and
+        // memory re-backed after a release stays RELEASED (unlock refused)
+        // until a restore succeeds
+        sync_all(c);
+        c->have_parent = false;
+        c->phase = ph0 == GCR_RELEASED ? GCR_RELEASED : GCR_LOCKED;
+    }
+    return s;
 }
 
 gcr_status gcr_mem_alloc(gcr_ctx *c, uint64_t bytes, uint64_t *dptr_out) {

@@ -60,7 +60,11 @@ def lock_all(ctx, group=None) -> int:
 
 
 def checkpoint_all(ctx, mode: int = 0, group=None):
-    """C2 + C3: barrier, local checkpoint, barrier, manifest gather to rank 0.
+    """C2 + C3: barrier, local checkpoint, outcome vote, manifest gather to
+    rank 0.  All or nothing: if any rank failed, every rank whose checkpoint
+    succeeded undoes it (gcr_checkpoint_abort: image freed, parent digest
+    state and generation restored, phase back to LOCKED), so every rank is
+    LOCKED exactly as before the attempt and a retry is legal everywhere.
     Returns (image or None, list of Manifest on rank 0 else None)."""
     dist = _pg()
     dist.barrier(group=group)
@@ -72,8 +76,11 @@ def checkpoint_all(ctx, mode: int = 0, group=None):
         st = getattr(e, "status", -1)
     dt = time.perf_counter_ns() - t0
     ok = _vote(st == GCR_OK, group)
-    dist.barrier(group=group)
     h = img.header() if img is not None else None
+    if not ok and img is not None:
+        ctx.checkpoint_abort(img)
+        img = None
+    dist.barrier(group=group)
     man = Manifest(rank=dist.get_rank(), status=st if ok or st != GCR_OK else GCR_E_PEER,
                    generation=int(h.generation) if h else 0, n_pages=int(h.n_pages) if h else 0,
                    image_bytes=int(h.image_bytes) if h else 0, meta_crc32c=int(h.meta_crc32c) if h else 0,
@@ -112,6 +119,12 @@ def release_all(ctx, group=None) -> int:
     return st if st != GCR_OK else GCR_E_PEER
 
 
-def unlock_all(ctx, group=None) -> None:
-    ctx.unlock()
-    _pg().barrier(group=group)
+def unlock_all(ctx, group=None) -> int:
+    """Unlock on every rank; every rank always reaches the vote (no rank is
+    left blocked in a barrier when another one cannot unlock, e.g. while it is
+    still RELEASED).  Returns GCR_OK, the local status, or GCR_E_PEER."""
+    st = ctx.try_unlock()
+    ok = _vote(st == GCR_OK, group)
+    if ok:
+        return GCR_OK
+    return st if st != GCR_OK else GCR_E_PEER

@@ -88,6 +88,7 @@ _SIGS = {
     "gcr_mem_alloc": [_vp, _u64, _P(_u64)],
     "gcr_mem_free": [_vp, _u64],
     "gcr_release": [_vp],
+    "gcr_checkpoint_abort": [_vp, _vp],
     "gcr_image_header": [_vp, _P(gcr_image_hdr)],
     "gcr_image_allocs": [_vp, _P(_P(gcr_alloc_rec)), _P(_u32)],
     "gcr_image_pagemap": [_vp, _P(_P(gcr_pagemap_entry)), _P(_u64)],
@@ -160,6 +161,19 @@ class Image:
         self.ctx._check(gcr_image_pagemap(self.handle, C.byref(p), C.byref(n)))
         return [(p[i].vaddr, p[i].nr_pages, p[i].flags) for i in range(n.value)]
 
+    def pagemap_array(self):
+        """Zero-copy numpy structured view {vaddr u64, nr_pages u32, flags u32} of
+        the pinned pagemap (valid until free)."""
+        import numpy as np
+        p = _P(gcr_pagemap_entry)()
+        n = C.c_uint64()
+        self.ctx._check(gcr_image_pagemap(self.handle, C.byref(p), C.byref(n)))
+        dt = np.dtype([("vaddr", "<u8"), ("nr_pages", "<u4"), ("flags", "<u4")])
+        if n.value == 0:
+            return np.zeros(0, dt)
+        buf = (C.c_uint8 * (16 * n.value)).from_address(C.addressof(p.contents))
+        return np.frombuffer(buf, dtype=dt)
+
     def data_view(self):
         """Zero-copy numpy view of the pinned image data (valid until free)."""
         import numpy as np
@@ -184,6 +198,7 @@ class Context:
     """One libgcr context per (process, device)."""
 
     def __init__(self, device: int = 0, **cfg):
+        self.device = device
         self.cfg = default_config(**cfg)
         h = C.c_void_p()
         st = gcr_create(device, C.byref(self.cfg), C.byref(h))
@@ -238,6 +253,11 @@ class Context:
         self._check(gcr_checkpoint(self.h, mode, C.byref(out)))
         return Image(self, out.value)
 
+    def checkpoint_abort(self, img: "Image"):
+        """Undo the last checkpoint (CHECKPOINTED -> LOCKED); frees img."""
+        self._check(gcr_checkpoint_abort(self.h, img.handle))
+        img.handle = C.c_void_p(None)
+
     def restore(self, chain) -> int:
         arr = (C.c_void_p * len(chain))(*[im.handle.value for im in chain])
         return self._check(gcr_restore(self.h, arr, len(chain)))
@@ -258,18 +278,21 @@ class Context:
     def mem_free(self, dptr: int):
         self._check(gcr_mem_free(self.h, dptr))
 
-    def alloc_tensor(self, nbytes: int, device: int = 0):
-        """A torch uint8 CUDA tensor over fresh gcr_mem_alloc memory (zero-copy,
-        via __cuda_array_interface__).  The tensor does not own the memory: it
-        stays valid until mem_free / close, and across release -> restore (the
-        address does not change)."""
+    def alloc_tensor(self, nbytes: int, device: int | None = None):
+        """A torch uint8 CUDA tensor over fresh gcr_mem_alloc memory on the ctx's
+        device (zero-copy, via __cuda_array_interface__).  The tensor keeps the
+        Context alive (the memory is the ctx's); it stays valid until mem_free /
+        close, and across release -> restore (the address does not change)."""
         import torch
         dptr = self.mem_alloc(nbytes)
+        dev = self.device if device is None else device
 
         class _Mem:
             __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (dptr, False),
                                         "version": 3, "strides": None}
-        return torch.as_tensor(_Mem(), device=f"cuda:{device}")
+        m = _Mem()
+        m.ctx = self  # the tensor's base object holds the ctx: no gcr_destroy under a live tensor
+        return torch.as_tensor(m, device=f"cuda:{dev}")
 
     def release(self):
         self._check(gcr_release(self.h))

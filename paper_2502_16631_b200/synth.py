@@ -4,7 +4,9 @@ Holds none of the snapshot method's arithmetic (no CRC, no classification, no
 packing): only the counter-based generator that both sides of every parity
 test draw their inputs from.  The CPU twin here (numpy) and the GPU fill in
 libgcr_synth.so (include/gcr_synth.h) implement the same formula, so the bytes
-are identical; tests/test_synth_gpu.py checks that on the GPU.
+are identical: tests/test_gpu_parity.py::test_gpu_generator_matches_cpu_twin
+checks that on the GPU and tests/test_synth.py pins the CPU twin to a scalar
+restatement of the formulas.
 
 Word i (u64 LE) of an allocation with key k under seed s:
     r = splitmix64(s ^ (k << 40) ^ i), then shaped by `kind` (gcr_synth.h).
@@ -38,19 +40,29 @@ _M = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
 def splitmix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 of every element (a new array; in-place steps keep the
+    full-size parity harness fast)."""
     with np.errstate(over="ignore"):
         z = x + np.uint64(0x9E3779B97F4A7C15)
-        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        return z ^ (z >> np.uint64(31))
+        t = z >> np.uint64(30)
+        z ^= t
+        z *= np.uint64(0xBF58476D1CE4E5B9)
+        np.right_shift(z, np.uint64(27), out=t)
+        z ^= t
+        z *= np.uint64(0x94D049BB133111EB)
+        np.right_shift(z, np.uint64(31), out=t)
+        z ^= t
+        return z
 
 
-def _f32(b: np.ndarray, e0: int, sign: bool) -> np.ndarray:
-    v = (np.uint32(e0) + ((b >> np.uint32(23)) & np.uint32(3))) << np.uint32(23)
-    v = v | (b & np.uint32(0x7FFFFF))
-    if sign:
-        v = v | (b & np.uint32(0x80000000))
-    return v
+def _f32_inplace(b: np.ndarray, e0: int, sign: bool) -> None:
+    """b (uint32, every 32-bit half of the words) <- sign(b) | (e0 + ((b>>23)&3)) << 23 | b & 0x7FFFFF."""
+    t = b >> np.uint32(23)
+    t &= np.uint32(3)
+    t += np.uint32(e0)
+    t <<= np.uint32(23)
+    b &= np.uint32(0x807FFFFF if sign else 0x007FFFFF)
+    b |= t
 
 
 def gen_words(seed: int, key: int, start: int, n: int, kind: int, const_bits: int = 0) -> np.ndarray:
@@ -60,23 +72,24 @@ def gen_words(seed: int, key: int, start: int, n: int, kind: int, const_bits: in
     if kind == F32_CONST:
         c = np.uint64(const_bits | (const_bits << 32))
         return np.full(n, c, np.uint64)
-    ctr = np.uint64(seed ^ (key << 40)) ^ np.arange(start, start + n, dtype=np.uint64)
+    ctr = np.arange(start, start + n, dtype=np.uint64)
+    ctr ^= np.uint64(seed ^ (key << 40))
     r = splitmix64(ctr)
     if kind == RANDOM:
         return r
     if kind in (F32_WEIGHT, F32_M, F32_V):
         e0, sg = {F32_WEIGHT: (118, True), F32_M: (113, True), F32_V: (103, False)}[kind]
-        lo = _f32((r & np.uint64(0xFFFFFFFF)).astype(np.uint32), e0, sg).astype(np.uint64)
-        hi = _f32((r >> np.uint64(32)).astype(np.uint32), e0, sg).astype(np.uint64)
-        return lo | (hi << np.uint64(32))
+        _f32_inplace(r.view(np.uint32), e0, sg)  # both halves of every LE word
+        return r
     if kind == BF16_WEIGHT:
-        out = np.zeros(n, np.uint64)
-        for k in range(4):
-            h = ((r >> np.uint64(16 * k)) & np.uint64(0xFFFF)).astype(np.uint32)
-            v = (h & np.uint32(0x8000)) | ((np.uint32(118) + ((h >> np.uint32(7)) & np.uint32(3))) << np.uint32(7)) \
-                | (h & np.uint32(0x7F))
-            out |= v.astype(np.uint64) << np.uint64(16 * k)
-        return out
+        h = r.view(np.uint16)  # the four 16-bit quarters of every LE word
+        t = h >> np.uint16(7)
+        t &= np.uint16(3)
+        t += np.uint16(118)
+        t <<= np.uint16(7)
+        h &= np.uint16(0x807F)
+        h |= t
+        return r
     raise ValueError(kind)
 
 

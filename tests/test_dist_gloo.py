@@ -32,10 +32,12 @@ class FakeImage:
 class FakeCtx:
     """Phase machine of include/gcr.h without a GPU (RUNNING/LOCKED/CHECKPOINTED)."""
 
-    def __init__(self, rank, lock_status=0, restore_status=0, nbytes=1000, release_status=0):
+    def __init__(self, rank, lock_status=0, restore_status=0, nbytes=1000, release_status=0, ckpt_fail_once=0):
         self.rank, self.lock_status, self.restore_status, self.nbytes = rank, lock_status, restore_status, nbytes
         self.release_status = release_status
+        self.ckpt_fail_once = ckpt_fail_once
         self.phase, self.gen, self.log = 0, 0, []
+        self.last = None
 
     def try_lock(self):
         self.log.append("lock")
@@ -49,11 +51,31 @@ class FakeCtx:
         assert self.phase in (1, 2)
         self.phase = 0
 
+    def try_unlock(self):
+        if self.phase not in (1, 2):
+            return 2  # GCR_E_STATE (e.g. still RELEASED)
+        self.unlock()
+        return 0
+
     def checkpoint(self, mode=0):
         assert self.phase == 1
+        if self.ckpt_fail_once:
+            st, self.ckpt_fail_once = self.ckpt_fail_once, 0
+            self.log.append("checkpoint_failed")
+            e = RuntimeError("injected")
+            e.status = st
+            raise e
         self.gen += 1
         self.phase = 2
-        return FakeImage(FakeHeader(self.gen, 10, self.nbytes * (self.rank + 1)))
+        self.last = FakeImage(FakeHeader(self.gen, 10, self.nbytes * (self.rank + 1)))
+        return self.last
+
+    def checkpoint_abort(self, img):  # CHECKPOINTED -> LOCKED, generation re-issued
+        assert self.phase == 2 and img is self.last
+        self.log.append("abort")
+        self.gen -= 1
+        self.phase = 1
+        self.last = None
 
     def try_restore(self, chain):
         assert self.phase in (1, 2, 3)
@@ -95,6 +117,23 @@ def _worker(rank, world, port, scenario, q):
             rs = gd.restore_all(ctx, [img])  # the only way out of RELEASED, everywhere
             gd.unlock_all(ctx)
             q.put((rank, rl, ph, rs, ctx.phase, ctx.log))
+        elif scenario == "ckpt_fail_on_1":
+            ctx = FakeCtx(rank, ckpt_fail_once=11 if rank == 1 else 0)
+            gd.lock_all(ctx)
+            img, mans = gd.checkpoint_all(ctx)
+            first = (img is None, ctx.phase, ctx.gen, mans and [(m.rank, m.status) for m in mans])
+            img2, mans2 = gd.checkpoint_all(ctx)  # a retry is legal on every rank
+            second = (img2 is not None, ctx.phase, img2.header().generation if img2 else None)
+            un = gd.unlock_all(ctx)
+            q.put((rank, first, second, un, ctx.log))
+        elif scenario == "unlock_while_released_on_1":
+            ctx = FakeCtx(rank)
+            gd.lock_all(ctx)
+            gd.checkpoint_all(ctx)
+            if rank == 1:
+                ctx.phase = 3  # RELEASED: unlock is not legal there
+            un = gd.unlock_all(ctx)  # must not leave rank 0 blocked in a barrier
+            q.put((rank, un, ctx.phase))
         elif scenario == "verify_on_0":
             ctx = FakeCtx(rank, restore_status=9 if rank == 0 else 0)
             gd.lock_all(ctx)
@@ -154,3 +193,22 @@ def test_release_failure_on_one_rank_is_reported_everywhere():
     out = _run("release", world=3)
     assert [(r, rl, ph) for r, rl, ph, *_ in out] == [(0, 4, 3), (1, 2, 2), (2, 4, 3)]
     assert all(rs == 0 and ph_end == 0 for _, _, _, rs, ph_end, _ in out)
+
+
+def test_checkpoint_failure_on_one_rank_is_all_or_nothing():
+    """A failed checkpoint on rank 1: rank 0 undoes its successful one
+    (checkpoint_abort), both stay LOCKED with the old generation, and a retry
+    of checkpoint_all then succeeds everywhere with the SAME generation."""
+    out = _run("ckpt_fail_on_1")
+    (r0, f0, s0, u0, log0), (r1, f1, s1, u1, log1) = out
+    assert f0[:3] == (True, 1, 0) and f1[:3] == (True, 1, 0)
+    assert f0[3] == [(0, 4), (1, 11)]      # rank 0's manifest: peer failure / local failure
+    assert s0 == (True, 2, 1) and s1 == (True, 2, 1)
+    assert u0 == u1 == 0
+    assert log0 == ["lock", "abort", "unlock"]
+    assert log1 == ["lock", "checkpoint_failed", "unlock"]
+
+
+def test_unlock_all_never_blocks_on_a_refusing_rank():
+    out = _run("unlock_while_released_on_1")
+    assert out == [(0, 4, 0), (1, 2, 3)]

@@ -185,3 +185,75 @@ def test_stats_and_launch_counter(G):
         ctx.unlock()
     finally:
         ctx.close()
+
+
+def test_unwatched_lock_waits_for_non_blocking_side_streams(G):
+    """No watched stream: lock must see the WHOLE device idle, including a
+    torch side stream (cudaStreamNonBlocking) running a never-ending kernel ->
+    TIMEOUT with phase RUNNING; once the kernel ends, lock succeeds."""
+    gcr, synth = G
+    L = synth.synth_lib()
+    hp, dp = C.c_uint64(), C.c_uint64()
+    assert L.gsy_flag_alloc(C.byref(hp), C.byref(dp)) == 0
+    t = torch.empty(1 << 20, dtype=torch.uint8, device="cuda").fill_(5)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()  # non-blocking w.r.t. the legacy stream
+    ctx = gcr.Context(0, lock_timeout_ms=300)
+    try:
+        ctx.register_tensor(t)
+        assert L.gsy_spin_until_flag(dp.value, C.c_void_p(s.cuda_stream)) == 0
+        import time
+        t0 = time.perf_counter()
+        st = ctx.try_lock()
+        dt = time.perf_counter() - t0
+        assert st == gcr.GCR_E_TIMEOUT and ctx.phase() == gcr.GCR_RUNNING
+        assert 0.29 <= dt < 3.0
+        L.gsy_flag_set(hp.value, 1)
+        assert ctx.try_lock() == gcr.GCR_OK  # waits for the kernel to end, well within 300 ms
+        ctx.unlock()
+    finally:
+        L.gsy_flag_set(hp.value, 1)
+        torch.cuda.synchronize()
+        ctx.close()
+        L.gsy_flag_free(hp.value)
+
+
+def test_checkpoint_abort_restores_the_parent_state(G, orc):
+    """gcr_checkpoint_abort undoes the last checkpoint: image freed, phase
+    LOCKED, generation re-issued, and the next incremental diffs against the
+    parent from BEFORE the aborted checkpoint."""
+    gcr, synth = G
+    P = 65536
+    t = torch.empty(8 * P, dtype=torch.uint8, device="cuda")
+    synth.gpu_fill(t.data_ptr(), t.numel(), 5, 0, synth.RANDOM)
+    torch.cuda.synchronize()
+    ctx = gcr.Context(0, page_size=P)
+    try:
+        ctx.register_tensor(t)
+        ctx.lock()
+        full = ctx.checkpoint()
+        ctx.unlock()
+        synth.gpu_xor_u32(t.data_ptr() + 2 * P, 1)
+        torch.cuda.synchronize()
+        ctx.lock()
+        inc = ctx.checkpoint(gcr.GCR_INCREMENTAL)
+        assert inc.header().generation == 2 and inc.header().n_present == 1
+        ctx.checkpoint_abort(inc)
+        assert ctx.phase() == gcr.GCR_LOCKED
+        # abort only the LAST checkpoint's image, only from CHECKPOINTED
+        assert gcr.gcr_checkpoint_abort(ctx.h, full.handle) == gcr.GCR_E_STATE
+        ctx.unlock()
+        synth.gpu_xor_u32(t.data_ptr() + 5 * P, 1)  # another page: both now differ from `full`
+        torch.cuda.synchronize()
+        ctx.lock()
+        inc2 = ctx.checkpoint(gcr.GCR_INCREMENTAL)
+        h = inc2.header()
+        assert h.generation == 2 and h.parent_generation == 1 and h.n_present == 2
+        assert gcr.gcr_checkpoint_abort(ctx.h, full.handle) == gcr.GCR_E_INVAL
+        ref = t.cpu().numpy().copy()
+        t.fill_(0xA5)
+        ctx.restore([full, inc2])
+        assert np.array_equal(t.cpu().numpy(), ref)
+        ctx.unlock()
+    finally:
+        ctx.close()

@@ -179,3 +179,45 @@ def test_mem_free_returns_memory(G):
             ctx.mem_free(p)
     finally:
         ctx.close()
+
+
+def test_failed_restore_from_released_stays_released(G, orc):
+    """A restore from RELEASED whose verify fails leaves the phase RELEASED
+    (content not valid: unlock refused) and drops the parent digest state; a
+    good restore afterwards brings the state back (no unlock onto
+    undefined memory)."""
+    gcr, synth = G
+    P = 65536
+    sizes = [3 * MiB, 2 * MiB]
+    ctx = gcr.Context(0, page_size=P)
+    try:
+        ts = _blocks(ctx, synth, sizes, 77, P)
+        registry_of(ctx, ts)
+        cont = host_copies(ts)
+        ctx.lock()
+        img = ctx.checkpoint(gcr.GCR_FULL)
+        bad = ctx.import_stream(img.stream())
+        bad.data_view()[12345] ^= 1
+        ctx.release()
+        assert ctx.try_restore([bad]) == gcr.GCR_E_VERIFY
+        assert ctx.phase() == gcr.GCR_RELEASED
+        assert ctx.try_unlock() == gcr.GCR_E_STATE
+        ctx.restore([img])
+        assert ctx.phase() == gcr.GCR_LOCKED
+        for t, c in zip(ts, cont):
+            assert np.array_equal(t.cpu().numpy(), c)
+        ctx.unlock()
+    finally:
+        ctx.close()
+
+
+def test_alloc_tensor_keeps_the_context_alive(G):
+    gcr, synth = G
+    import gc
+    ctx = gcr.Context(0)
+    t = ctx.alloc_tensor(4 * MiB)
+    del ctx
+    gc.collect()
+    t.fill_(3)  # the memory is still mapped: the tensor holds the ctx
+    torch.cuda.synchronize()
+    assert int(t[4 * MiB - 1].item()) == 3
