@@ -15,8 +15,14 @@ value  = sum over ranks of registered bytes / step time (GB/s of state that
          CUDA-event interval on the library's stream.
 e2e    = the same bytes / host wall clock of the public Python API calls
          (Context.lock/checkpoint/restore/unlock + image free), max over ranks.
---impl reference times the CPU oracle (oracle/, plain C, 1 thread) on a
-bounded sample of the same workload (rank 0 only).
+box    = the same bytes / barrier-to-barrier host time per step (every rank
+         passes a gloo barrier before and after each step), max over ranks.
+--gpus N without torchrun re-launches this script as N ranks
+(torch.distributed.run, 127.0.0.1); each rank binds itself and its pinned
+memory to its GPU's NUMA node before any pinned allocation.
+--impl reference times the CPU oracle (oracle/, plain C, one single-threaded
+instance per host core over a partition of the allocations) on the WHOLE
+workload (rank 0 only); it never loads the product library.
 """
 from __future__ import annotations
 
@@ -27,6 +33,8 @@ import statistics
 import subprocess
 import sys
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -133,12 +141,18 @@ def _barrier(pg):
         pg.barrier()
 
 
-def probe_links(torch, nbytes=1 << 30):
-    """K10 probes: pinned D2H / H2D copy bandwidth (the drain / restore roofline
-    denominators), measured in this run with this rank's concurrency."""
+def probe_links(torch, ctx=None, nbytes=1 << 30):
+    """K10 probes, taken with every rank probing at once
+    (the caller brackets this with barriers): pinned D2H / H2D copy bandwidth
+    -- the drain / restore roofline denominators -- over the image pool itself
+    (gcr_probe_link: the pinned pages the next image lands on) and over a
+    separate torch pinned buffer, plus an HBM read probe."""
+    out = {}
+    if ctx is not None:
+        d2h, h2d = ctx.probe_link(nbytes)
+        out["pool_d2h_gbs"], out["pool_h2d_gbs"] = round(d2h, 2), round(h2d, 2)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-    out = {}
     for name, fn in (("d2h_gbs", lambda: h.copy_(d, non_blocking=True)),
                      ("h2d_gbs", lambda: d.copy_(h, non_blocking=True))):
         fn()
@@ -167,16 +181,86 @@ def probe_links(torch, nbytes=1 << 30):
     return out
 
 
+def bind_numa(torch, dev: int) -> dict:
+    """Bind this rank's threads and its later host allocations (the pinned
+    image pool) to the NUMA node of its GPU (SURVEY §8(e) 'shared resources',
+    H4): sysfs numa_node of the GPU's PCI function -> sched_setaffinity to the
+    node's CPUs + set_mempolicy(MPOL_PREFERRED, node).  Called before any
+    pinned allocation.  A node of -1 (a single-node VM) binds nothing."""
+    p = torch.cuda.get_device_properties(dev)
+    bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    info = {"gpu_bdf": bdf}
+    try:
+        node = int(open(f"/sys/bus/pci/devices/{bdf}/numa_node").read().strip())
+    except OSError as e:
+        return {**info, "numa_node": None, "bound": False, "why": f"sysfs: {e.strerror}"}
+    info["numa_node"] = node
+    if node < 0:
+        return {**info, "bound": False, "why": "sysfs numa_node = -1 (one NUMA node: nothing to bind)"}
+    cpus = set()
+    for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+        a, _, b = part.partition("-")
+        cpus.update(range(int(a), int(b or a) + 1))
+    os.sched_setaffinity(0, cpus)
+    import ctypes
+    libc = ctypes.CDLL(None, use_errno=True)
+    mask = (ctypes.c_ulong * 16)()
+    mask[node // 64] = 1 << (node % 64)
+    MPOL_PREFERRED, SYS_set_mempolicy = 1, 238  # x86_64
+    rc = libc.syscall(SYS_set_mempolicy, MPOL_PREFERRED, mask, 16 * 64 + 1)
+    return {**info, "bound": True, "cpus": len(cpus), "mempolicy": "preferred" if rc == 0 else
+            f"set_mempolicy failed (errno {ctypes.get_errno()})"}
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: re-run this script as N ranks of one node
+    (one process per GPU) through torch.distributed.run on 127.0.0.1; rank 0
+    prints the JSON line (stdout is inherited)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 def run_ours(args):
     import torch
     world, rank, local, pg = _dist()
-    # one rank per GPU; on a box with fewer GPUs than ranks (functional tests)
-    # ranks share devices round-robin
-    dev = local % torch.cuda.device_count()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but {world} rank(s) running")
+    if args.dry_run:  # launch plumbing only (CPU-testable): every rank reports, rank 0 prints
+        me = {"rank": rank, "local_rank": local, "pid": os.getpid()}
+        allr = [None] * world
+        if pg is not None:
+            pg.all_gather_object(allr, me)
+            pg.barrier()
+        else:
+            allr = [me]
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": allr}), flush=True)
+        if pg is not None:
+            pg.destroy_process_group()
+        return
+    # one rank per GPU; on a box with fewer GPUs than ranks (functional runs)
+    # ranks share devices round-robin, and the line says so
+    n_dev = torch.cuda.device_count()
+    dev = local % n_dev
+    numa = bind_numa(torch, dev)  # before the first pinned allocation
     torch.cuda.set_device(dev)
     local = dev
     from paper_2502_16631_b200 import dist as gdist
     from paper_2502_16631_b200 import gcr, synth
+    if args.direct_min_mb is None:
+        args.direct_min_mb = gcr.default_config().direct_min_bytes / (1 << 20)
 
     w = synth.make_workload(args.config, rank=rank, page_size=args.page_size, gib=args.gib)
     ctx = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20,
@@ -200,7 +284,9 @@ def run_ours(args):
         ctx.reserve_host(need if keep_chain else 2 * R0 + 2 * per_inc + (256 << 20))
     else:
         ctx.reserve_host(R0 + (256 << 20))
-    probes = probe_links(torch)
+    _barrier(pg)  # every rank probes at once: BW_d2h(N), BW_h2d(N)
+    probes = probe_links(torch, ctx)
+    _barrier(pg)
     R = w.total_bytes
     cst = ctx.stream()
     stream = torch.cuda.ExternalStream(cst)
@@ -225,12 +311,14 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         h0 = time.perf_counter()
         e0.record(stream)
+        v0 = time.perf_counter()
         if pg is not None:  # globally consistent cut: all-or-nothing lock vote over gloo (dist.py)
             st = gdist.lock_all(ctx)
             if st != 0:
                 raise RuntimeError(f"lock vote failed: {st}")
         else:
             ctx.lock()
+        lock_wall = time.perf_counter() - v0
         img = ctx.checkpoint(gcr.GCR_INCREMENTAL if incremental else gcr.GCR_FULL)
         s_ck = ctx.stats()
         if args.release:
@@ -255,6 +343,7 @@ def run_ours(args):
         h1 = time.perf_counter()
         e1.synchronize()
         s = ctx.stats()
+        s["lock_wall_ns"] = int(lock_wall * 1e9)
         return e0.elapsed_time(e1) * 1e-3, h1 - h0, s_ck, s
 
     for _ in range(args.warmup):
@@ -262,12 +351,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     _barrier(pg)
     launches0 = ctx.stats()["kernel_launches"]
-    dev, host, recs = [], [], []
+    dev, host, recs, box = [], [], [], []
     with ClockSampler(local) as clk:
         _barrier(pg)
         torch.cuda.synchronize()
         for _ in range(args.steps):
+            _barrier(pg)
+            b0 = time.perf_counter()
             d, h, sck, s = step(True)
+            torch.cuda.synchronize()
+            _barrier(pg)
+            box.append(time.perf_counter() - b0)
             dev.append(d)
             host.append(h)
             recs.append((sck, s))
@@ -290,6 +384,16 @@ def run_ours(args):
         base_img.free()
     t_dev = _max_over_ranks(pg, sum(dev))
     t_host = _max_over_ranks(pg, sum(host))
+    t_box = _max_over_ranks(pg, sum(box))
+    lock_ms = sum(r[1]["lock_ns"] for r in recs) / len(recs) * 1e-6
+    unlock_ms = sum(r[1]["unlock_ns"] for r in recs) / len(recs) * 1e-6
+    vote_ms = sum(r[1]["lock_wall_ns"] - r[1]["lock_ns"] for r in recs) / len(recs) * 1e-6
+    clocks_me = clk.summary()
+    if pg is not None:
+        allc = [None] * world
+        pg.all_gather_object(allc, {"rank": rank, "gpu": local, **clocks_me, "numa": numa})
+    else:
+        allc = [{"rank": 0, "gpu": local, **clocks_me, "numa": numa}]
     R_all = _sum_over_ranks(pg, float(R))
     K = args.steps
     # per-phase, per-rank means
@@ -361,11 +465,20 @@ def run_ours(args):
                     "roundtrip_GBps": round(R * K / t_dev / 1e9, 3),
                     "image_GBps_ckpt": round(img_b / ck / 1e9, 3)},
         "box": {"checkpoint_GBps": round(_sum_over_ranks(pg, ck_gbs), 3),
-                "restore_GBps": round(_sum_over_ranks(pg, rs_gbs), 3)},
+                "restore_GBps": round(_sum_over_ranks(pg, rs_gbs), 3),
+                "barrier_to_barrier_GBps": round(R_all * K / t_box / 1e9, 3),
+                "barrier_to_barrier_ms_per_step": round(t_box / K * 1e3, 3),
+                "what": "sum over ranks of registered bytes / (gloo barrier -> step -> sync -> gloo barrier), max over ranks"},
+        "phases_ms": {"lock": round(_max_over_ranks(pg, lock_ms), 4), "unlock": round(_max_over_ranks(pg, unlock_ms), 4),
+                      "vote": round(_max_over_ranks(pg, vote_ms), 4) if pg is not None else None,
+                      "what": "mean per step, max over ranks: gcr_lock / gcr_unlock host time; vote = lock_all wall "
+                              "time minus the local lock (gloo all_reduce MIN), N > 1 only (paper: lock 240 ms, "
+                              "unlock ~160 ms for GPT-2 S on H100, P:392-393)"},
         "link_roofline": {"drain_GBps": round(img_b / (sc["drain_ns"] * 1e-9) / 1e9, 2),
-                          "d2h_probe_GBps": probes["d2h_gbs"], "h2d_probe_GBps": probes["h2d_gbs"],
-                          "checkpoint_frac_of_d2h": round(ck_gbs / probes["d2h_gbs"] * img_b / R, 3),
-                          "restore_frac_of_h2d": round(rs_gbs / probes["h2d_gbs"] * img_b / R, 3) if not incremental else None},
+                          "d2h_probe_GBps": probes["pool_d2h_gbs"], "h2d_probe_GBps": probes["pool_h2d_gbs"],
+                          "probe": "image pool itself (gcr_probe_link), all ranks probing at once",
+                          "checkpoint_frac_of_d2h": round(ck_gbs / probes["pool_d2h_gbs"] * img_b / R, 3),
+                          "restore_frac_of_h2d": round(rs_gbs / probes["pool_h2d_gbs"] * img_b / R, 3) if not incremental else None},
         "roofline": {"kernel": "k_scan (K1 scan + K8 verify launches)", "bound": "hbm",
                      "launches_per_step": round(scan_launches / K, 2),
                      "alg_bytes_per_launch": round(scan_bytes / max(scan_launches, 1)),
@@ -392,7 +505,14 @@ def run_ours(args):
                     "what": "f3: pinned image -> file (parallel pwrite + fdatasync + drop cache) -> pinned image (parallel pread)"}
         if args.storage else None,
     }
-    result["clocks"] = clk.summary()
+    sm = [c["sm_mhz"] for c in allc if c.get("sm_mhz")]
+    result["clocks"] = {"sm_mhz": min(sm) if sm else None, "sm_max_mhz": clocks_me["sm_max_mhz"],
+                        "reasons": sorted({r for c in allc for r in c["reasons"]}),
+                        "samples": sum(c["samples"] for c in allc),
+                        "per_rank": [{k: c[k] for k in ("rank", "gpu", "sm_mhz", "reasons", "samples")} for c in allc],
+                        "what": "nvidia-smi during the timed region on every rank's GPU; sm_mhz = the lowest rank median"}
+    result["placement"] = {"ranks": world, "gpus_visible": n_dev, "shared_gpus": world > n_dev,
+                           "numa": [c["numa"] for c in allc]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_seconds)
     if rank == 0:
@@ -411,84 +531,128 @@ def _workload_desc(name, w):
             "C5": f"C5: {len(w.allocs)} GiB per GPU, 25% zero 2 MiB regions, full checkpoint + restore"}[name]
 
 
+def _partition(sizes, T):
+    """Allocations -> T groups, greedy by bytes (largest first onto the least
+    loaded), order kept inside a group."""
+    load, groups = [0] * T, [[] for _ in range(T)]
+    for a in sorted(range(len(sizes)), key=lambda i: -sizes[i]):
+        k = min(range(T), key=lambda j: load[j])
+        groups[k].append(a)
+        load[k] += sizes[a]
+    return [sorted(g) for g in groups if g]
+
+
+class OracleWorkload:
+    """The oracle as it stands (oracle/gcr_oracle.c: plain C, single-threaded,
+    Sarwate CRC) over the WHOLE workload: the allocations are partitioned over
+    T threads, each running one unmodified oracle instance -- checkpoint into a
+    canonical stream, then restore it into a poisoned copy with the full verify
+    -- on its own registry (ctypes releases the GIL in the C calls).  Inputs
+    come from the CPU twin of the generator, built once, untimed."""
+
+    def __init__(self, w, threads: int):
+        from oracle import oracle
+        self.orc, self.P = oracle, w.page_size
+        sizes = [s.nbytes for s in w.allocs]
+        self.groups = _partition(sizes, max(1, threads))
+        self.cont = [w.cpu_bytes(a) for a in range(len(sizes))]
+        self.sizes = sizes
+        self.bytes = sum(sizes)
+
+    def _one(self, g):
+        orc = self.orc
+        reg = [(a + 1, 0x7F0000000000 + (a << 32), self.sizes[a]) for a in g]
+        st, s = orc.checkpoint(self.P, reg, [self.cont[a] for a in g])
+        tgt = [np.full(self.sizes[a], 0xA5, np.uint8) for a in g]
+        st2, vf, _ = orc.restore([s], self.P, [self.sizes[a] for a in g], tgt)
+        assert st == 0 and st2 == 0 and vf == 0
+
+    def step(self):
+        """One checkpoint + restore of every allocation; returns seconds."""
+        import threading
+        t0 = time.perf_counter()
+        ths = [threading.Thread(target=self._one, args=(g,)) for g in self.groups]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        return time.perf_counter() - t0
+
+    def step_one_thread(self, budget_s):
+        """The single-instance rate: groups one after another on one thread for ~budget_s."""
+        t0, done = time.perf_counter(), 0
+        for g in sorted(self.groups, key=len):
+            self._one(g)
+            done += sum(self.sizes[a] for a in g)
+            if time.perf_counter() - t0 >= budget_s:
+                break
+        return done, time.perf_counter() - t0
+
+
+def _host_threads():
+    return max(1, min(len(os.sched_getaffinity(0)), 32))
+
+
 def cpu_baseline(args, budget_s=15.0):
-    """The oracle as it stands (plain C, single-threaded, Sarwate CRC) on a
-    bounded sample of the same workload: a prefix of its allocations,
-    checkpoint + restore into a poisoned copy, repeated for ~budget_s: half on
-    1 thread, half on every host core (one oracle instance per thread)."""
-    import numpy as np
-    from oracle import oracle
+    """the oracle as it stands timed on this box's host cores
+    (rank 0, N=1): one pass over the WHOLE workload on T threads (T = the
+    cores this process may use), repeated within budget_s, plus the
+    single-thread rate on part of it."""
     from paper_2502_16631_b200 import synth
     w = synth.make_workload(args.config, rank=0, page_size=args.page_size, gib=args.gib)
-    cap = 256 << 20
-    idx, tot = [], 0
-    for a, s in enumerate(w.allocs):
-        if tot + s.nbytes > cap and idx:
-            continue
-        idx.append(a)
-        tot += s.nbytes
-        if tot >= cap:
-            break
-    cont = [w.cpu_bytes(a) for a in idx]
-    reg = [(a + 1, 0x7F0000000000 + (a << 32), w.allocs[a].nbytes) for a in idx]
-    sizes = [w.allocs[a].nbytes for a in idx]
-
-    def loop(budget, out):
-        done, t0, reps = 0, time.perf_counter(), 0
-        while True:
-            st, s = oracle.checkpoint(w.page_size, reg, cont)
-            tgt = [np.full(n, 0xA5, np.uint8) for n in sizes]
-            st2, vf, _ = oracle.restore([s], w.page_size, sizes, tgt)
-            assert st == 0 and st2 == 0 and vf == 0
-            done += tot
-            reps += 1
-            if time.perf_counter() - t0 >= budget:
-                break
-        out.append((done, reps))
-
-    # SURVEY §8(d) d.5: T = 1, then T = the host's cores, each thread running
-    # the unmodified single-threaded oracle on its own copy of the sample
-    # (ctypes releases the GIL inside the C calls)
-    import threading
-    one = []
-    t0 = time.perf_counter()
-    loop(budget_s / 2, one)
-    v1 = one[0][0] / (time.perf_counter() - t0) / 1e9
-    T = max(1, min(os.cpu_count() or 1, 32))
-    outs = []
-    ths = [threading.Thread(target=loop, args=(budget_s / 2, outs)) for _ in range(T)]
-    t0 = time.perf_counter()
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    vT = sum(d for d, _ in outs) / (time.perf_counter() - t0) / 1e9
-    reps = one[0][1] + sum(r for _, r in outs)
-    return {"value": round(vT, 4), "unit": "GB/s", "cores": T, "kind": "oracle", "value_1thread": round(v1, 4),
-            "sample": f"{len(idx)} of {len(w.allocs)} allocations ({tot} B) of {args.config}, checkpoint+restore "
-                      f"x{reps} ({one[0][1]} on 1 thread, then {T} threads concurrently)"}
+    T = _host_threads()
+    ow = OracleWorkload(w, T)
+    times = [ow.step()]
+    while sum(times) < budget_s * 0.75:
+        times.append(ow.step())
+    done1, t1 = ow.step_one_thread(budget_s * 0.25)
+    v = ow.bytes * len(times) / sum(times) / 1e9
+    return {"value": round(v, 4), "unit": "GB/s", "cores": len(ow.groups), "kind": "oracle",
+            "value_1thread": round(done1 / t1 / 1e9, 4),
+            "sample": f"the whole {args.config} workload ({ow.bytes} B, {len(w.allocs)} allocations) partitioned "
+                      f"over {len(ow.groups)} threads (one oracle instance each), checkpoint + restore with verify, "
+                      f"x{len(times)}; value_1thread: {done1} B on one thread"}
 
 
 def run_reference(args):
-    world, rank, local, pg = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0, None
-    if rank != 0:
+    """--impl reference: the CPU oracle on our arm's config, metric and unit
+    (the paper ships no runnable code).  Never imports the product package's
+    libgcr binding.  Under torchrun only rank 0 runs; the others exit 0."""
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    import numpy as np  # noqa: F401
+    from paper_2502_16631_b200 import synth  # the harness generator (no method arithmetic)
+    w = synth.make_workload(args.config, rank=0, page_size=args.page_size, gib=args.gib)
+    T = _host_threads()
+    ow = OracleWorkload(w, T)
     for _ in range(args.warmup):
-        pass
-    budget = max(3.0, min(30.0, 120.0 / max(1, args.steps)))
-    vals = []
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(args, budget_s=budget))
-    v = statistics.median(x["value"] for x in vals)
+        ow.step()
+    times = [ow.step() for _ in range(args.steps)]
+    v = ow.bytes * len(times) / sum(times) / 1e9
     res = {"impl": "reference", "metric": "checkpoint & restore GB/s per GPU and box-aggregate at 1/2/4/8 B200 vs roofline",
-           "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "value": round(v, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(sum(times) / len(times) * 1e3, 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-           "data": "synthetic", "config": {"workload": args.config + " (bounded sample; see cpu_baseline.sample)"},
-           "cpu_baseline": {**vals[0], "value": v},
-           "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "note": "the plain CPU oracle (oracle/gcr_oracle.c) as it stands; the paper ships no runnable code"}
+           "data": "synthetic (seeded counter-based generator; the same bytes as our arm)",
+           "config": {"workload": _workload_desc(args.config, w), "registered_bytes_per_rank": ow.bytes,
+                      "allocations": len(w.allocs), "page_size": w.page_size, "same_config": True},
+           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": len(ow.groups), "kind": "oracle",
+                            "sample": f"the whole {args.config} workload, {args.steps} steps of checkpoint + restore "
+                                      f"with verify, {len(ow.groups)} threads (one oracle instance each)"},
+           "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "the plain CPU oracle (oracle/gcr_oracle.c) as it stands; the paper ships no runnable code",
+           "repo_libs_loaded": _repo_libs_loaded()}
     print(json.dumps(res), flush=True)
+
+
+def _repo_libs_loaded():
+    """Shared objects of this repo mapped into the process (evidence of which
+    native code ran: the reference arm maps only oracle/liboracle.so)."""
+    try:
+        return sorted({os.path.relpath(l.split()[-1], ROOT) for l in open("/proc/self/maps")
+                       if l.rstrip().endswith(".so") and l.split()[-1].startswith(ROOT)})
+    except OSError:
+        return None
 
 
 def main():
@@ -512,6 +676,7 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launch the ranks and report them; no GPU work")
     ap.add_argument("--storage", default=None, help="full mode: directory for the f3 storage tier round trip")
     ap.add_argument("--release", action="store_true",
                     help="full mode: state in releasable gcr_mem_alloc memory; each step releases the HBM after "
@@ -521,13 +686,12 @@ def main():
         ap.error("--storage needs --mode full")
     if args.release and args.mode != "full":
         ap.error("--release needs --mode full (the restore re-maps the released memory)")
-    if args.direct_min_mb is None:
-        from paper_2502_16631_b200 import gcr as _g
-        args.direct_min_mb = _g.default_config().direct_min_bytes / (1 << 20)
     if args.gib is None:
         args.gib = {"C4": 40, "C5": 16}.get(args.config, 16)
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     else:
         run_ours(args)
 

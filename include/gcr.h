@@ -305,6 +305,16 @@ gcr_status gcr_get_stats(const gcr_ctx *ctx, gcr_stats *out);
  * caller bracket calls with its own CUDA events.  Not owned by the caller. */
 gcr_status gcr_ctx_stream(const gcr_ctx *ctx, void **cuda_stream_out);
 
+/* Host-link roofline probe (SURVEY §8(d) d.2 BW_d2h / BW_h2d) over the SAME
+ * pinned memory images use: takes the pinned pool's first free range of
+ * `bytes` (where the next image's data buffer lands; grows the pool if none),
+ * times 3 copies between it and staging slot 0 in each direction on copy
+ * stream 0 with CUDA events (after one warm-up copy), and returns the GB/s
+ * (1e9 B/s).  Any phase; nothing else may run on the ctx meanwhile.
+ * GCR_E_INVAL (null outputs, bytes == 0 or > chunk_bytes), GCR_E_NOMEM,
+ * GCR_E_CUDA. */
+gcr_status gcr_probe_link(gcr_ctx *ctx, uint64_t bytes, double *d2h_gbs, double *h2d_gbs);
+
 /* Message of the last failed call on ctx ("" if none).  Owned by ctx. */
 const char *gcr_last_error(const gcr_ctx *ctx);
 

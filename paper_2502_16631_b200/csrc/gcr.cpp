@@ -1733,6 +1733,43 @@ gcr_status gcr_release(gcr_ctx *c) {
     return s;
 }
 
+gcr_status gcr_probe_link(gcr_ctx *c, uint64_t bytes, double *d2h_gbs, double *h2d_gbs) {
+    if (!c) return GCR_E_INVAL;
+    if (!d2h_gbs || !h2d_gbs || bytes == 0 || bytes > c->cfg.chunk_bytes || c->slots.empty())
+        return fail(c, GCR_E_INVAL, "probe_link: null output, or bytes not in (0, chunk_bytes]");
+    *d2h_gbs = *h2d_gbs = 0.0;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    sync_all(c);
+    // the pool's first free range of `bytes`: where the next image's data lands
+    void *h = c->pool.alloc(bytes);
+    if (!h) return fail(c, GCR_E_NOMEM, "probe_link: pinned pool allocation failed");
+    gcr_status st = GCR_OK;
+    cudaStream_t cs = c->copy[0];
+    for (int dir = 0; dir < 2 && st == GCR_OK; dir++) {
+        cudaEvent_t e0 = c->ev(), e1 = c->ev();
+        auto copy = [&]() {
+            return dir == 0 ? cudaMemcpyAsync(h, c->slots[0], bytes, cudaMemcpyDeviceToHost, cs)
+                            : cudaMemcpyAsync(c->slots[0], h, bytes, cudaMemcpyHostToDevice, cs);
+        };
+        cudaError_t e = copy();  // warm-up
+        if (e == cudaSuccess) e = cudaEventRecord(e0, cs);
+        for (int r = 0; r < 3 && e == cudaSuccess; r++) e = copy();
+        if (e == cudaSuccess) e = cudaEventRecord(e1, cs);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        float ms = 0.f;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            st = fail(c, GCR_E_CUDA, std::string("probe_link: ") + cudaGetErrorString(e));
+            break;
+        }
+        (dir == 0 ? *d2h_gbs : *h2d_gbs) = 3.0 * (double)bytes / (ms * 1e-3) / 1e9;
+    }
+    c->ev_used = 0;
+    c->pool.release(h, bytes);
+    return st;
+}
+
 gcr_status gcr_get_phase(const gcr_ctx *c, gcr_phase *out) {
     if (!c || !out) return GCR_E_INVAL;
     *out = c->phase;

@@ -89,6 +89,7 @@ _SIGS = {
     "gcr_mem_free": [_vp, _u64],
     "gcr_release": [_vp],
     "gcr_checkpoint_abort": [_vp, _vp],
+    "gcr_probe_link": [_vp, _u64, _P(C.c_double), _P(C.c_double)],
     "gcr_image_header": [_vp, _P(gcr_image_hdr)],
     "gcr_image_allocs": [_vp, _P(_P(gcr_alloc_rec)), _P(_u32)],
     "gcr_image_pagemap": [_vp, _P(_P(gcr_pagemap_entry)), _P(_u64)],
@@ -329,6 +330,12 @@ class Context:
         out = C.c_void_p()
         self._check(gcr_image_read_file(self.h, os.fsencode(path), threads, C.byref(out)))
         return Image(self, out.value)
+
+    def probe_link(self, nbytes: int = 1 << 30):
+        """(D2H GB/s, H2D GB/s) between the image pool and a staging slot."""
+        d, h = C.c_double(), C.c_double()
+        self._check(gcr_probe_link(self.h, nbytes, C.byref(d), C.byref(h)))
+        return d.value, h.value
 
     def last_error(self) -> str:
         return gcr_last_error(self.h).decode()

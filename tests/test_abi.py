@@ -23,7 +23,7 @@ def built():
 
 def test_gcr_exports_every_declared_symbol(built):
     names = _declared("gcr.h")
-    assert len(names) == 30
+    assert len(names) == 31
     lib = ctypes.CDLL(built["libgcr.so"])
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
@@ -66,5 +66,7 @@ def test_null_handles(built):
     assert gcr.gcr_lock(None) == gcr.GCR_E_INVAL
     assert gcr.gcr_image_free(None) == gcr.GCR_E_INVAL
     assert gcr.gcr_release(None) == gcr.GCR_E_INVAL
+    assert gcr.gcr_checkpoint_abort(None, None) == gcr.GCR_E_INVAL
+    assert gcr.gcr_probe_link(None, 1 << 20, None, None) == gcr.GCR_E_INVAL
     assert gcr.gcr_mem_free(None, 0) == gcr.GCR_E_INVAL
     assert gcr.gcr_mem_alloc(None, 1 << 20, None) == gcr.GCR_E_INVAL
