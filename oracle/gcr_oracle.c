@@ -16,7 +16,7 @@
  * the operation; CRIU's page-granular memory dump ("pages scanned", P:432,
  * §5.3) and incremental/differential checkpointing (§7) name the
  * page scan and the dirty diff.  The paper prints no digest, page count or
- * byte of any image, so every rule here is the DESIGN.md reading (R-1..R-18)
+ * byte of any image, so every rule here is the DESIGN.md reading (R-1..R-19)
  * and each one is pinned in tests/test_oracle_*.py against something other
  * than this file: RFC 3720 B.4 CRC32C vectors, the x86 SSE4.2 crc32
  * instruction, closed forms Z(n), brute force on tiny registries,
@@ -124,6 +124,154 @@ static int valid_page_size(uint32_t P) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* f4 PAGE CODEC -- "data compression ... could further improve the efficiency
+ * of checkpoint/restore operations" (§5.2; §7).  The paper names
+ * the technique only; the code below is DESIGN.md reading R-19 ("byte-plane
+ * dictionary code"), written out step by step:
+ *
+ *  A PRESENT page of L bytes (L % 16 == 0) is n = L/4 little-endian 32-bit
+ *  words x_0..x_{n-1}.  Plane k (k = 0..3) is the sequence of byte k of every
+ *  word.  For each plane: D_k = its distinct byte values in ascending order,
+ *  d_k = |D_k|, b_k = ceil(log2 d_k) (0 when d_k == 1); packed section size
+ *  S_p = pad16(d_k) + pad16(ceil(n*b_k/8)), raw section size S_r = pad16(n);
+ *  mode_k = b_k if d_k <= 128 and S_p < S_r, else 8 (raw).
+ *  Coded page = 16-byte header (byte k = mode_k; byte 4+k = d_k - 1 for a
+ *  packed plane, 0 for a raw one; bytes 8..15 = 0) followed by the four plane
+ *  sections in order: raw = the n plane bytes zero-padded to 16; packed = D_k
+ *  zero-padded to 16, then code(i) = rank of plane value i in D_k as a b_k-bit
+ *  field at bit position i*b_k (bit j of section byte m is bit 8m+j: LSB
+ *  first), zero-padded to 16.  The page is stored coded iff its coded length C
+ *  is < L, else raw: stored length == L <=> raw.
+ *  Decoding a coded page: a MALFORMED header (a mode > 8; a raw plane with
+ *  byte 4+k != 0; a packed plane with d_k > 128 or b_k != ceil(log2 d_k); a
+ *  non-zero byte 8..15; section sizes not summing to the stored length)
+ *  restores the page as zero bytes; a code >= d_k restores byte 0.  (Both
+ *  sides implement this, so corrupted images restore identically; the
+ *  restore's verify reports such pages.)                                     */
+static uint64_t pad16(uint64_t x) { return (x + 15u) / 16u * 16u; }
+
+static uint32_t ceil_log2(uint32_t d) {
+    uint32_t b = 0;
+    while ((1u << b) < d) b++;
+    return b;
+}
+
+/* modes / dictionary sizes of a page's four planes; returns the coded length C */
+static uint64_t orc_plan_page(const uint8_t *page, uint64_t len, uint8_t present[4][256], uint32_t d[4],
+                              uint32_t mode[4]) {
+    uint64_t n = len / 4, C = 16;
+    for (int k = 0; k < 4; k++) {
+        memset(present[k], 0, 256);
+        for (uint64_t i = 0; i < n; i++) present[k][page[4 * i + k]] = 1;
+        d[k] = 0;
+        for (int v = 0; v < 256; v++) d[k] += present[k][v];
+        uint32_t b = ceil_log2(d[k]);
+        uint64_t sp = pad16(d[k]) + pad16((n * b + 7) / 8), sr = pad16(n);
+        if (d[k] <= 128 && sp < sr) {
+            mode[k] = b;
+            C += sp;
+        } else {
+            mode[k] = 8;
+            C += sr;
+        }
+    }
+    return C;
+}
+
+/* Stored form of one page into out (capacity >= len); returns its length. */
+uint64_t orc_encode_page(const uint8_t *page, uint64_t len, uint8_t *out) {
+    uint8_t present[4][256];
+    uint32_t d[4], mode[4];
+    uint64_t n = len / 4;
+    uint64_t C = orc_plan_page(page, len, present, d, mode);
+    if (C >= len) {  /* raw */
+        memcpy(out, page, len);
+        return len;
+    }
+    memset(out, 0, C);
+    for (int k = 0; k < 4; k++) {
+        out[k] = (uint8_t)mode[k];
+        out[4 + k] = mode[k] < 8 ? (uint8_t)(d[k] - 1) : 0;
+    }
+    uint64_t o = 16;
+    for (int k = 0; k < 4; k++) {
+        if (mode[k] == 8) {
+            for (uint64_t i = 0; i < n; i++) out[o + i] = page[4 * i + k];
+            o += pad16(n);
+            continue;
+        }
+        uint8_t rank[256];
+        uint32_t r = 0;
+        for (int v = 0; v < 256; v++)
+            if (present[k][v]) {
+                out[o + r] = (uint8_t)v; /* dictionary, ascending */
+                rank[v] = (uint8_t)r++;
+            }
+        o += pad16(d[k]);
+        uint32_t b = mode[k];
+        for (uint64_t i = 0; i < n; i++) {
+            uint32_t code = rank[page[4 * i + k]];
+            for (uint32_t j = 0; j < b; j++) {
+                uint64_t pos = i * b + j;
+                out[o + pos / 8] |= (uint8_t)(((code >> j) & 1u) << (pos % 8));
+            }
+        }
+        o += pad16((n * b + 7) / 8);
+    }
+    return C;
+}
+
+/* Inverse of orc_encode_page: `stored` bytes (stored == len: raw) -> page. */
+void orc_decode_page(const uint8_t *src, uint64_t stored, uint8_t *page, uint64_t len) {
+    if (stored == len) {
+        memcpy(page, src, len);
+        return;
+    }
+    uint64_t n = len / 4;
+    int malformed = stored < 16;
+    uint64_t o = 16;
+    uint64_t off[4];
+    for (int k = 0; k < 4 && !malformed; k++) {
+        uint32_t m = src[k], dm1 = src[4 + k];
+        off[k] = o;
+        if (m > 8) malformed = 1;
+        else if (m == 8) {
+            if (dm1 != 0) malformed = 1;
+            o += pad16(n);
+        } else {
+            uint32_t dk = dm1 + 1;
+            if (dk > 128 || ceil_log2(dk) != m) malformed = 1;
+            o += pad16(dk) + pad16((n * m + 7) / 8);
+        }
+    }
+    for (int j = 8; j < 16 && !malformed; j++)
+        if (src[j] != 0) malformed = 1;
+    if (!malformed && o != stored) malformed = 1;
+    if (malformed) {
+        memset(page, 0, len);
+        return;
+    }
+    for (int k = 0; k < 4; k++) {
+        uint32_t m = src[k];
+        const uint8_t *sec = src + off[k];
+        if (m == 8) {
+            for (uint64_t i = 0; i < n; i++) page[4 * i + k] = sec[i];
+            continue;
+        }
+        uint32_t dk = (uint32_t)src[4 + k] + 1;
+        const uint8_t *codes = sec + pad16(dk);
+        for (uint64_t i = 0; i < n; i++) {
+            uint32_t code = 0;
+            for (uint32_t j = 0; j < m; j++) {
+                uint64_t pos = i * m + j;
+                code |= (uint32_t)((codes[pos / 8] >> (pos % 8)) & 1u) << j;
+            }
+            page[4 * i + k] = code < dk ? sec[code] : 0;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* CHECKPOINT.
  *
  * Inputs: the registry in registration order (alloc_id[a], vaddr[a],
@@ -137,12 +285,12 @@ static int valid_page_size(uint32_t P) {
  * Also, if digests_out != NULL, the new parent digest table (c.1 step 9),
  * which is the digest table in the stream.
  */
-int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
-                   const uint64_t *vaddr, const uint64_t *bytes,
-                   const uint8_t *const *contents, int mode,
-                   const uint32_t *d_prev, uint64_t n_prev,
-                   uint64_t generation, uint64_t parent_generation,
-                   uint8_t **out, uint64_t *out_len) {
+int orc_checkpoint_ex(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
+                      const uint64_t *vaddr, const uint64_t *bytes,
+                      const uint8_t *const *contents, int mode,
+                      const uint32_t *d_prev, uint64_t n_prev,
+                      uint64_t generation, uint64_t parent_generation, int compress,
+                      uint8_t **out, uint64_t *out_len) {
     orc_init_table();
     *out = NULL;
     *out_len = 0;
@@ -157,7 +305,9 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
 
     uint32_t *D = (uint32_t *)malloc(n_pages * sizeof(uint32_t));
     uint8_t *cls = (uint8_t *)malloc(n_pages);
-    if (!D || !cls) { free(D); free(cls); return ORC_E_NOMEM; }
+    uint64_t *stored = (uint64_t *)malloc(n_pages * sizeof(uint64_t)); /* f4: stored length per page */
+    uint8_t *scratch = (uint8_t *)malloc(P);
+    if (!D || !cls || !stored || !scratch) { free(D); free(cls); free(stored); free(scratch); return ORC_E_NOMEM; }
 
     /* steps 3-5: digest, zero test, classify every page */
     uint64_t g = 0, n_present = 0, n_zero = 0, n_parent = 0, image_bytes = 0;
@@ -169,7 +319,13 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
                             mode == ORC_INCREMENTAL ? d_prev[g] : 0u, &D[g], &cls[g]);
             if (cls[g] == ORC_CLASS_ZERO) n_zero++;
             else if (cls[g] == ORC_CLASS_PARENT) n_parent++;
-            else { n_present++; image_bytes += len; }
+            else {
+                n_present++;
+                /* step 6 with f4 (R-19): the page's stored form is its coded
+                 * form if shorter, else its raw bytes */
+                stored[g] = compress ? orc_encode_page(contents[a] + p * (uint64_t)P, len, scratch) : len;
+                image_bytes += stored[g];
+            }
         }
     }
 
@@ -183,11 +339,12 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
             if (p == 0 || cls[g] != cls[g - 1]) n_entries++;
     }
 
+    /* f4: one u32 stored length per PRESENT page after the digests (R-19) */
     uint64_t meta_bytes = ORC_HEADER_BYTES + (uint64_t)ORC_ALLOC_REC_BYTES * n_allocs +
-                          ORC_PAGEMAP_ENTRY_BYTES * n_entries + 4u * n_pages;
+                          ORC_PAGEMAP_ENTRY_BYTES * n_entries + 4u * n_pages + (compress ? 4u * n_present : 0u);
     uint64_t total = meta_bytes + image_bytes;
     uint8_t *s = (uint8_t *)calloc(total ? total : 1, 1);
-    if (!s) { free(D); free(cls); return ORC_E_NOMEM; }
+    if (!s) { free(D); free(cls); free(stored); free(scratch); return ORC_E_NOMEM; }
 
     /* alloc table: {u64 vaddr; u64 bytes; u32 alloc_id; u32 reserved=0} */
     uint8_t *at = s + ORC_HEADER_BYTES;
@@ -219,9 +376,16 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
     uint8_t *dg = pm + ORC_PAGEMAP_ENTRY_BYTES * n_entries;
     for (uint64_t i = 0; i < n_pages; i++) put_u32(dg + 4u * i, D[i]);
 
+    /* f4 stored lengths, PRESENT pages in g order */
+    uint8_t *cs = dg + 4u * n_pages;
+    if (compress) {
+        uint64_t i = 0;
+        for (uint64_t q = 0; q < n_pages; q++)
+            if (cls[q] == ORC_CLASS_PRESENT) put_u32(cs + 4u * i++, (uint32_t)stored[q]);
+    }
     /* step 6: image data = concatenation in g order of PRESENT pages, true
-     * lengths, no padding */
-    uint8_t *data = dg + 4u * n_pages;
+     * lengths, no padding (f4: each page's stored form) */
+    uint8_t *data = cs + (compress ? 4u * n_present : 0u);
     uint64_t cur = 0;
     g = 0;
     for (uint32_t a = 0; a < n_allocs; a++) {
@@ -229,8 +393,11 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
         for (uint64_t p = 0; p < m; p++, g++) {
             if (cls[g] != ORC_CLASS_PRESENT) continue;
             uint64_t len = page_len(bytes[a], P, p);
-            memcpy(data + cur, contents[a] + p * (uint64_t)P, len);
-            cur += len;
+            if (compress) cur += orc_encode_page(contents[a] + p * (uint64_t)P, len, data + cur);
+            else {
+                memcpy(data + cur, contents[a] + p * (uint64_t)P, len);
+                cur += len;
+            }
         }
     }
 
@@ -242,7 +409,7 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
     put_u64(s + 16, generation);
     put_u64(s + 24, mode == ORC_INCREMENTAL ? parent_generation : 0);
     put_u32(s + 32, n_allocs);
-    put_u32(s + 36, mode == ORC_INCREMENTAL ? 1u : 0u);
+    put_u32(s + 36, (mode == ORC_INCREMENTAL ? 1u : 0u) | (compress ? 2u : 0u)); /* bit1: f4 coded */
     put_u64(s + 40, n_pages);
     put_u64(s + 48, n_present);
     put_u64(s + 56, n_zero);
@@ -255,9 +422,21 @@ int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
 
     free(D);
     free(cls);
+    free(stored);
+    free(scratch);
     *out = s;
     *out_len = total;
     return ORC_OK;
+}
+
+int orc_checkpoint(uint32_t P, uint32_t n_allocs, const uint32_t *alloc_id,
+                   const uint64_t *vaddr, const uint64_t *bytes,
+                   const uint8_t *const *contents, int mode,
+                   const uint32_t *d_prev, uint64_t n_prev,
+                   uint64_t generation, uint64_t parent_generation,
+                   uint8_t **out, uint64_t *out_len) {
+    return orc_checkpoint_ex(P, n_allocs, alloc_id, vaddr, bytes, contents, mode, d_prev, n_prev, generation,
+                             parent_generation, 0, out, out_len);
 }
 
 void orc_free(void *p) { free(p); }
@@ -270,7 +449,7 @@ typedef struct {
     uint32_t page_size, n_allocs, flags;
     uint64_t generation, parent_generation, n_pages, n_present, n_zero, n_parent, n_entries,
         image_bytes;
-    const uint8_t *allocs, *pagemap, *digests, *data;
+    const uint8_t *allocs, *pagemap, *digests, *stored, *data; /* stored: f4 lengths or NULL */
 } orc_view;
 
 /* Validation, first part of c.2 step 1: framing, magic and meta CRC
@@ -292,8 +471,10 @@ static int orc_parse(const uint8_t *s, uint64_t len, orc_view *v) {
     v->n_entries = get_u64(s + 72);
     v->image_bytes = get_u64(s + 80);
     /* declared sizes must frame the stream exactly (guard overflow first) */
-    if (v->n_pages > len / 4 || v->n_entries > len / 16 || v->n_allocs > len / 24) return ORC_E_CORRUPT;
-    uint64_t meta = ORC_HEADER_BYTES + 24ull * v->n_allocs + 16ull * v->n_entries + 4ull * v->n_pages;
+    if (v->n_pages > len / 4 || v->n_entries > len / 16 || v->n_allocs > len / 24 || v->n_present > len / 4)
+        return ORC_E_CORRUPT;
+    uint64_t meta = ORC_HEADER_BYTES + 24ull * v->n_allocs + 16ull * v->n_entries + 4ull * v->n_pages +
+                    ((v->flags & 2u) ? 4ull * v->n_present : 0ull);
     if (meta > len || len - meta != v->image_bytes) return ORC_E_CORRUPT;
     /* meta CRC with the field itself taken as 0 */
     uint32_t stored = get_u32(s + 88);
@@ -304,11 +485,12 @@ static int orc_parse(const uint8_t *s, uint64_t len, orc_view *v) {
     uint32_t st = orc_crc32c_update(0xFFFFFFFFu, hdr, ORC_HEADER_BYTES);
     st = orc_crc32c_update(st, s + ORC_HEADER_BYTES, meta - ORC_HEADER_BYTES);
     if ((st ^ 0xFFFFFFFFu) != stored) return ORC_E_CORRUPT;
-    if (get_u32(s + 8) != ORC_VERSION) return ORC_E_VERSION;
+    if (get_u32(s + 8) != ORC_VERSION || (v->flags & ~3u) != 0) return ORC_E_VERSION; /* unknown flag bits */
     v->allocs = s + ORC_HEADER_BYTES;
     v->pagemap = v->allocs + 24ull * v->n_allocs;
     v->digests = v->pagemap + 16ull * v->n_entries;
-    v->data = v->digests + 4ull * v->n_pages;
+    v->stored = (v->flags & 2u) ? v->digests + 4ull * v->n_pages : NULL;
+    v->data = v->digests + 4ull * v->n_pages + ((v->flags & 2u) ? 4ull * v->n_present : 0ull);
     return ORC_OK;
 }
 
@@ -317,7 +499,7 @@ static int orc_parse(const uint8_t *s, uint64_t len, orc_view *v) {
  * at the run's first page, flags one of the three, counts and data length
  * consistent with the header.  Anything else is CORRUPT. */
 static int orc_check_pagemap(const orc_view *v) {
-    uint64_t e = 0, npres = 0, nzero = 0, npar = 0, bytes_present = 0;
+    uint64_t e = 0, npres = 0, nzero = 0, npar = 0, bytes_present = 0, bytes_stored = 0;
     uint32_t P = v->page_size;
     if (!valid_page_size(P)) return ORC_E_CORRUPT;
     uint64_t total_pages = 0;
@@ -335,7 +517,17 @@ static int orc_check_pagemap(const orc_view *v) {
             if (eva != va + p * (uint64_t)P || nr == 0 || p + nr > m) return ORC_E_CORRUPT;
             if (fl != ORC_PE_PRESENT && fl != ORC_PE_ZERO && fl != ORC_PE_PARENT) return ORC_E_CORRUPT;
             for (uint64_t q = p; q < p + nr; q++) {
-                if (fl == ORC_PE_PRESENT) { npres++; bytes_present += page_len(by, P, q); }
+                if (fl == ORC_PE_PRESENT) {
+                    uint64_t L = page_len(by, P, q);
+                    bytes_present += L;
+                    if (v->stored) { /* f4: raw (== L) or a coded form, a multiple of 16 shorter than L */
+                        if (npres >= v->n_present) return ORC_E_CORRUPT;
+                        uint64_t st = get_u32(v->stored + 4ull * npres);
+                        if (st > L || (st != L && (st % 16 != 0 || st < 16))) return ORC_E_CORRUPT;
+                        bytes_stored += st;
+                    }
+                    npres++;
+                }
                 else if (fl == ORC_PE_ZERO) nzero++;
                 else npar++;
             }
@@ -345,7 +537,7 @@ static int orc_check_pagemap(const orc_view *v) {
     }
     if (e != v->n_entries || total_pages != v->n_pages) return ORC_E_CORRUPT;
     if (npres != v->n_present || nzero != v->n_zero || npar != v->n_parent) return ORC_E_CORRUPT;
-    if (bytes_present != v->image_bytes) return ORC_E_CORRUPT;
+    if ((v->stored ? bytes_stored : bytes_present) != v->image_bytes) return ORC_E_CORRUPT;
     return ORC_OK;
 }
 
@@ -392,7 +584,7 @@ int orc_restore(const uint8_t *const *streams, const uint64_t *lens, uint32_t n_
     /* step 2: apply in chain order */
     for (uint32_t k = 0; k < n_images; k++) {
         const orc_view *v = &views[k];
-        uint64_t e = 0, cursor = 0;
+        uint64_t e = 0, cursor = 0, ip = 0; /* ip: ordinal of the next PRESENT page */
         for (uint32_t a = 0; a < n_allocs; a++) {
             uint64_t m = pages_of(bytes[a], P);
             uint64_t p = 0;
@@ -402,7 +594,12 @@ int orc_restore(const uint8_t *const *streams, const uint64_t *lens, uint32_t n_
                 for (uint64_t q = p; q < p + nr; q++) {
                     uint64_t len = page_len(bytes[a], P, q);
                     uint8_t *dst = contents[a] + q * (uint64_t)P;
-                    if (fl == ORC_PE_PRESENT) { memcpy(dst, v->data + cursor, len); cursor += len; }
+                    if (fl == ORC_PE_PRESENT) {
+                        uint64_t st = v->stored ? get_u32(v->stored + 4ull * ip) : len;
+                        orc_decode_page(v->data + cursor, st, dst, len); /* raw when st == len */
+                        cursor += st;
+                        ip++;
+                    }
                     else if (fl == ORC_PE_ZERO) memset(dst, 0, len);
                     /* PARENT: skip */
                 }

@@ -52,6 +52,14 @@ def lib():
         L.orc_checkpoint.argtypes = [C.c_uint32, C.c_uint32, u32p, u64p, u64p, C.POINTER(C.c_void_p),
                                      C.c_int, u32p, C.c_uint64, C.c_uint64, C.c_uint64,
                                      C.POINTER(C.c_void_p), u64p]
+        L.orc_checkpoint_ex.restype = C.c_int
+        L.orc_checkpoint_ex.argtypes = [C.c_uint32, C.c_uint32, u32p, u64p, u64p, C.POINTER(C.c_void_p),
+                                        C.c_int, u32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                        C.POINTER(C.c_void_p), u64p]
+        L.orc_encode_page.restype = C.c_uint64
+        L.orc_encode_page.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+        L.orc_decode_page.restype = None
+        L.orc_decode_page.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]
         L.orc_restore.restype = C.c_int
         L.orc_restore.argtypes = [C.POINTER(C.c_void_p), u64p, C.c_uint32, C.c_uint32, C.c_uint32, u64p,
                                   C.POINTER(C.c_void_p), u64p, u64p]
@@ -81,12 +89,28 @@ def page_record(page: np.ndarray, mode: int = FULL, d_prev: int = 0):
     return d.value, c.value
 
 
+def encode_page(page) -> bytes:
+    """f4 stored form of one page (R-19): the coded form if shorter, else raw."""
+    page = np.ascontiguousarray(page).view(np.uint8)
+    out = np.zeros(max(page.size, 16), np.uint8)
+    n = lib().orc_encode_page(C.c_void_p(_ptr(page)), page.size, C.c_void_p(_ptr(out)))
+    return out[:n].tobytes()
+
+
+def decode_page(stored: bytes, length: int) -> np.ndarray:
+    src = np.frombuffer(bytes(stored) + b"\0", dtype=np.uint8)
+    out = np.zeros(length, np.uint8)
+    lib().orc_decode_page(C.c_void_p(_ptr(src)), len(stored), C.c_void_p(_ptr(out)), length)
+    return out
+
+
 def checkpoint(page_size: int, registry, contents, mode: int = FULL, d_prev=None,
-               generation: int = 1, parent_generation: int = 0):
+               generation: int = 1, parent_generation: int = 0, compress: bool = False):
     """Canonical image stream (bytes) of the registry.
 
     registry: list of (alloc_id, vaddr, nbytes); contents: list of uint8 numpy
-    arrays (len == nbytes each).  Returns (status, stream_bytes or None)."""
+    arrays (len == nbytes each).  compress: f4 stored forms (R-19).
+    Returns (status, stream_bytes or None)."""
     n = len(registry)
     ids = np.array([r[0] for r in registry], dtype=np.uint32)
     va = np.array([r[1] for r in registry], dtype=np.uint64)
@@ -100,10 +124,10 @@ def checkpoint(page_size: int, registry, contents, mode: int = FULL, d_prev=None
         dpp, ndp = None, 0
     out = C.c_void_p()
     out_len = C.c_uint64()
-    st = lib().orc_checkpoint(page_size, n, ids.ctypes.data_as(C.POINTER(C.c_uint32)),
-                              va.ctypes.data_as(C.POINTER(C.c_uint64)), by.ctypes.data_as(C.POINTER(C.c_uint64)),
-                              ptrs, mode, dpp, ndp, generation, parent_generation,
-                              C.byref(out), C.byref(out_len))
+    st = lib().orc_checkpoint_ex(page_size, n, ids.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                 va.ctypes.data_as(C.POINTER(C.c_uint64)), by.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                 ptrs, mode, dpp, ndp, generation, parent_generation, 1 if compress else 0,
+                                 C.byref(out), C.byref(out_len))
     if st != OK:
         return st, None
     try:
@@ -148,6 +172,9 @@ def parse(stream: bytes) -> dict:
     at = np.frombuffer(stream[o:o + 24 * hdr["n_allocs"]], dtype=np.uint8); o += 24 * hdr["n_allocs"]
     pm = np.frombuffer(stream[o:o + 16 * hdr["n_entries"]], dtype=np.uint8); o += 16 * hdr["n_entries"]
     dg = np.frombuffer(stream[o:o + 4 * hdr["n_pages"]], dtype=np.uint32); o += 4 * hdr["n_pages"]
+    stored = None
+    if hdr["flags"] & 2:  # f4: stored length of every PRESENT page
+        stored = np.frombuffer(stream[o:o + 4 * hdr["n_present"]], dtype=np.uint32); o += 4 * hdr["n_present"]
     data = stream[o:]
     pmr = pm.reshape(-1, 16)
     entries = [(int(r[0:8].view(np.uint64)[0]), int(r[8:12].view(np.uint32)[0]), int(r[12:16].view(np.uint32)[0]))
@@ -155,4 +182,4 @@ def parse(stream: bytes) -> dict:
     atr = at.reshape(-1, 24)
     allocs = [(int(r[0:8].view(np.uint64)[0]), int(r[8:16].view(np.uint64)[0]), int(r[16:20].view(np.uint32)[0]))
               for r in atr]
-    return dict(header=hdr, allocs=allocs, entries=entries, digests=dg, data=data)
+    return dict(header=hdr, allocs=allocs, entries=entries, digests=dg, stored=stored, data=data)
