@@ -264,7 +264,7 @@ def run_ours(args):
 
     w = synth.make_workload(args.config, rank=rank, page_size=args.page_size, gib=args.gib)
     ctx = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20,
-                      n_copy_streams=args.streams, n_staging_slots=args.slots,
+                      n_copy_streams=args.streams, n_staging_slots=args.slots, compress=args.compress,
                       direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
     # --release: the state lives in one releasable gcr_mem_alloc block, carved
     # into the workload's allocations (f2: checkpoint frees the HBM, restore
@@ -423,6 +423,16 @@ def run_ours(args):
         "K8_verify": None if incremental else
         {"dev_ms_per_step": ver_ns / K * 1e-6, "alg_bytes_per_step": R, "GBps": R * K / max(ver_ns, 1)},
     }
+    if args.compress:  # f4: KA + KC read every PRESENT byte, KC writes the stored form; KD the reverse
+        raw_b = sc["present_raw_bytes"]
+        cod_ns = sum(r[0]["codec_dev_ns"] for r in recs)
+        dec_ns = sum(r[1]["decode_dev_ns"] for r in recs)
+        kern["KABC_codec_encode"] = {"dev_ms_per_step": cod_ns / K * 1e-6, "alg_bytes_per_step": 2 * raw_b + img_b,
+                                     "GBps": (2 * raw_b + img_b) * K / max(cod_ns, 1),
+                                     "ratio_stored_over_raw": round(img_b / max(raw_b, 1), 4)}
+        kern["KD_codec_decode"] = None if incremental else {
+            "dev_ms_per_step": dec_ns / K * 1e-6, "alg_bytes_per_step": raw_b + img_b,
+            "GBps": (raw_b + img_b) * K / max(dec_ns, 1)}
     # dominant kernel = k_scan (K1 in scan mode during the checkpoint, K8 =
     # the same kernel in verify mode during the restore): average over all its
     # launches in the timed region of algorithmic bytes per launch / duration.
@@ -458,6 +468,7 @@ def run_ours(args):
         "config": {"workload": _workload_desc(args.config + ("i" if incremental and args.config == "C4" else ""), w),
                    "dirty_fraction": args.dirty if incremental else None, "registered_bytes_per_rank": R,
                    "allocations": len(w.allocs), "page_size": w.page_size, "chunk_bytes": args.chunk_mb << 20,
+                   "compress": "f4 byte-plane dictionary code (R-19)" if args.compress else None,
                    "copy_streams": args.streams, "staging_slots": args.slots or args.streams, "direct_min_bytes": int(args.direct_min_mb * (1 << 20)) if args.direct_min_mb >= 0 else None,
                    "parallelism": f"independent ranks x{world} (gloo control plane)",
                    "l2": "inputs larger than L2 (registered state >> 126 MB; no flush needed)"},
@@ -676,6 +687,8 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--compress", type=int, default=0, choices=[0, 1],
+                    help="1: f4 page codec (PRESENT pages stored in byte-plane dictionary form, GPU encode/decode)")
     ap.add_argument("--dry-run", action="store_true", help="launch the ranks and report them; no GPU work")
     ap.add_argument("--storage", default=None, help="full mode: directory for the f3 storage tier round trip")
     ap.add_argument("--release", action="store_true",

@@ -99,6 +99,14 @@ typedef struct {
                                  efficiency); 0 = every eligible run direct;
                                  UINT64_MAX = every run staged.  The image bytes are identical
                                  either way. */
+    uint32_t compress;        /* 0 (default) = PRESENT pages stored raw; 1 = f4 page codec: every
+                                 PRESENT page is stored in its byte-plane dictionary form when that
+                                 is shorter (R-19; "data compression"), encoded on
+                                 the GPU before the drain and decoded on the GPU after the H2D.
+                                 Digests, classes and the pagemap are unchanged; the image gets a
+                                 stored-length table and header flag bit 1.  All PRESENT data then
+                                 moves through the staging slots (direct_min_bytes is unused). */
+    uint32_t reserved0;       /* 0 */
 } gcr_config;
 
 /* Statistics of the most recent lock / checkpoint / restore / unlock
@@ -135,13 +143,19 @@ typedef struct {
     uint64_t remap_ns;                           /* host: last restore's re-create + re-map (0 if
                                                     the memory was resident) */
     uint64_t released_bytes;                     /* last gcr_release: physical bytes returned */
+    uint64_t present_raw_bytes;                  /* last checkpoint: PRESENT bytes before coding (==
+                                                    image_bytes unless compress) */
+    uint64_t codec_dev_ns;                       /* last checkpoint: f4 plan + offsets + encode kernels */
+    uint64_t decode_dev_ns;                      /* last restore: f4 decode kernels */
 } gcr_stats;
 
 /* gcr_image_hdr -- 96 bytes, offsets: magic 0, version 8, page_size 12,
  * generation 16, parent_generation 24, n_allocs 32, flags 36, n_pages 40,
  * n_present 48, n_zero 56, n_parent 64, n_entries 72, image_bytes 80,
  * meta_crc32c 88, reserved 92.  meta_crc32c = CRC32C over header (with this
- * field 0) || alloc table || pagemap || digests (SPEC S:298 analog).  This is
+ * field 0) || alloc table || pagemap || digests [|| stored lengths, f4]
+ * (SPEC S:298 analog); image_bytes = length of the data section (for an f4
+ * image the sum of the stored lengths).  This is
  * the analog of the paper's inventory flag "contains GPU state". */
 typedef struct {
     char magic[8];               /* "GCRIMG\0\1" */
@@ -150,7 +164,8 @@ typedef struct {
     uint64_t generation;         /* 1, 2, ... per ctx */
     uint64_t parent_generation;  /* 0 for a full image */
     uint32_t n_allocs;
-    uint32_t flags;              /* bit0 = incremental */
+    uint32_t flags;              /* bit0 = incremental, bit1 = f4 coded (stored-length table present);
+                                    other bits: GCR_E_VERSION */
     uint64_t n_pages, n_present, n_zero, n_parent, n_entries, image_bytes;
     uint32_t meta_crc32c;
     uint32_t reserved;           /* 0 */
@@ -324,12 +339,18 @@ gcr_status gcr_image_header(const gcr_image *img, gcr_image_hdr *out);
 gcr_status gcr_image_allocs(const gcr_image *img, const gcr_alloc_rec **p, uint32_t *n);
 gcr_status gcr_image_pagemap(const gcr_image *img, const gcr_pagemap_entry **p, uint64_t *n);
 gcr_status gcr_image_digests(const gcr_image *img, const uint32_t **p, uint64_t *n);
-/* PRESENT page bytes, concatenated in page order (c.1 step 6); pinned host. */
+/* PRESENT page bytes, concatenated in page order (c.1 step 6); pinned host.
+ * For an f4 image (flags bit 1) every page's stored form (R-19). */
 gcr_status gcr_image_data(const gcr_image *img, const uint8_t **p, uint64_t *bytes);
+/* f4 images: the stored length of every PRESENT page, in page order (n =
+ * n_present; raw pages have stored length == page length).  Other images:
+ * *p = NULL, *n = 0. */
+gcr_status gcr_image_stored(const gcr_image *img, const uint32_t **p, uint64_t *n);
 gcr_status gcr_image_free(gcr_image *img);
 
 /* Canonical byte stream = header(96) || alloc table || pagemap || digests ||
- * data: exactly what the oracle writes for the same input. */
+ * [stored lengths, f4 images only] || data: exactly what the oracle writes for
+ * the same input.  meta_crc32c covers everything before the data. */
 gcr_status gcr_image_stream_size(const gcr_image *img, uint64_t *bytes);
 /* Write the stream into caller-owned dst of capacity cap (GCR_E_INVAL if too small). */
 gcr_status gcr_image_serialize(const gcr_image *img, void *dst, uint64_t cap);

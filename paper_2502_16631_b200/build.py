@@ -17,7 +17,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 LIBS = {
     "libgcr.so": (
-        [os.path.join(CSRC, f) for f in ("kernels.cu", "gcr.cpp", "crc_host.cpp")],
+        [os.path.join(CSRC, f) for f in ("kernels.cu", "codec.cu", "gcr.cpp", "crc_host.cpp")],
         [os.path.join(CSRC, "gcr_internal.h"), os.path.join(INCLUDE, "gcr.h")],
     ),
     "libgcr_synth.so": (

@@ -250,6 +250,8 @@ struct gcr_image {
     uint64_t digests_cap = 0;
     uint8_t *data = nullptr;
     uint64_t data_cap = 0;
+    uint32_t *stored = nullptr;  // f4: stored length per PRESENT page (flags bit 1), pinned
+    uint64_t stored_cap = 0;
 };
 
 struct gcr_ctx {
@@ -294,6 +296,13 @@ struct gcr_ctx {
     FoldSlots fold{};
     uint32_t *pm_blk_cnt = nullptr, *pm_blk_off = nullptr, *run_start = nullptr;
     void *entries_d = nullptr;
+    // f4 codec (cfg.compress): per staging slot the KA/KB/KC scratch (plan,
+    // offsets, presence masks of one chunk's pages), the image's compact
+    // stored-length table, and each chunk's stored total (mapped pinned)
+    std::vector<uint32_t *> cx_scratch;
+    uint64_t cx_pages = 0;  // pages per chunk at most (chunk_bytes / P)
+    uint32_t *stored_d = nullptr;
+    unsigned long long *ctot_h = nullptr, *ctot_map = nullptr;
     ChunkTotals *totals_h = nullptr, *totals_map = nullptr;  // mapped pinned, written by K2
     unsigned long long *misc_d = nullptr, *misc_h = nullptr;  // [0] n_entries, [1] verify count, [2] first bad
     unsigned long long *nent_h = nullptr, *nent_map = nullptr;  // mapped pinned n_entries
@@ -372,6 +381,13 @@ void free_layout(gcr_ctx *c) {
                     c->pm_blk_off, c->run_start, c->entries_d, c->misc_d};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (uint32_t *p : c->cx_scratch)
+        if (p) cudaFree(p);
+    c->cx_scratch.clear();
+    if (c->stored_d) cudaFree(c->stored_d);
+    c->stored_d = nullptr;
+    if (c->ctot_h) cudaFreeHost(c->ctot_h);
+    c->ctot_h = c->ctot_map = nullptr;
     if (c->totals_h) cudaFreeHost(c->totals_h);
     if (c->misc_h) cudaFreeHost(c->misc_h);
     if (c->nent_h) cudaFreeHost(c->nent_h);
@@ -558,6 +574,17 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->nent_map), c->nent_h, 0));
     CUDA_TRY(c, cudaMalloc(&c->misc_d, 8 * 4));
     CUDA_TRY(c, cudaHostAlloc(&c->misc_h, 8 * 4, cudaHostAllocDefault));
+    if (c->cfg.compress) {  // f4 scratch: {plan, offsets, 32 mask words} per page of a chunk, per slot
+        c->cx_pages = c->cfg.chunk_bytes / P;
+        for (size_t k = 0; k < c->slots.size(); k++) {
+            uint32_t *x = nullptr;
+            CUDA_TRY(c, cudaMalloc(&x, 4 * 34 * c->cx_pages));
+            c->cx_scratch.push_back(x);
+        }
+        CUDA_TRY(c, cudaMalloc(&c->stored_d, 4 * std::max<uint64_t>(g, 1)));
+        CUDA_TRY(c, cudaHostAlloc(&c->ctot_h, 8 * std::max<uint64_t>(nch, 1), cudaHostAllocMapped));
+        CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->ctot_map), c->ctot_h, 0));
+    }
     CUDA_TRY(c, cudaMemcpyAsync(c->allocs_d, c->allocs_h.data(), sizeof(AllocDev) * na, cudaMemcpyHostToDevice,
                                 c->compute));
     LAUNCH_TRY(c, launch_build_page_table(c->allocs_d, (uint32_t)na, c->page_alloc, c->tile_alloc,
@@ -583,9 +610,11 @@ void image_free_buffers(gcr_image *img) {
     p.release(img->pagemap, img->pagemap_cap);
     p.release(img->digests, img->digests_cap);
     p.release(img->data, img->data_cap);
+    p.release(img->stored, img->stored_cap);
     img->pagemap = nullptr;
     img->digests = nullptr;
     img->data = nullptr;
+    img->stored = nullptr;
 }
 
 void destroy_image(gcr_ctx *c, gcr_image *img) {
@@ -608,6 +637,7 @@ uint32_t meta_crc(const gcr_image *img, const uint32_t *digests_reg = nullptr) {
     s = host_crc32c_update(s, img->pagemap, sizeof(gcr_pagemap_entry) * img->hdr.n_entries);
     if (digests_reg) s = crc_shift(s, 4ull * img->hdr.n_pages) ^ *digests_reg;
     else s = host_crc32c_update(s, img->digests, 4ull * img->hdr.n_pages);
+    if (img->hdr.flags & 2u) s = host_crc32c_update(s, img->stored, 4ull * img->hdr.n_present);
     return s ^ 0xFFFFFFFFu;
 }
 
@@ -622,7 +652,8 @@ gcr_status check_pagemap(gcr_ctx *c, const gcr_image *img) {
     const gcr_image_hdr &h = img->hdr;
     const uint32_t P = h.page_size;
     if (!valid_page_size(P)) return fail(c, GCR_E_CORRUPT, "image page size invalid");
-    uint64_t e = 0, np = 0, nz = 0, npa = 0, pb = 0, tot = 0;
+    uint64_t e = 0, np = 0, nz = 0, npa = 0, pb = 0, tot = 0, sb = 0;
+    const bool coded = h.flags & 2u;
     for (uint32_t a = 0; a < h.n_allocs; a++) {
         const gcr_alloc_rec &r = img->allocs[a];
         if (r.bytes == 0) return fail(c, GCR_E_CORRUPT, "image alloc of 0 bytes");
@@ -635,6 +666,15 @@ gcr_status check_pagemap(gcr_ctx *c, const gcr_image *img) {
             if (pe.vaddr != r.vaddr + p * P || pe.nr_pages == 0 || p + pe.nr_pages > m)
                 return fail(c, GCR_E_CORRUPT, "pagemap entry inconsistent with alloc table");
             if (pe.flags == GCR_PE_PRESENT) {
+                if (coded) {  // f4: raw (== length) or a coded form, a multiple of 16 shorter
+                    for (uint64_t q = p; q < p + pe.nr_pages; q++) {
+                        if (np + (q - p) >= h.n_present) return fail(c, GCR_E_CORRUPT, "stored-length table too short");
+                        const uint64_t L = page_len(r.bytes, P, q), st = img->stored[np + (q - p)];
+                        if (st > L || (st != L && (st % 16 != 0 || st < 16)))
+                            return fail(c, GCR_E_CORRUPT, "stored length inconsistent with its page");
+                        sb += st;
+                    }
+                }
                 np += pe.nr_pages;
                 uint64_t last = p + pe.nr_pages;
                 pb += (last == m) ? (uint64_t)(pe.nr_pages - 1) * P + page_len(r.bytes, P, m - 1)
@@ -651,7 +691,7 @@ gcr_status check_pagemap(gcr_ctx *c, const gcr_image *img) {
         }
     }
     if (e != h.n_entries || tot != h.n_pages || np != h.n_present || nz != h.n_zero || npa != h.n_parent ||
-        pb != h.image_bytes)
+        (coded ? sb : pb) != h.image_bytes)
         return fail(c, GCR_E_CORRUPT, "pagemap counts inconsistent with header");
     return GCR_OK;
 }
@@ -670,6 +710,8 @@ gcr_status gcr_config_default(gcr_config *out) {
     out->verify = 1;
     out->lock_timeout_ms = 10000;
     out->direct_min_bytes = 16ull << 20;
+    out->compress = 0;
+    out->reserved0 = 0;
     return GCR_OK;
 }
 
@@ -681,7 +723,7 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     if (cfg_in) cfg = *cfg_in;
     if (!valid_page_size(cfg.page_size) || cfg.n_copy_streams < 1 || cfg.n_copy_streams > 8 ||
         cfg.chunk_bytes == 0 || cfg.chunk_bytes % cfg.page_size != 0 || cfg.chunk_bytes % kTileBytes != 0 ||
-        cfg.chunk_bytes > kMaxChunk ||
+        cfg.chunk_bytes > kMaxChunk || cfg.compress > 1 ||
         (cfg.n_staging_slots != 0 && (cfg.n_staging_slots < cfg.n_copy_streams || cfg.n_staging_slots > 16)))
         return GCR_E_INVAL;
     if (!crc_self_test()) return GCR_E_INVAL;
@@ -903,12 +945,18 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // Small metadata first, then the worst-case (R) data buffer, which is
     // shrunk to the image size right after the drain: nothing is ever placed
     // behind the data buffer, so the pool does not fragment across checkpoints.
+    const bool coded = c->cfg.compress != 0;  // f4 page codec (R-19)
     img->digests_cap = 4 * c->n_pages;
     img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
+    if (coded) {  // worst case: every page PRESENT; shrunk after the drain
+        img->stored_cap = 4 * c->n_pages;
+        img->stored = static_cast<uint32_t *>(c->pool.alloc(img->stored_cap));
+    }
     img->data_cap = R;
     img->data = static_cast<uint8_t *>(c->pool.alloc(R));
     st.pinned_alloc_ns = c->pool.pin_ns;
-    if (!img->data || !img->digests) return fail(c, GCR_E_NOMEM, "checkpoint: pinned host allocation failed");
+    if (!img->data || !img->digests || (coded && !img->stored))
+        return fail(c, GCR_E_NOMEM, "checkpoint: pinned host allocation failed");
 
     ScanParams sp{};
     sp.allocs = c->allocs_d;
@@ -975,7 +1023,8 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // tiles of at least direct_min_bytes go straight from the allocation to the
     // pinned image; the other PRESENT tiles are packed (K4) into the chunk's
     // staging slot and copied out in contiguous ranges.
-    uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0;
+    uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0, raw_present = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> codec_ev;  // f4: KA+KB and KC spans
     Clock::time_point drain0;
     const size_t S = c->copy.size(), NS = c->slots.size();
     const uint64_t direct_min = c->cfg.direct_min_bytes;
@@ -1017,9 +1066,11 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             const volatile unsigned long long *h = reinterpret_cast<volatile unsigned long long *>(c->totals_h + i);
             T = ChunkTotals{h[0], h[1], h[2], h[3]};
         }
+        const uint64_t present_base = n_present;  // f4: this chunk's first entry of the stored-length table
         n_present += T.n_present;
         n_zero += T.n_zero;
         n_parent += T.n_parent;
+        raw_present += T.image_bytes;
         if (T.image_bytes == ~0ull) return fail(c, GCR_E_CUDA, "checkpoint: scan did not publish a chunk in time");
         if (base + T.image_bytes > R) return fail(c, GCR_E_CUDA, "checkpoint: image larger than registry");
         // ---- plan (host walk of the chunk's tiles) ----
@@ -1029,7 +1080,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         StageItem *items = c->stage_h + ch.tile_begin;
         uint32_t n_items = 0;
         bool any_staged = false;
-        if (T.image_bytes) {
+        if (T.image_bytes && !coded) {
             std::memset(flags, 0, ch.tile_end - ch.tile_begin);
             Run run{0, 0, 0, 0, 0};
             bool open = false;
@@ -1115,7 +1166,35 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         pks[i] = c->ev();
         pke[i] = c->ev();
         CUDA_TRY(c, cudaStreamWaitEvent(c->packs, tot[i], 0));
-        if (any_staged) {  // slot i mod NS was last drained by chunk i - NS
+        uint64_t chunk_stored = T.image_bytes;
+        if (coded && T.n_present) {
+            // f4: KA (stored length + presence masks per page), KB (slot offsets,
+            // stored-length table, chunk total -> mapped host), then -- once
+            // slot i mod NS is drained -- KC encodes the chunk's PRESENT pages
+            // into it; ONE D2H of the chunk's stored bytes follows.  All on the
+            // packs stream (in order: KC(i - NS) is done with the scratch before
+            // KA(i) overwrites it).
+            uint32_t *x = c->cx_scratch[i % NS];
+            uint32_t *plan = x, *off = x + c->cx_pages, *masks = x + 2 * c->cx_pages;
+            const uint32_t npg = (uint32_t)(ch.page_end - ch.page_begin);
+            cudaEvent_t ca = c->ev(), kb = c->ev();
+            CUDA_TRY(c, cudaEventRecord(ca, c->packs));
+            LAUNCH_TRY(c, launch_codec_plan(c->allocs_d, c->page_alloc, c->cls, ch.page_begin, npg, P, c->lg, plan,
+                                            masks, c->n_sms, c->packs));
+            LAUNCH_TRY(c, launch_codec_offsets(plan, npg, off, c->stored_d, present_base, c->ctot_map + i, c->packs));
+            CUDA_TRY(c, cudaEventRecord(kb, c->packs));
+            if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
+            CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
+            LAUNCH_TRY(c, launch_codec_encode(c->allocs_d, c->page_alloc, c->cls, ch.page_begin, npg, P, c->lg, plan,
+                                              off, masks, c->slots[i % NS], c->n_sms, c->packs));
+            codec_ev.emplace_back(ca, kb);
+            CUDA_TRY(c, cudaEventSynchronize(kb));
+            chunk_stored = *reinterpret_cast<volatile unsigned long long *>(c->ctot_h + i);
+            if (chunk_stored > T.image_bytes) return fail(c, GCR_E_CUDA, "checkpoint: coded chunk larger than its pages");
+            staged.emplace_back(0, chunk_stored);
+        } else if (coded) {
+            CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
+        } else if (any_staged) {  // slot i mod NS was last drained by chunk i - NS
             if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
             // narrowed to the SMs K1 leaves free while the scan's last chunk is unpublished
@@ -1156,12 +1235,21 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             gcr_status cs_ = crc_batches(false);  // digests that already landed (the host is idle here)
             if (cs_ != GCR_OK) return cs_;
         }
-        base += T.image_bytes;
+        base += chunk_stored;
     }
     if (direct_bytes + staged_bytes != base) return fail(c, GCR_E_CUDA, "checkpoint: drain plan does not cover the image");
     st.direct_bytes = direct_bytes;
     c->pool.shrink(img->data, img->data_cap, base);  // the tail is free before the pagemap is allocated
     img->data_cap = base;
+    if (coded) {  // the stored-length table (KB wrote it chunk by chunk on the packs stream)
+        c->pool.shrink(img->stored, img->stored_cap, 4 * n_present);
+        img->stored_cap = 4 * n_present;
+        cudaEvent_t e = c->ev();
+        CUDA_TRY(c, cudaEventRecord(e, c->packs));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
+        if (n_present)
+            CUDA_TRY(c, cudaMemcpyAsync(img->stored, c->stored_d, 4 * n_present, cudaMemcpyDeviceToHost, c->compute));
+    }
     // K3 pagemap over all pages (maximal runs, independent of chunking): every
     // class is final once the last K1 (same stream) has ended.
     auto pm0 = c->ev(), pm1 = c->ev();
@@ -1199,6 +1287,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     }
     CUDA_TRY(c, cudaEventElapsedTime(&ms, pm0, pm1));
     st.compact_dev_ns = (uint64_t)(ms * 1e6);
+    st.codec_dev_ns = 0;
+    for (const auto &ce : codec_ev) {
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, ce.first, ce.second));
+        st.codec_dev_ns += (uint64_t)(ms * 1e6);
+    }
+    if (coded) st.codec_dev_ns += st.pack_dev_ns;  // KC ran between pks / pke
+    st.present_raw_bytes = raw_present;
     const double host_stats = ns_since(host0) * 1e-6;
     if (trace) {  // GCR_TRACE=1: per-chunk timeline (ms from the checkpoint's first event) on stderr
         auto rel = [&](cudaEvent_t e) {
@@ -1233,7 +1328,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     h.generation = c->next_gen;
     h.parent_generation = mode == GCR_INCREMENTAL ? c->parent_gen : 0;
     h.n_allocs = (uint32_t)c->reg.size();
-    h.flags = mode == GCR_INCREMENTAL ? 1u : 0u;
+    h.flags = (mode == GCR_INCREMENTAL ? 1u : 0u) | (coded ? 2u : 0u);
     h.n_pages = c->n_pages;
     h.n_present = n_present;
     h.n_zero = n_zero;
@@ -1358,7 +1453,8 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         const gcr_image *im = chain[k];
         if (std::memcmp(im->hdr.magic, kMagic, 8) != 0 || meta_crc(im) != im->hdr.meta_crc32c)
             return fail(c, GCR_E_CORRUPT, "restore: meta_crc32c mismatch");
-        if (im->hdr.version != 1) return fail(c, GCR_E_VERSION, "restore: unknown image version");
+        if (im->hdr.version != 1 || (im->hdr.flags & ~3u))
+            return fail(c, GCR_E_VERSION, "restore: unknown image version or flag bits");
         gcr_status s = check_pagemap(c, im);
         if (s != GCR_OK) return s;
     }
@@ -1408,7 +1504,8 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     struct Item {
         bool direct;
         uint64_t img_off, bytes, dst;  // direct: dst device address
-        uint64_t d_begin, d_end;       // staged: scatter descriptors
+        uint64_t d_begin, d_end;       // staged: scatter (or, f4 image, decode) descriptors
+        bool decode;                   // f4: the group's pages are stored forms (K-D decodes them)
     };
     struct ImgPlan {
         std::vector<Item> items;
@@ -1418,15 +1515,17 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     std::vector<ImgPlan> plans(n);
     std::vector<ScatterDesc> sdesc;
     std::vector<ZeroDesc> zdesc;
+    std::vector<DecodeDesc> ddesc;
     uint64_t h2d_bytes = 0, direct_bytes = 0;
     for (uint32_t k = 0; k < n; k++) {
         const gcr_image *im = chain[k];
         ImgPlan &pl = plans[k];
         pl.z_begin = zdesc.size();
-        uint64_t cursor = 0, e = 0;
+        uint64_t cursor = 0, e = 0, ip = 0;  // ip: ordinal of the next PRESENT page (f4 stored lengths)
+        const bool coded = im->hdr.flags & 2u;
         bool group_open = false;
         auto close_group = [&]() {
-            if (group_open) pl.items.back().d_end = sdesc.size();
+            if (group_open) pl.items.back().d_end = coded ? ddesc.size() : sdesc.size();
             group_open = false;
         };
         for (uint32_t a = 0; a < im->hdr.n_allocs; a++) {
@@ -1438,12 +1537,28 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                 uint64_t bytes = (last == m) ? (uint64_t)(pe.nr_pages - 1) * P + page_len(c->reg[a].bytes, P, m - 1)
                                              : (uint64_t)pe.nr_pages * P;
                 uint64_t dst = c->reg[a].dptr + p * P;  // remapped by allocation index (R-14)
-                if (pe.flags == GCR_PE_PRESENT) {
+                if (pe.flags == GCR_PE_PRESENT && coded) {
+                    // f4: every page's stored form goes through a slot; groups of
+                    // consecutive stored forms up to one slot, one decode
+                    // descriptor per page
+                    for (uint64_t q = p; q < last; q++) {
+                        const uint32_t L = (uint32_t)page_len(c->reg[a].bytes, P, q), sl = im->stored[ip++];
+                        if (group_open && pl.items.back().bytes + sl > slot) close_group();
+                        if (!group_open) {
+                            pl.items.push_back(Item{false, cursor, 0, 0, ddesc.size(), 0, true});
+                            group_open = true;
+                        }
+                        Item &g = pl.items.back();
+                        ddesc.push_back(DecodeDesc{c->reg[a].dptr + q * P, cursor - g.img_off, L, sl});
+                        g.bytes += sl;
+                        cursor += sl;
+                    }
+                } else if (pe.flags == GCR_PE_PRESENT) {
                     if (bytes >= direct_min) {
                         close_group();
                         while (bytes) {  // pieces of at most one slot keep the copy streams busy
                             const uint64_t piece = std::min(bytes, slot);
-                            pl.items.push_back(Item{true, cursor, piece, dst, 0, 0});
+                            pl.items.push_back(Item{true, cursor, piece, dst, 0, 0, false});
                             direct_bytes += piece;
                             dst += piece;
                             cursor += piece;
@@ -1453,7 +1568,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                         while (bytes) {
                             if (group_open && pl.items.back().bytes + bytes > slot) close_group();
                             if (!group_open) {
-                                pl.items.push_back(Item{false, cursor, 0, 0, sdesc.size(), 0});
+                                pl.items.push_back(Item{false, cursor, 0, 0, sdesc.size(), 0, false});
                                 group_open = true;
                             }
                             Item &g = pl.items.back();
@@ -1481,16 +1596,19 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         h2d_bytes += im->hdr.image_bytes;
     }
     const uint64_t sbytes = sizeof(ScatterDesc) * sdesc.size(), zbytes = sizeof(ZeroDesc) * zdesc.size();
-    s = ensure_desc(c, sbytes + zbytes + 16);
+    const uint64_t dbytes = sizeof(DecodeDesc) * ddesc.size();
+    s = ensure_desc(c, sbytes + zbytes + dbytes + 16);
     if (s != GCR_OK) return s;
     std::memcpy(c->desc_h, sdesc.data(), sbytes);
     std::memcpy(c->desc_h + sbytes, zdesc.data(), zbytes);
+    std::memcpy(c->desc_h + sbytes + zbytes, ddesc.data(), dbytes);
     const ScatterDesc *sd = reinterpret_cast<const ScatterDesc *>(c->desc_d);
     const ZeroDesc *zd = reinterpret_cast<const ZeroDesc *>(c->desc_d + sbytes);
-    CUDA_TRY(c, cudaMemcpyAsync(c->desc_d, c->desc_h, sbytes + zbytes, cudaMemcpyHostToDevice, c->compute));
+    const DecodeDesc *dd = reinterpret_cast<const DecodeDesc *>(c->desc_d + sbytes + zbytes);
+    CUDA_TRY(c, cudaMemcpyAsync(c->desc_d, c->desc_h, sbytes + zbytes + dbytes, cudaMemcpyHostToDevice, c->compute));
 
     // ---- apply the chain ----------------------------------------------------
-    std::vector<cudaEvent_t> sc0, sc1;
+    std::vector<cudaEvent_t> sc0, sc1, dc0, dc1;  // scatter+zero / f4 decode spans
     auto h2d0 = Clock::now();
     for (uint32_t k = 0; k < n; k++) {
         const gcr_image *im = chain[k];
@@ -1509,10 +1627,13 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
             CUDA_TRY(c, cudaMemcpyAsync(c->slots[j % S], im->data + it.img_off, it.bytes, cudaMemcpyHostToDevice, cs));
             cudaEvent_t a = c->ev(), b = c->ev();
             CUDA_TRY(c, cudaEventRecord(a, cs));
-            LAUNCH_TRY(c, launch_scatter(sd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
+            if (it.decode)
+                LAUNCH_TRY(c, launch_codec_decode(dd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
+            else
+                LAUNCH_TRY(c, launch_scatter(sd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
             CUDA_TRY(c, cudaEventRecord(b, cs));
-            sc0.push_back(a);
-            sc1.push_back(b);
+            (it.decode ? dc0 : sc0).push_back(a);
+            (it.decode ? dc1 : sc1).push_back(b);
         }
         if (pl.z_end > pl.z_begin) {
             cudaEvent_t a = c->ev(), b = c->ev();
@@ -1605,6 +1726,11 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     for (size_t i = 0; i < sc0.size(); i++) {
         CUDA_TRY(c, cudaEventElapsedTime(&ms, sc0[i], sc1[i]));
         st.scatter_dev_ns += (uint64_t)(ms * 1e6);
+    }
+    st.decode_dev_ns = 0;
+    for (size_t i = 0; i < dc0.size(); i++) {
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, dc0[i], dc1[i]));
+        st.decode_dev_ns += (uint64_t)(ms * 1e6);
     }
     st.verify_dev_ns = 0;
     st.verify_failures = 0;
@@ -1833,10 +1959,19 @@ gcr_status gcr_image_free(gcr_image *img) {
     return GCR_OK;
 }
 
+gcr_status gcr_image_stored(const gcr_image *img, const uint32_t **p, uint64_t *n) {
+    if (!img || !p || !n) return GCR_E_INVAL;
+    const bool coded = img->hdr.flags & 2u;
+    *p = coded ? img->stored : nullptr;
+    *n = coded ? img->hdr.n_present : 0;
+    return GCR_OK;
+}
+
 gcr_status gcr_image_stream_size(const gcr_image *img, uint64_t *bytes) {
     if (!img || !bytes) return GCR_E_INVAL;
     const gcr_image_hdr &h = img->hdr;
-    *bytes = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages + h.image_bytes;
+    *bytes = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages +
+             ((h.flags & 2u) ? 4ull * h.n_present : 0ull) + h.image_bytes;
     return GCR_OK;
 }
 
@@ -1853,6 +1988,10 @@ gcr_status gcr_image_serialize(const gcr_image *img, void *dst, uint64_t cap) {
     o += 16ull * h.n_entries;
     std::memcpy(o, img->digests, 4ull * h.n_pages);
     o += 4ull * h.n_pages;
+    if ((h.flags & 2u) && h.n_present) {
+        std::memcpy(o, img->stored, 4ull * h.n_present);
+        o += 4ull * h.n_present;
+    }
     if (h.image_bytes) std::memcpy(o, img->data, h.image_bytes);
     return GCR_OK;
 }
@@ -1866,16 +2005,17 @@ gcr_status gcr_image_import(gcr_ctx *c, const void *stream, uint64_t bytes, gcr_
     gcr_image_hdr h;
     std::memcpy(&h, s, 96);
     if (std::memcmp(h.magic, kMagic, 8) != 0) return fail(c, GCR_E_CORRUPT, "import: bad magic");
-    if (h.n_pages > bytes / 4 || h.n_entries > bytes / 16 || h.n_allocs > bytes / 24)
+    if (h.n_pages > bytes / 4 || h.n_entries > bytes / 16 || h.n_allocs > bytes / 24 || h.n_present > bytes / 4)
         return fail(c, GCR_E_CORRUPT, "import: section sizes exceed the stream");
-    const uint64_t meta = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages;
+    const uint64_t nst = (h.flags & 2u) ? h.n_present : 0;  // f4 stored-length table
+    const uint64_t meta = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages + 4ull * nst;
     if (meta > bytes || bytes - meta != h.image_bytes) return fail(c, GCR_E_CORRUPT, "import: framing mismatch");
     gcr_image_hdr h0 = h;
     h0.meta_crc32c = 0;
     uint32_t st = host_crc32c_update(0xFFFFFFFFu, &h0, 96);
     st = host_crc32c_update(st, s + 96, meta - 96) ^ 0xFFFFFFFFu;
     if (st != h.meta_crc32c) return fail(c, GCR_E_CORRUPT, "import: meta_crc32c mismatch");
-    if (h.version != 1) return fail(c, GCR_E_VERSION, "import: unknown version");
+    if (h.version != 1 || (h.flags & ~3u)) return fail(c, GCR_E_VERSION, "import: unknown version or flag bits");
     CUDA_TRY(c, cudaSetDevice(c->device));
     gcr_image *img = new (std::nothrow) gcr_image;
     if (!img) return fail(c, GCR_E_NOMEM, "import: out of host memory");
@@ -1889,8 +2029,10 @@ gcr_status gcr_image_import(gcr_ctx *c, const void *stream, uint64_t bytes, gcr_
     img->pagemap = static_cast<gcr_pagemap_entry *>(c->pool.alloc(img->pagemap_cap));
     img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
     img->data = static_cast<uint8_t *>(c->pool.alloc(img->data_cap));
+    img->stored_cap = 4ull * nst;
+    img->stored = nst ? static_cast<uint32_t *>(c->pool.alloc(img->stored_cap)) : nullptr;
     c->stats.pinned_alloc_ns = c->pool.pin_ns;
-    if (!img->pagemap || !img->digests || !img->data) {
+    if (!img->pagemap || !img->digests || !img->data || (nst && !img->stored)) {
         image_free_buffers(img);
         delete img;
         return fail(c, GCR_E_NOMEM, "import: pinned allocation failed");
@@ -1900,6 +2042,8 @@ gcr_status gcr_image_import(gcr_ctx *c, const void *stream, uint64_t bytes, gcr_
     o += 16ull * h.n_entries;
     std::memcpy(img->digests, o, 4ull * h.n_pages);
     o += 4ull * h.n_pages;
+    if (nst) std::memcpy(img->stored, o, 4ull * nst);
+    o += 4ull * nst;
     std::memcpy(img->data, o, h.image_bytes);
     c->images.push_back(img);
     *out = img;
@@ -1987,6 +2131,10 @@ gcr_status gcr_image_write_file(const gcr_image *img, const char *path, uint32_t
     o += 16ull * h.n_entries;
     segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->digests), 4ull * h.n_pages});
     o += 4ull * h.n_pages;
+    if (h.flags & 2u) {
+        segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->stored), 4ull * h.n_present});
+        o += 4ull * h.n_present;
+    }
     segs.push_back(IoSeg{o, img->data, h.image_bytes});
     const int e = parallel_io(fd, segs, n_threads, true);
     if (e) return io_fail("pwrite", e);
@@ -2018,11 +2166,12 @@ gcr_status gcr_image_read_file(gcr_ctx *c, const char *path, uint32_t n_threads,
     }
     // framing checks as in gcr_image_import, before allocating anything
     if (std::memcmp(h.magic, kMagic, 8) != 0 || h.n_pages > bytes / 4 || h.n_entries > bytes / 16 ||
-        h.n_allocs > bytes / 24) {
+        h.n_allocs > bytes / 24 || h.n_present > bytes / 4) {
         close(fd);
         return fail(c, GCR_E_CORRUPT, "read_file: bad magic or section sizes exceed the file");
     }
-    const uint64_t meta = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages;
+    const uint64_t nst = (h.flags & 2u) ? h.n_present : 0;  // f4 stored-length table
+    const uint64_t meta = 96 + 24ull * h.n_allocs + 16ull * h.n_entries + 4ull * h.n_pages + 4ull * nst;
     if (meta > bytes || bytes - meta != h.image_bytes) {
         close(fd);
         return fail(c, GCR_E_CORRUPT, "read_file: framing mismatch (file size != stream size)");
@@ -2051,8 +2200,11 @@ gcr_status gcr_image_read_file(gcr_ctx *c, const char *path, uint32_t n_threads,
     img->pagemap = static_cast<gcr_pagemap_entry *>(c->pool.alloc(img->pagemap_cap));
     img->digests = static_cast<uint32_t *>(c->pool.alloc(img->digests_cap));
     img->data = static_cast<uint8_t *>(c->pool.alloc(img->data_cap));
+    img->stored_cap = 4ull * nst;
+    img->stored = nst ? static_cast<uint32_t *>(c->pool.alloc(img->stored_cap)) : nullptr;
     c->stats.pinned_alloc_ns = c->pool.pin_ns;
-    if ((img->pagemap_cap && !img->pagemap) || (img->digests_cap && !img->digests) || (img->data_cap && !img->data))
+    if ((img->pagemap_cap && !img->pagemap) || (img->digests_cap && !img->digests) || (img->data_cap && !img->data) ||
+        (nst && !img->stored))
         return bail(GCR_E_NOMEM, "read_file: pinned allocation failed");
     std::vector<IoSeg> segs;
     uint64_t o = 96;
@@ -2062,6 +2214,10 @@ gcr_status gcr_image_read_file(gcr_ctx *c, const char *path, uint32_t n_threads,
     o += 16ull * h.n_entries;
     segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->digests), 4ull * h.n_pages});
     o += 4ull * h.n_pages;
+    if (nst) {
+        segs.push_back(IoSeg{o, reinterpret_cast<uint8_t *>(img->stored), 4ull * nst});
+        o += 4ull * nst;
+    }
     segs.push_back(IoSeg{o, img->data, h.image_bytes});
     const int e = parallel_io(fd, segs, n_threads, false);
     if (e) return bail(GCR_E_IO, std::string("read_file: pread: ") + std::strerror(e));
@@ -2071,10 +2227,10 @@ gcr_status gcr_image_read_file(gcr_ctx *c, const char *path, uint32_t n_threads,
         delete img;
         return fail(c, GCR_E_CORRUPT, "read_file: meta_crc32c mismatch");
     }
-    if (h.version != 1) {
+    if (h.version != 1 || (h.flags & ~3u)) {
         image_free_buffers(img);
         delete img;
-        return fail(c, GCR_E_VERSION, "read_file: unknown version");
+        return fail(c, GCR_E_VERSION, "read_file: unknown version or flag bits");
     }
     c->images.push_back(img);
     *out = img;

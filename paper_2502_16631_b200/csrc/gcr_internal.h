@@ -139,6 +139,14 @@ struct ZeroDesc {
     uint64_t bytes;
 };
 
+// f4 restore: one PRESENT page's stored form in a staging slot -> its page.
+struct DecodeDesc {
+    uint64_t dst;      // device address of the page
+    uint64_t src_off;  // offset of the stored form in the slot (multiple of 16)
+    uint32_t len;      // page length (multiple of 16)
+    uint32_t stored;   // stored length (== len: raw)
+};
+
 // ---- kernel launchers (kernels.cu); all asynchronous on `st` -------------
 // Each returns the number of kernels it launched (for stats) or -1 on a
 // launch error (cudaGetLastError holds it).
@@ -170,6 +178,23 @@ int launch_scatter(const ScatterDesc *desc, uint64_t n_desc, const uint8_t *slot
                    cudaStream_t st);
 int launch_zero_fill(const ZeroDesc *desc, uint64_t n_desc, int n_sms, cudaStream_t st);
 size_t scan_smem_bytes();
+
+// ---- f4 page codec (codec.cu, R-19) -------------------------------
+// KA over the chunk's pages [page_begin, page_begin + n_pages): stored length
+// per page (0 if not PRESENT) and presence masks (32 u32 per page).
+int launch_codec_plan(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls, uint64_t page_begin,
+                      uint32_t n_pages, uint32_t page_size, uint32_t log2_page, uint32_t *plan, uint32_t *masks,
+                      int n_sms, cudaStream_t st);
+// KB: chunk-local slot offsets, the image's compact stored-length table from
+// present_base on, the chunk's stored total into mapped host memory.
+int launch_codec_offsets(const uint32_t *plan, uint32_t n_pages, uint32_t *off, uint32_t *stored_compact,
+                         uint64_t present_base, unsigned long long *total_host, cudaStream_t st);
+// KC: stored forms of the chunk's PRESENT pages into the slot.
+int launch_codec_encode(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls, uint64_t page_begin,
+                        uint32_t n_pages, uint32_t page_size, uint32_t log2_page, const uint32_t *plan,
+                        const uint32_t *off, const uint32_t *masks, uint8_t *slot, int n_sms, cudaStream_t st);
+// KD: restore a staged group of stored pages.
+int launch_codec_decode(const DecodeDesc *desc, uint64_t n_desc, const uint8_t *slot, int n_sms, cudaStream_t st);
 
 // ---- host CRC32C math (crc_host.cpp), independent of oracle/ --------------
 void build_tables(CrcTables *out);

@@ -32,7 +32,7 @@ GCR_PE_PARENT, GCR_PE_PRESENT, GCR_PE_ZERO = 1, 4, 8
 class gcr_config(C.Structure):
     _fields_ = [("page_size", C.c_uint32), ("n_copy_streams", C.c_uint32), ("chunk_bytes", C.c_uint64),
                 ("n_staging_slots", C.c_uint32), ("verify", C.c_uint32), ("lock_timeout_ms", C.c_uint64),
-                ("direct_min_bytes", C.c_uint64)]
+                ("direct_min_bytes", C.c_uint64), ("compress", C.c_uint32), ("reserved0", C.c_uint32)]
 
 
 _STAT_FIELDS = ["lock_ns", "unlock_ns", "checkpoint_ns", "restore_ns", "scan_dev_ns", "scan_launches", "scan_bytes",
@@ -40,7 +40,7 @@ _STAT_FIELDS = ["lock_ns", "unlock_ns", "checkpoint_ns", "restore_ns", "scan_dev
                 "verify_launches", "pages_scanned", "pages_zero", "pages_parent", "pages_written", "image_bytes",
                 "n_entries", "verify_failures", "first_bad_page", "restore_h2d_bytes", "kernel_launches",
                 "pinned_alloc_ns", "direct_bytes", "restore_direct_bytes", "release_ns", "remap_ns",
-                "released_bytes"]
+                "released_bytes", "present_raw_bytes", "codec_dev_ns", "decode_dev_ns"]
 
 
 class gcr_stats(C.Structure):
@@ -95,6 +95,7 @@ _SIGS = {
     "gcr_image_pagemap": [_vp, _P(_P(gcr_pagemap_entry)), _P(_u64)],
     "gcr_image_digests": [_vp, _P(_P(_u32)), _P(_u64)],
     "gcr_image_data": [_vp, _P(_P(C.c_uint8)), _P(_u64)],
+    "gcr_image_stored": [_vp, _P(_P(_u32)), _P(_u64)],
     "gcr_image_free": [_vp],
     "gcr_image_stream_size": [_vp, _P(_u64)],
     "gcr_image_serialize": [_vp, _vp, _u64],
@@ -174,6 +175,16 @@ class Image:
             return np.zeros(0, dt)
         buf = (C.c_uint8 * (16 * n.value)).from_address(C.addressof(p.contents))
         return np.frombuffer(buf, dtype=dt)
+
+    def stored(self):
+        """f4 images: stored length of every PRESENT page (numpy copy); else None."""
+        import numpy as np
+        p = _P(_u32)()
+        n = C.c_uint64()
+        self.ctx._check(gcr_image_stored(self.handle, C.byref(p), C.byref(n)))
+        if not p:
+            return None
+        return np.ctypeslib.as_array(p, shape=(n.value,)).copy() if n.value else np.zeros(0, np.uint32)
 
     def data_view(self):
         """Zero-copy numpy view of the pinned image data (valid until free)."""

@@ -50,19 +50,26 @@ def page_lengths(sizes, P):
     return lens, starts
 
 
-def parse_stream(s: bytes):
-    """Sections of a canonical stream as numpy views (layout only)."""
+def parse_stream(s: bytes, with_stored: bool = False):
+    """Sections of a canonical stream as numpy views (layout only, DESIGN.md §3;
+    f4 streams, header flags bit 1, carry a stored-length table)."""
     h = np.frombuffer(s, dtype=np.uint8, count=96)
     n_allocs = int(h[32:36].view(np.uint32)[0])
+    flags = int(h[36:40].view(np.uint32)[0])
     n_pages = int(h[40:48].view(np.uint64)[0])
+    n_present = int(h[48:56].view(np.uint64)[0])
     n_entries = int(h[72:80].view(np.uint64)[0])
     o = 96 + 24 * n_allocs
     pm = np.frombuffer(s, dtype=PM_DT, count=n_entries, offset=o)
     o += 16 * n_entries
     dg = np.frombuffer(s, dtype="<u4", count=n_pages, offset=o)
     o += 4 * n_pages
+    st = None
+    if flags & 2:
+        st = np.frombuffer(s, dtype="<u4", count=n_present, offset=o)
+        o += 4 * n_present
     data = np.frombuffer(s, dtype=np.uint8, offset=o)
-    return h, pm, dg, data
+    return (h, pm, dg, st, data) if with_stored else (h, pm, dg, data)
 
 
 def expand_flags(pm, n_pages):
@@ -97,7 +104,7 @@ def slices_of(sizes, P, slice_bytes):
 
 
 def check_image_full(orc, w, img, reg, mode=0, d_prev=None, generation=1, parent_generation=0,
-                     slice_bytes=128 << 20, threads=None):
+                     slice_bytes=128 << 20, threads=None, compress=False):
     """Compare the GPU image `img` of workload `w` (registered as `reg` = [(alloc_id,
     vaddr, bytes)] in order) with the oracle, page by page.  Returns the oracle's
     digest table (the next incremental's D_prev)."""
@@ -114,11 +121,21 @@ def check_image_full(orc, w, img, reg, mode=0, d_prev=None, generation=1, parent
     assert int(gpm["nr_pages"].astype(np.int64).sum()) == n
     gflags = expand_flags(gpm, n)
     # GPU image offset of every page (used to locate a slice's data; verified below)
-    goff = np.concatenate([[0], np.cumsum(np.where(gflags == PE_PRESENT, lens, 0))])
+    present = gflags == PE_PRESENT
+    if compress:  # f4: data offsets advance by each PRESENT page's stored length
+        gst = img.stored()
+        assert gst is not None and gst.size == int(present.sum()) == hdr.n_present
+        per_page = np.zeros(n, np.int64)
+        per_page[present] = gst
+    else:
+        assert img.stored() is None
+        per_page = np.where(present, lens, 0)
+    goff = np.concatenate([[0], np.cumsum(per_page)])
     assert goff[-1] == hdr.image_bytes == gdata.size
     tasks = slices_of(sizes, P, slice_bytes)
     exp_dig = np.empty(n, np.uint32)
     exp_flags = np.empty(n, np.uint32)
+    exp_stored = np.zeros(n, np.int64)  # f4: the oracle's stored length of every PRESENT page
     data_len = np.zeros(len(tasks), np.int64)
     bad = []
 
@@ -129,12 +146,14 @@ def check_image_full(orc, w, img, reg, mode=0, d_prev=None, generation=1, parent
         content = w.cpu_bytes(a, p0 * P, L)
         dp = None if mode == 0 else np.ascontiguousarray(d_prev[g0:g1], dtype=np.uint32)
         st, s = orc.checkpoint(P, [(reg[a][0], vaddrs[a] + p0 * P, L)], [content], mode=mode, d_prev=dp,
-                               generation=generation, parent_generation=parent_generation)
+                               generation=generation, parent_generation=parent_generation, compress=compress)
         assert st == orc.OK, st
         del content
-        _, pm, dg, data = parse_stream(s)
+        _, pm, dg, sst, data = parse_stream(s, with_stored=True)
         exp_dig[g0:g1] = dg
         exp_flags[g0:g1] = expand_flags(pm, g1 - g0)
+        if compress:
+            exp_stored[g0:g1][exp_flags[g0:g1] == PE_PRESENT] = sst
         data_len[k] = data.size
         msg = []
         if not np.array_equal(dg, gdig[g0:g1]):
@@ -150,6 +169,8 @@ def check_image_full(orc, w, img, reg, mode=0, d_prev=None, generation=1, parent
         list(ex.map(work, range(len(tasks))))
     assert not bad, bad[:5]
     assert np.array_equal(exp_flags, gflags), f"class of page {int(np.flatnonzero(exp_flags != gflags)[0])} differs"
+    if compress:
+        assert np.array_equal(exp_stored[present], gst), "stored-length table differs"
     # the offsets used above are the oracle's: prefix sums of its slice data lengths
     cum = np.concatenate([[0], np.cumsum(data_len)])
     for k, (a, p0, _) in enumerate(tasks):
@@ -172,7 +193,7 @@ def check_image_full(orc, w, img, reg, mode=0, d_prev=None, generation=1, parent
     u64(16, generation)
     u64(24, parent_generation if mode == 1 else 0)
     u32(32, len(reg))
-    u32(36, 1 if mode == 1 else 0)
+    u32(36, (1 if mode == 1 else 0) | (2 if compress else 0))
     u64(40, n)
     u64(48, n_present)
     u64(56, n_zero)
@@ -183,7 +204,10 @@ def check_image_full(orc, w, img, reg, mode=0, d_prev=None, generation=1, parent
     al["vaddr"] = vaddrs
     al["bytes"] = sizes
     al["alloc_id"] = [r[0] for r in reg]
-    meta = np.concatenate([eh, al.view(np.uint8), epm.view(np.uint8), exp_dig.view(np.uint8)])
+    parts = [eh, al.view(np.uint8), epm.view(np.uint8), exp_dig.view(np.uint8)]
+    if compress:
+        parts.append(exp_stored[exp_flags == PE_PRESENT].astype(np.uint32).view(np.uint8))
+    meta = np.concatenate(parts)
     u32(88, orc.crc32c(meta))
     assert bytes(eh) == bytes(memoryview(hdr)), "header differs"
     return exp_dig

@@ -15,7 +15,7 @@ class StreamImage:
     def __init__(self, s: bytes):
         from paper_2502_16631_b200 import gcr
         self.s = bytearray(s)
-        self.h, self.pm, self.dg, self.data = fc.parse_stream(self.s)
+        self.h, self.pm, self.dg, self.st, self.data = fc.parse_stream(self.s, with_stored=True)
         self._hdr = gcr.gcr_image_hdr.from_buffer_copy(bytes(self.s[:96]))
 
     def header(self):
@@ -29,6 +29,9 @@ class StreamImage:
 
     def data_view(self):
         return self.data
+
+    def stored(self):
+        return None if self.st is None else self.st.copy()
 
 
 def small_workload(P):
@@ -47,30 +50,31 @@ def registry(w):
 
 @pytest.mark.parametrize("P", [4096, 65536])
 @pytest.mark.parametrize("slice_pages", [1, 3, 64])
-def test_harness_accepts_whole_oracle_stream(orc, P, slice_pages):
+@pytest.mark.parametrize("compress", [False, True])
+def test_harness_accepts_whole_oracle_stream(orc, P, slice_pages, compress):
     w = small_workload(P)
     reg = registry(w)
     cont = [w.cpu_bytes(a) for a in range(len(reg))]
-    st, s = orc.checkpoint(P, reg, cont, generation=1)
+    st, s = orc.checkpoint(P, reg, cont, generation=1, compress=compress)
     assert st == 0
-    d0 = fc.check_image_full(orc, w, StreamImage(s), reg, slice_bytes=slice_pages * P, threads=3)
+    d0 = fc.check_image_full(orc, w, StreamImage(s), reg, slice_bytes=slice_pages * P, threads=3, compress=compress)
     assert np.array_equal(d0, fc.parse_stream(s)[2])
     # incremental over a mutated state
     w.mutations = [(0, 4 * P + 8, 0x1234), (3, 2 * P, 0xFFFF0000)]
     cont = [w.cpu_bytes(a) for a in range(len(reg))]
-    st, s2 = orc.checkpoint(P, reg, cont, mode=1, d_prev=d0, generation=2, parent_generation=1)
+    st, s2 = orc.checkpoint(P, reg, cont, mode=1, d_prev=d0, generation=2, parent_generation=1, compress=compress)
     assert st == 0
     fc.check_image_full(orc, w, StreamImage(s2), reg, mode=1, d_prev=d0, generation=2, parent_generation=1,
-                        slice_bytes=slice_pages * P, threads=2)
+                        slice_bytes=slice_pages * P, threads=2, compress=compress)
 
 
-@pytest.mark.parametrize("defect", ["digest", "data", "pagemap", "header", "generation"])
+@pytest.mark.parametrize("defect", ["digest", "data", "pagemap", "header", "generation", "stored"])
 def test_harness_rejects_defects(orc, defect):
     P = 4096
     w = small_workload(P)
     reg = registry(w)
     cont = [w.cpu_bytes(a) for a in range(len(reg))]
-    st, s = orc.checkpoint(P, reg, cont, generation=1)
+    st, s = orc.checkpoint(P, reg, cont, generation=1, compress=True)
     im = StreamImage(s)
     gen = 1
     if defect == "digest":
@@ -84,7 +88,12 @@ def test_harness_rejects_defects(orc, defect):
         im.pm = pm
     elif defect == "header":
         im._hdr.meta_crc32c ^= 1
+    elif defect == "stored":
+        st2 = im.st.copy()
+        i, j = 0, int(np.flatnonzero(st2 != st2[0])[0])
+        st2[i], st2[j] = st2[j], st2[i]  # same total, wrong per-page lengths
+        im.st = st2
     else:
         gen = 2
     with pytest.raises(AssertionError):
-        fc.check_image_full(orc, w, im, reg, generation=gen, slice_bytes=2 * P, threads=2)
+        fc.check_image_full(orc, w, im, reg, generation=gen, slice_bytes=2 * P, threads=2, compress=True)
