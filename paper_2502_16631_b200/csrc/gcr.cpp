@@ -1681,40 +1681,44 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         sp.verify_count = c->misc_d + 1;
         sp.first_bad = c->misc_d + 2;
         sp.tables = c->tables_d;
-        // GCR_SCAN_TIMES=1: per-warp {entry, first chunk done, exit} globaltimer
-        // stamps of this verify launch, summarised on stderr (diagnostics)
+        // GCR_SCAN_TIMES=1: per-warp globaltimer stamps of this verify launch
+        // (entry, tables staged, first rows loaded, chunk done, exit),
+        // summarised on stderr relative to the earliest entry (diagnostics)
         static const bool stamps = std::getenv("GCR_SCAN_TIMES") != nullptr;
         unsigned long long *wt = nullptr;
-        if (stamps && cudaMalloc(&wt, 24 * sp.workers) == cudaSuccess) {
-            cudaMemsetAsync(wt, 0, 24 * sp.workers, c->compute);
+        const uint64_t SW = kScanStamps;
+        if (stamps && cudaMalloc(&wt, 8 * SW * sp.workers) == cudaSuccess) {
+            cudaMemsetAsync(wt, 0, 8 * SW * sp.workers, c->compute);
             sp.warp_times = wt;
         }
         CUDA_TRY(c, cudaEventRecord(v0, c->compute));
         LAUNCH_TRY(c, launch_scan(sp, c->n_sms, c->compute));
         CUDA_TRY(c, cudaEventRecord(v1, c->compute));
         if (wt) {
-            std::vector<unsigned long long> h(3 * sp.workers);
-            cudaMemcpy(h.data(), wt, 24 * sp.workers, cudaMemcpyDeviceToHost);
+            std::vector<unsigned long long> h(SW * sp.workers);
+            cudaMemcpy(h.data(), wt, 8 * SW * sp.workers, cudaMemcpyDeviceToHost);
             cudaFree(wt);
-            std::vector<double> st0, en;
             unsigned long long t0 = ~0ull;
-            for (uint64_t w = 0; w < sp.workers; w++) t0 = std::min(t0, h[3 * w]);
-            for (uint64_t w = 0; w < sp.workers; w++) {
-                st0.push_back((h[3 * w] - t0) * 1e-3);
-                en.push_back((h[3 * w + 2] - t0) * 1e-3);
-            }
-            std::vector<double> a = st0, b = en;
-            std::sort(a.begin(), a.end());
-            std::sort(b.begin(), b.end());
-            auto pct = [](const std::vector<double> &v, double q) { return v[(size_t)(q * (v.size() - 1))]; };
+            for (uint64_t w = 0; w < sp.workers; w++) t0 = std::min(t0, h[SW * w]);
+            auto pct = [](std::vector<double> v, double q) {
+                std::sort(v.begin(), v.end());
+                return v[(size_t)(q * (v.size() - 1))];
+            };
             float kms = 0;
             cudaEventSynchronize(v1);
             cudaEventElapsedTime(&kms, v0, v1);
-            std::fprintf(stderr,
-                         "{\"gcr_scan_times\": \"verify\", \"warps\": %llu, \"event_us\": %.1f, \"start_us\": [%.2f, %.2f, "
-                         "%.2f, %.2f], \"end_us\": [%.1f, %.1f, %.1f, %.1f, %.1f]}\n",
-                         (unsigned long long)sp.workers, kms * 1e3, pct(a, 0), pct(a, 0.5), pct(a, 0.99), pct(a, 1),
-                         pct(b, 0), pct(b, 0.1), pct(b, 0.5), pct(b, 0.9), pct(b, 1));
+            std::fprintf(stderr, "{\"gcr_scan_times\": \"verify\", \"warps\": %llu, \"event_us\": %.1f",
+                         (unsigned long long)sp.workers, kms * 1e3);
+            const char *names[5] = {"entry_us", "staged_us", "first_rows_us", "chunk0_us", "exit_us"};
+            for (uint64_t k = 0; k < 5; k++) {
+                std::vector<double> v;
+                for (uint64_t w = 0; w < sp.workers; w++)
+                    if (h[SW * w + k]) v.push_back((h[SW * w + k] - t0) * 1e-3);
+                if (v.empty()) continue;
+                std::fprintf(stderr, ", \"%s\": [%.2f, %.2f, %.2f, %.2f, %.2f]", names[k], pct(v, 0), pct(v, 0.1),
+                             pct(v, 0.5), pct(v, 0.9), pct(v, 1));
+            }
+            std::fprintf(stderr, "}\n");
         }
         CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));
         verify_launches = 1;

@@ -36,6 +36,10 @@ struct AllocDev {
     uint64_t grp0;      // small pages (K1g): global index of its first page group
 };
 
+// GCR_SCAN_TIMES diagnostics: per K1 warp {entry, tables staged, first rows
+// loaded, chunk 0 done, exit} globaltimer stamps (+1 spare).
+constexpr uint32_t kScanStamps = 6;
+
 // Small pages (P = 4 KiB / 8 KiB): K1g scans G = 16 KiB / P consecutive pages
 // of one allocation (a page GROUP, 16 KiB) at once, one page per 32/G lanes,
 // so the per-page lane tree is shared by G pages.
@@ -124,7 +128,7 @@ struct ScanParams {
     const CrcTables *tables;
     uint32_t prefetch;         // bytes: each warp keeps [cursor + prefetch, + block) requested into L2
     const uint64_t *chunk_groups;  // K1g: n_chunks + 1 global page-group boundaries (device)
-    unsigned long long *warp_times;  // optional (GCR_SCAN_TIMES): per warp {start, end} globaltimer ns
+    unsigned long long *warp_times;  // optional (GCR_SCAN_TIMES): kScanStamps globaltimer ns per warp
     uint32_t grp_pf_block;     // K1g: block of a group (0..7) at which the next group is prefetched
 };
 

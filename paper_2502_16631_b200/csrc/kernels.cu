@@ -67,6 +67,8 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kScanPrefetchDefault = GCR_SCAN_PREFETCH_DEFAULT;
 
 enum : uint32_t { kT4 = 0, kA16 = 1, kA32 = 2, kA64 = 3, kA128 = 4, kA256 = 5 };
+// GCR_SCAN_TIMES stamps per warp: entry, tables staged, first rows loaded (chunk 0), chunk 0 done, exit
+constexpr uint32_t kStamps = kScanStamps;
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     uint32_t r;
@@ -561,7 +563,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     const uint32_t lane4 = lane * 4u;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (wid >= p.workers) return;
-    if (p.warp_times && lane == 0) p.warp_times[3 * wid] = t_entry;
+    if (p.warp_times && lane == 0) {
+        p.warp_times[kStamps * wid] = t_entry;
+        p.warp_times[kStamps * wid + 1] = globaltimer_ns();  // tables staged
+    }
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t Rp = P >> kLog2Row;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
@@ -612,6 +617,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u;
             uint4 wa[U], wb[U];
             load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
+            if (p.warp_times && ch == 0) {  // first rows in registers: the range's first HBM round trip
+                uint32_t dep = wa[0].x;
+                asm volatile("mov.b32 %0, %0;" : "+r"(dep));  // wait for the load before the stamp
+                const uint64_t t = globaltimer_ns();
+                if (lane == 0) p.warp_times[kStamps * wid + 2] = t;
+                wa[0].x = dep;
+            }
             while (to_proc > 0) {
                 if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
                 process_rows<U>(p, cc, pc, wa, to_proc, x, acc, small, lane4, sb, lane);
@@ -639,9 +651,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             }
         }
         __syncwarp();
-        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[3 * wid + 1] = globaltimer_ns();
+        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
     }
-    if (p.warp_times && lane == 0) p.warp_times[3 * wid + 2] = globaltimer_ns();
+    if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
 // ---------------------------------------------------------------------------
@@ -703,7 +715,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (wid >= p.workers) return;
-    if (p.warp_times && lane == 0) p.warp_times[3 * wid] = t_entry;
+    if (p.warp_times && lane == 0) {
+        p.warp_times[kStamps * wid] = t_entry;
+        p.warp_times[kStamps * wid + 1] = globaltimer_ns();
+    }
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
         const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
@@ -804,9 +819,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             }
         }
         __syncwarp();
-        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[3 * wid + 1] = globaltimer_ns();
+        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
     }
-    if (p.warp_times && lane == 0) p.warp_times[3 * wid + 2] = globaltimer_ns();
+    if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
 // K0: page -> allocation and tile -> allocation (A1).  One CTA per allocation.
@@ -1044,6 +1059,11 @@ __global__ void k_pm_entries(const AllocDev *allocs, const uint32_t *page_alloc,
 }
 
 // K6: staged image pieces -> allocation pages.  One CTA per descriptor.
+// kPlain (diagnostic GCR_DIAG_SCATTER_PLAIN=1): coherent ld.global instead of
+// the read-only streaming path, to separate tool artefacts from real hazards.
+__device__ __forceinline__ uint4 ld_plain(const void *p) { return *reinterpret_cast<const volatile uint4 *>(p); }
+
+template <bool kPlain>
 __global__ void __launch_bounds__(256) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
     for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const uint64_t dst = desc[i].dst, so = desc[i].src_off, by = desc[i].bytes;
@@ -1055,11 +1075,12 @@ __global__ void __launch_bounds__(256) k_scatter(const ScatterDesc *desc, uint64
         for (; off + (U - 1) * stride < by; off += U * stride) {
             uint4 v[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) v[u] = ldg_stream(src + off + u * stride);
+            for (int u = 0; u < U; u++) v[u] = kPlain ? ld_plain(src + off + u * stride) : ldg_stream(src + off + u * stride);
 #pragma unroll
             for (int u = 0; u < U; u++) *reinterpret_cast<uint4 *>(d + off + u * stride) = v[u];
         }
-        for (; off < by; off += stride) *reinterpret_cast<uint4 *>(d + off) = ldg_stream(src + off);
+        for (; off < by; off += stride)
+            *reinterpret_cast<uint4 *>(d + off) = kPlain ? ld_plain(src + off) : ldg_stream(src + off);
     }
 }
 
@@ -1211,7 +1232,12 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
     uint64_t g = n < (uint64_t)n_sms * 8 ? n : (uint64_t)n_sms * 8;
-    k_scatter<<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
+    static const bool plain = [] {
+        const char *e = std::getenv("GCR_DIAG_SCATTER_PLAIN");
+        return e && e[0] == '1';
+    }();
+    if (plain) k_scatter<true><<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
+    else k_scatter<false><<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
     return launched(1);
 }
 

@@ -162,8 +162,8 @@ def test_corrupted_compressed_pages_restore_like_the_oracle(G, orc):
         s = img.stream()
         v = orc.parse(s)
         stored = v["stored"]
-        data0 = len(s) - v["header"]["image_bytes"]
-        offs = np.concatenate([[0], np.cumsum(stored)])
+        data0 = int(len(s) - v["header"]["image_bytes"])
+        offs = np.concatenate([np.zeros(1, np.int64), np.cumsum(stored, dtype=np.int64)])
         coded = [i for i in range(stored.size) if stored[i] % 16 == 0 and stored[i] < 65536]
         b = bytearray(s)
         b[data0 + offs[coded[0]] + 3] = 9            # malformed: mode 9 -> zero page
