@@ -1061,7 +1061,7 @@ __global__ void k_pm_entries(const AllocDev *allocs, const uint32_t *page_alloc,
 // K6: staged image pieces -> allocation pages.  One CTA per descriptor.
 // kPlain (diagnostic GCR_DIAG_SCATTER_PLAIN=1): coherent ld.global instead of
 // the read-only streaming path, to separate tool artefacts from real hazards.
-__device__ __forceinline__ uint4 ld_plain(const void *p) { return *reinterpret_cast<const volatile uint4 *>(p); }
+__device__ __forceinline__ uint4 ld_plain(const void *p) { return __ldcg(reinterpret_cast<const uint4 *>(p)); }
 
 template <bool kPlain>
 __global__ void __launch_bounds__(256) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
