@@ -382,6 +382,41 @@ def run_ours(args):
             im.free()
     if base_img is not None:
         base_img.free()
+    # f4 on: the same workload without the codec, measured in the same run (context for the headline)
+    plain_cmp = None
+    if args.compress and not incremental and not args.release and not args.storage:
+        ctx2 = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20, n_copy_streams=args.streams,
+                           n_staging_slots=args.slots, compress=0,
+                           direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
+        for t in ts:
+            ctx2.register_tensor(t)
+        ctx2.reserve_host(R0 + (256 << 20))
+        st2 = torch.cuda.ExternalStream(ctx2.stream())
+        t2, ck2, rs2 = [], [], []
+        for k in range(2 + 3):
+            _barrier(pg)
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(st2)
+            ctx2.lock()
+            im2 = ctx2.checkpoint()
+            ctx2.restore([im2])
+            ctx2.unlock()
+            f1.record(st2)
+            im2.free()
+            f1.synchronize()
+            if k >= 2:
+                s2 = ctx2.stats()
+                t2.append(f0.elapsed_time(f1) * 1e-3)
+                ck2.append(s2["checkpoint_ns"] * 1e-9)
+                rs2.append(s2["restore_ns"] * 1e-9)
+        ctx2.close()
+        tt2 = _max_over_ranks(pg, sum(t2))
+        plain_cmp = {"value": round(_sum_over_ranks(pg, float(R)) * len(t2) / tt2 / 1e9, 3),
+                     "ms_per_step": round(tt2 / len(t2) * 1e3, 3), "steps": len(t2),
+                     "checkpoint_GBps": round(R * len(ck2) / sum(ck2) / 1e9, 3),
+                     "restore_GBps": round(R * len(rs2) / sum(rs2) / 1e9, 3),
+                     "what": "the same workload and launch configuration with compress=0 (raw PRESENT pages), "
+                             "measured in this run after the headline steps"}
     t_dev = _max_over_ranks(pg, sum(dev))
     t_host = _max_over_ranks(pg, sum(host))
     t_box = _max_over_ranks(pg, sum(box))
@@ -412,11 +447,13 @@ def run_ours(args):
     pack_b = 2 * (img_b - sc["direct_bytes"])
     rs_last = recs[-1][1]
     scat_b = 2 * (img_b - rs_last["restore_direct_bytes"]) + rs_last["pages_zero"] * w.page_size
+    if args.compress:  # f4: PRESENT pages go through the decode kernel (KD), K6/K7 only zero-fill
+        scat_b = rs_last["pages_zero"] * w.page_size
     kern = {
         "K1_scan": {"dev_ms_per_step": scan_ns / K * 1e-6, "launches_per_step": scan_l / K,
                     "alg_bytes_per_step": R, "GBps": R * K / max(scan_ns, 1)},
-        "K4_pack": {"dev_ms_per_step": pack_ns / K * 1e-6, "alg_bytes_per_step": pack_b,
-                    "GBps": pack_b * K / max(pack_ns, 1)},
+        "K4_pack": None if args.compress else
+        {"dev_ms_per_step": pack_ns / K * 1e-6, "alg_bytes_per_step": pack_b, "GBps": pack_b * K / max(pack_ns, 1)},
         "K6K7_scatter_zero": None if incremental else
         {"dev_ms_per_step": scat_ns / K * 1e-6, "alg_bytes_per_step": scat_b,
          "GBps": scat_b * K / max(scat_ns, 1), "note": "zero bytes counted as pages_zero x page_size (upper bound)"},
@@ -503,6 +540,7 @@ def run_ours(args):
                 "what": "host wall clock of Context.lock/checkpoint/restore/unlock/free via the Python binding"},
         "gpu_launches": int(_sum_over_ranks(pg, float(launches))),
         "paper_context": PAPER_CONTEXT,
+        "uncompressed": plain_cmp,
         "mode": args.mode,
         "chain_restore": chain_restore,
         "probes": probes,
@@ -687,7 +725,7 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--compress", type=int, default=0, choices=[0, 1],
+    ap.add_argument("--compress", type=int, default=1, choices=[0, 1],
                     help="1: f4 page codec (PRESENT pages stored in byte-plane dictionary form, GPU encode/decode)")
     ap.add_argument("--dry-run", action="store_true", help="launch the ranks and report them; no GPU work")
     ap.add_argument("--storage", default=None, help="full mode: directory for the f3 storage tier round trip")

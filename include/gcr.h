@@ -243,6 +243,9 @@ gcr_status gcr_lock(gcr_ctx *ctx);
  * valid: chains).  On any failure the phase stays LOCKED, no image is
  * returned and the parent digest state is unchanged. */
 gcr_status gcr_checkpoint(gcr_ctx *ctx, gcr_mode mode, gcr_image **out);
+/* (checkpoint and restore both first wait for caller work already enqueued on
+ * the watched streams -- or, with none watched, on the whole device -- so they
+ * are ordered after it even though the library's streams are non-blocking.) */
 
 /* CHECKPOINTED -> LOCKED: undo the ctx's LAST checkpoint, whose image `img`
  * is freed, and restore the parent digest state it replaced (the next

@@ -93,6 +93,11 @@ void build_tables(CrcTables *t) {
     for (int d = 1; d < 4096; d++) t->fold_m[d] = apply4(row, t->fold_m[d - 1]);
 }
 
+void table_basis(const uint32_t (&tab)[4][256], uint32_t *basis32) {
+    for (int k = 0; k < 4; k++)
+        for (int i = 0; i < 8; i++) basis32[8 * k + i] = tab[k][1u << i];
+}
+
 // The reflected GF(2) product K1 evaluates lane-parallel (lane k: v * x^k).
 static uint32_t mulmod(uint32_t m, uint32_t v) {
     uint32_t r = 0;

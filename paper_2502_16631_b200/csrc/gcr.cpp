@@ -273,6 +273,7 @@ struct gcr_ctx {
     std::vector<cudaStream_t> copy;
     std::vector<uint8_t *> slots;
     CrcTables *tables_d = nullptr;
+    uint32_t basis[8][32] = {};  // ScanParams::basis rows: braid(512), t4, a16 .. a256, then a128 / a256 for K1g
     PinnedPool pool;
     std::vector<gcr_image *> images;
 
@@ -761,6 +762,13 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     }
     CrcTables *th = new CrcTables;
     build_tables(th);
+    table_basis(th->braid, c->basis[0]);
+    table_basis(th->t4, c->basis[1]);
+    table_basis(th->a16, c->basis[2]);
+    table_basis(th->a32, c->basis[3]);
+    table_basis(th->a64, c->basis[4]);
+    table_basis(th->a128, c->basis[5]);
+    table_basis(th->a256, c->basis[6]);
     if (cudaMalloc(&c->tables_d, sizeof(CrcTables)) != cudaSuccess ||
         cudaMemcpy(c->tables_d, th, sizeof(CrcTables), cudaMemcpyHostToDevice) != cudaSuccess) {
         delete th;
@@ -932,6 +940,30 @@ gcr_status gcr_unlock(gcr_ctx *c) {
     return GCR_OK;
 }
 
+// Order a checkpoint / restore after every piece of caller work already
+// enqueued: the watched streams, or the whole device when none is watched.
+// Under the cooperative lock nothing should be pending, so this is a no-op
+// wait; it makes "write the registered memory, then checkpoint / restore"
+// on another stream (e.g. a test poisoning memory on torch's stream while
+// LOCKED) safe instead of a race with the library's non-blocking streams.
+static gcr_status fence_caller_work(gcr_ctx *c) {
+    if (c->watched.empty()) {
+        CUDA_TRY(c, cudaDeviceSynchronize());
+        return GCR_OK;
+    }
+    for (cudaStream_t s : c->watched) CUDA_TRY(c, cudaStreamSynchronize(s));
+    return GCR_OK;
+}
+
+// The launch's table bases (ScanParams::basis): the braid step is adv_512
+// for K1, adv_{512/G} for K1g (a128 at 4 KiB pages, a256 at 8 KiB).
+static void set_basis(const gcr_ctx *c, ScanParams &sp) {
+    int braid = 0;
+    if (sp.chunk_groups != nullptr) braid = sp.page_size == kGroupBytes / 4 ? 5 : 6;
+    std::memcpy(sp.basis[0], c->basis[braid], sizeof sp.basis[0]);
+    for (int t = 1; t < 7; t++) std::memcpy(sp.basis[t], c->basis[t], sizeof sp.basis[t]);
+}
+
 static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     const uint32_t P = c->P;
     const int cur = c->have_parent ? 1 - c->parent_idx : 0;
@@ -989,6 +1021,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     sp.chunk_done = c->chunk_sync_d + std::max<size_t>(nch, 1);
     const int scan_free = scan_free_sms(mode == GCR_INCREMENTAL);
     sp.workers = scan_workers(c->n_sms, scan_free);
+    set_basis(c, sp);
     std::vector<cudaEvent_t> k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
     cudaEvent_t t0 = c->ev(), k1s = c->ev(), k1m = c->ev();
@@ -1371,6 +1404,8 @@ gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
     CUDA_TRY(c, cudaSetDevice(c->device));
     gcr_status s = build_layout(c);
     if (s != GCR_OK) return s;
+    s = fence_caller_work(c);
+    if (s != GCR_OK) return s;
     gcr_image *img = new (std::nothrow) gcr_image;
     if (!img) return fail(c, GCR_E_NOMEM, "checkpoint: out of host memory");
     img->ctx = c;
@@ -1474,6 +1509,10 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
             return fail(c, GCR_E_CHAIN, "restore: parent_generation link broken");
     }
     CUDA_TRY(c, cudaSetDevice(c->device));
+    {
+        const gcr_status fs = fence_caller_work(c);
+        if (fs != GCR_OK) return fs;
+    }
     st.remap_ns = 0;
     writes_began = true;  // from here on a failure leaves the memory content undefined
     if (c->phase == GCR_RELEASED) {  // back the same VAs again, then apply the chain
@@ -1681,6 +1720,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         sp.verify_count = c->misc_d + 1;
         sp.first_bad = c->misc_d + 2;
         sp.tables = c->tables_d;
+        set_basis(c, sp);
         // GCR_SCAN_TIMES=1: per-warp globaltimer stamps of this verify launch
         // (entry, tables staged, first rows loaded, chunk done, exit),
         // summarised on stderr relative to the earliest entry (diagnostics)

@@ -130,6 +130,13 @@ struct ScanParams {
     const uint64_t *chunk_groups;  // K1g: n_chunks + 1 global page-group boundaries (device)
     unsigned long long *warp_times;  // optional (GCR_SCAN_TIMES): kScanStamps globaltimer ns per warp
     uint32_t grp_pf_block;     // K1g: block of a group (0..7) at which the next group is prefetched
+    // Every table is linear in its byte index (tab[k][e] = adv(e << 8k)), so
+    // the kernel rebuilds it in shared memory from 8 basis values per k:
+    // basis[t][8k + i] = tab_t[k][1 << i], t = 0: the braid table of this
+    // launch (adv_512; K1g: adv_128 / adv_256), 1..6: t4, a16 .. a256.  Kernel
+    // parameters live in the constant bank: no 148-SM burst on the same L2
+    // lines at launch (the global-table staging cost ~4.8 us per launch).
+    uint32_t basis[7][32];
 };
 
 struct ScatterDesc {
@@ -202,6 +209,8 @@ int launch_codec_decode(const DecodeDesc *desc, uint64_t n_desc, const uint8_t *
 
 // ---- host CRC32C math (crc_host.cpp), independent of oracle/ --------------
 void build_tables(CrcTables *out);
+// basis[8k + i] = tab[k][1 << i] of a 4x256 table (see ScanParams::basis)
+void table_basis(const uint32_t (&tab)[4][256], uint32_t *basis32);
 uint32_t zero_digest(uint64_t n);                 // Z(n)
 uint32_t crc_shift(uint32_t reg, uint64_t nbytes);  // adv_nbytes(reg): reg(s, A|B) = crc_shift(reg(s, A), |B|) ^ reg(0, B)
 uint32_t host_crc32c_update(uint32_t state, const void *p, uint64_t n);  // raw register update

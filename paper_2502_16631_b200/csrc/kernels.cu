@@ -511,32 +511,31 @@ __device__ __forceinline__ void process_rows(const ScanParams &p, const ChunkCtx
     if (pc.vr == Rp) page_end(p, cc, pc, x, acc, small, lane);
 }
 
-// Stage the tables in shared memory: the braid table `gb` (adv_{row}) into
-// all 32 lane-private replicas (word (k>>1)*16384 + e*64 + (k&1)*32 + l) and
-// the small tables (t4, a16 .. a256) once.  Each thread loads a few table
-// words (all loads issued before any store).
-__device__ __forceinline__ void stage_tables(uint32_t *sm, const CrcTables *tables, const uint32_t *gb) {
-    const uint32_t *gs = &tables->t4[0][0];  // t4, a16, ..., a256 are contiguous
+// Build the tables in shared memory from the launch's basis vectors
+// (ScanParams::basis, constant bank): entry e of table k = XOR of basis[8k + i]
+// over the set bits i of e.  The braid table goes into all 32 lane-private
+// replicas (word (k>>1)*16384 + e*64 + (k&1)*32 + l), the small tables (t4,
+// a16 .. a256) once.  Every warp works on one k at a time (k is warp-uniform),
+// so the basis reads are constant-bank broadcasts.
+__device__ __forceinline__ uint32_t tab_entry(const uint32_t *b32, uint32_t k, uint32_t e) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+        if ((e >> i) & 1u) v ^= b32[8 * k + i];
+    return v;
+}
+
+__device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) {
     constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
     constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
-    uint32_t bv[kPer], sv[kPerS];
-#pragma unroll
-    for (uint32_t j = 0; j < kPer; j++) {
-        const uint32_t ke = threadIdx.x + j * kScanThreads;
-        bv[j] = ke < 1024u ? __ldg(gb + ke) : 0u;
-    }
-#pragma unroll
-    for (uint32_t j = 0; j < kPerS; j++) {
-        const uint32_t i = threadIdx.x + j * kScanThreads;
-        sv[j] = i < kSmallTables * 1024u ? __ldg(gs + i) : 0u;
-    }
 #pragma unroll
     for (uint32_t j = 0; j < kPer; j++) {
         const uint32_t ke = threadIdx.x + j * kScanThreads;
         if (ke < 1024u) {
             const uint32_t k = ke >> 8, e = ke & 255u;
+            const uint32_t v = tab_entry(p.basis[0], k, e);
             uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
-            const uint4 v4 = make_uint4(bv[j], bv[j], bv[j], bv[j]);
+            const uint4 v4 = make_uint4(v, v, v, v);
 #pragma unroll
             for (int l = 0; l < 8; l++) dst[l] = v4;
         }
@@ -545,7 +544,7 @@ __device__ __forceinline__ void stage_tables(uint32_t *sm, const CrcTables *tabl
 #pragma unroll
     for (uint32_t j = 0; j < kPerS; j++) {
         const uint32_t i = threadIdx.x + j * kScanThreads;
-        if (i < kSmallTables * 1024u) ss[i] = sv[j];
+        if (i < kSmallTables * 1024u) ss[i] = tab_entry(p.basis[1 + (i >> 10)], (i >> 8) & 3u, i & 255u);
     }
 }
 
@@ -556,12 +555,28 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     const uint32_t *small = sm + kBraidSmem / 4;
 
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
-    stage_tables(sm, p.tables, &p.tables->braid[0][0]);
-    __syncthreads();
-
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lane4 = lane * 4u;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    // Before building the tables: request the first bytes of this warp's
+    // chunk-0 range into L2, so the first loads after staging hit L2 instead
+    // of paying the HBM round trip (real rows of an allocation are contiguous:
+    // row r lives at base + (r - row0) * 512).
+    if (p.prefetch != 0u && p.n_chunks != 0 && wid < p.workers) {
+        const uint64_t rb = p.chunk_rows[0], rows = p.chunk_rows[1] - rb;
+        const uint64_t r = rb + rows * wid / p.workers, re = rb + rows * (wid + 1) / p.workers;
+        if (r < re) {
+            const AllocDev *al = p.allocs + alloc_of_row(p.allocs, p.n_allocs, r, lane);
+            if (lane == 0) {
+                const uint64_t a0 = __ldg(&al->base) + ((r - __ldg(&al->row0)) << kLog2Row);
+                const uint64_t e = min(min(a0 + p.prefetch, __ldg(&al->base) + __ldg(&al->bytes)),
+                                       a0 + ((re - r) << kLog2Row));
+                if (e > a0) prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(e - a0));
+            }
+        }
+    }
+    stage_tables(sm, p);
+    __syncthreads();
     if (wid >= p.workers) return;
     if (p.warp_times && lane == 0) {
         p.warp_times[kStamps * wid] = t_entry;
@@ -709,11 +724,23 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t *small = sm + kBraidSmem / 4;
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
-    stage_tables(sm, p.tables, G == 4 ? &p.tables->a128[0][0] : &p.tables->a256[0][0]);
-    __syncthreads();
-
     const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    // before building the tables: the warp's first group of chunk 0 into L2
+    if (p.prefetch != 0u && p.n_chunks != 0 && wid < p.workers) {
+        const uint64_t cb = p.chunk_groups[0], n = p.chunk_groups[1] - cb;
+        const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
+        if (g0 < g1) {
+            const AllocDev *al = p.allocs + alloc_of_group(p.allocs, p.n_allocs, g0, lane);
+            if (lane == 0) {
+                const uint64_t a0 = __ldg(&al->base) + ((g0 - __ldg(&al->grp0)) * G << p.log2_page);
+                const uint64_t e = min(a0 + (uint64_t)G * p.page_size, __ldg(&al->base) + __ldg(&al->bytes));
+                if (e > a0) prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(e - a0));
+            }
+        }
+    }
+    stage_tables(sm, p);  // the host put adv_{512/G} (a128 / a256) in basis[0]
+    __syncthreads();
     if (wid >= p.workers) return;
     if (p.warp_times && lane == 0) {
         p.warp_times[kStamps * wid] = t_entry;
