@@ -1758,6 +1758,25 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                 std::fprintf(stderr, ", \"%s\": [%.2f, %.2f, %.2f, %.2f, %.2f]", names[k], pct(v, 0), pct(v, 0.1),
                              pct(v, 0.5), pct(v, 0.9), pct(v, 1));
             }
+            // per-SM mean exit time: is the tail a few slow SMs or spread evenly?
+            {
+                std::vector<double> sum(256, 0.0), cnt(256, 0.0);
+                for (uint64_t w = 0; w < sp.workers; w++) {
+                    const uint64_t sid = h[SW * w + 5] & 255u;
+                    sum[sid] += (h[SW * w + 4] - t0) * 1e-3;
+                    cnt[sid] += 1;
+                }
+                std::vector<std::pair<double, int>> sms;
+                for (int i = 0; i < 256; i++)
+                    if (cnt[i] > 0) sms.emplace_back(sum[i] / cnt[i], i);
+                std::sort(sms.begin(), sms.end());
+                std::fprintf(stderr, ", \"sm_exit_mean_us\": {\"fastest\": [%d, %.2f], \"median\": %.2f, \"slowest\": [",
+                             sms.front().second, sms.front().first, sms[sms.size() / 2].first);
+                for (size_t i = sms.size() >= 8 ? sms.size() - 8 : 0; i < sms.size(); i++)
+                    std::fprintf(stderr, "%s[%d, %.2f]", i + 8 == sms.size() || (sms.size() < 8 && i == 0) ? "" : ", ",
+                                 sms[i].second, sms[i].first);
+                std::fprintf(stderr, "]}");
+            }
             std::fprintf(stderr, "}\n");
         }
         CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));

@@ -526,26 +526,22 @@ __device__ __forceinline__ uint32_t tab_entry(const uint32_t *b32, uint32_t k, u
 }
 
 __device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) {
-    constexpr uint32_t kPer = (1024u + kScanThreads - 1) / kScanThreads;
-    constexpr uint32_t kPerS = (kSmallTables * 1024u + kScanThreads - 1) / kScanThreads;
-#pragma unroll
-    for (uint32_t j = 0; j < kPer; j++) {
-        const uint32_t ke = threadIdx.x + j * kScanThreads;
-        if (ke < 1024u) {
-            const uint32_t k = ke >> 8, e = ke & 255u;
-            const uint32_t v = tab_entry(p.basis[0], k, e);
-            uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u);
-            const uint4 v4 = make_uint4(v, v, v, v);
-#pragma unroll
-            for (int l = 0; l < 8; l++) dst[l] = v4;
-        }
+    // Braid table: the 32 replicas of entry (k, e) are 128 contiguous bytes;
+    // 8 threads write them with one 16-B store each, so every 8-lane phase of a
+    // warp's STS.128 covers 128 contiguous bytes (no bank conflict).  (Thread
+    // per entry, 8 stores each, put all lanes of a phase on the same 4 banks:
+    // 8-way conflicts, ~4 us per launch.)
+    constexpr uint32_t kGroups = kScanThreads / 8;
+    const uint32_t sub = threadIdx.x & 7u;
+    for (uint32_t ke = threadIdx.x >> 3; ke < 1024u; ke += kGroups) {
+        const uint32_t k = ke >> 8, e = ke & 255u;
+        const uint32_t v = tab_entry(p.basis[0], k, e);
+        uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u) + sub;
+        *dst = make_uint4(v, v, v, v);
     }
     uint32_t *ss = sm + kBraidSmem / 4;
-#pragma unroll
-    for (uint32_t j = 0; j < kPerS; j++) {
-        const uint32_t i = threadIdx.x + j * kScanThreads;
-        if (i < kSmallTables * 1024u) ss[i] = tab_entry(p.basis[1 + (i >> 10)], (i >> 8) & 3u, i & 255u);
-    }
+    for (uint32_t i = threadIdx.x; i < kSmallTables * 1024u; i += kScanThreads)
+        ss[i] = tab_entry(p.basis[1 + (i >> 10)], (i >> 8) & 3u, i & 255u);
 }
 
 // K1.
@@ -579,8 +575,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     __syncthreads();
     if (wid >= p.workers) return;
     if (p.warp_times && lane == 0) {
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
         p.warp_times[kStamps * wid] = t_entry;
         p.warp_times[kStamps * wid + 1] = globaltimer_ns();  // tables staged
+        p.warp_times[kStamps * wid + 5] = smid;
     }
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t Rp = P >> kLog2Row;
