@@ -265,6 +265,7 @@ def run_ours(args):
     w = synth.make_workload(args.config, rank=rank, page_size=args.page_size, gib=args.gib)
     ctx = gcr.Context(local, page_size=w.page_size, chunk_bytes=args.chunk_mb << 20,
                       n_copy_streams=args.streams, n_staging_slots=args.slots, compress=args.compress,
+                      in_scan_pack=args.in_scan_pack,
                       direct_min_bytes=(1 << 64) - 1 if args.direct_min_mb < 0 else int(args.direct_min_mb * (1 << 20)))
     # --release: the state lives in one releasable gcr_mem_alloc block, carved
     # into the workload's allocations (f2: checkpoint frees the HBM, restore
@@ -506,6 +507,7 @@ def run_ours(args):
                    "dirty_fraction": args.dirty if incremental else None, "registered_bytes_per_rank": R,
                    "allocations": len(w.allocs), "page_size": w.page_size, "chunk_bytes": args.chunk_mb << 20,
                    "compress": "f4 byte-plane dictionary code (R-19)" if args.compress else None,
+                   "in_scan_pack": args.in_scan_pack,
                    "copy_streams": args.streams, "staging_slots": args.slots or args.streams, "direct_min_bytes": int(args.direct_min_mb * (1 << 20)) if args.direct_min_mb >= 0 else None,
                    "parallelism": f"independent ranks x{world} (gloo control plane)",
                    "l2": "inputs larger than L2 (registered state >> 126 MB; no flush needed)"},
@@ -725,6 +727,9 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--in-scan-pack", type=int, default=1, choices=[0, 1, 2],
+                    help="f1: 1 = incremental checkpoints written by the scan kernel itself (default), 0 = staged "
+                         "pipeline, 2 = every checkpoint")
     ap.add_argument("--compress", type=int, default=1, choices=[0, 1],
                     help="1: f4 page codec (PRESENT pages stored in byte-plane dictionary form, GPU encode/decode)")
     ap.add_argument("--dry-run", action="store_true", help="launch the ranks and report them; no GPU work")

@@ -78,7 +78,8 @@ struct PinnedPool {
     bool add_slab(uint64_t bytes) {
         auto t0 = Clock::now();
         void *p = nullptr;
-        if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        // mapped: the f1 in-scan pack writes image data from the scan kernel
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
             cudaGetLastError();
             return false;
         }
@@ -301,6 +302,11 @@ struct gcr_ctx {
     // offsets, presence masks of one chunk's pages), the image's compact
     // stored-length table, and each chunk's stored total (mapped pinned)
     std::vector<uint32_t *> cx_scratch;
+    // f1 in-scan pack (cfg.in_scan_pack): per-CTA aggregates, chunk bases,
+    // per-warp page lists, error word (InScanPack)
+    unsigned long long *isp_cta = nullptr, *isp_base = nullptr, *isp_err = nullptr;
+    uint32_t *isp_ready = nullptr, *isp_list = nullptr;
+    uint32_t isp_cap = 0;
     uint64_t cx_pages = 0;  // pages per chunk at most (chunk_bytes / P)
     uint32_t *stored_d = nullptr;
     unsigned long long *ctot_h = nullptr, *ctot_map = nullptr;
@@ -385,6 +391,11 @@ void free_layout(gcr_ctx *c) {
     for (uint32_t *p : c->cx_scratch)
         if (p) cudaFree(p);
     c->cx_scratch.clear();
+    for (void *p : {(void *)c->isp_cta, (void *)c->isp_base, (void *)c->isp_err, (void *)c->isp_ready,
+                    (void *)c->isp_list})
+        if (p) cudaFree(p);
+    c->isp_cta = c->isp_base = c->isp_err = nullptr;
+    c->isp_ready = c->isp_list = nullptr;
     if (c->stored_d) cudaFree(c->stored_d);
     c->stored_d = nullptr;
     if (c->ctot_h) cudaFreeHost(c->ctot_h);
@@ -575,6 +586,25 @@ gcr_status build_layout(gcr_ctx *c) {
     CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->nent_map), c->nent_h, 0));
     CUDA_TRY(c, cudaMalloc(&c->misc_d, 8 * 4));
     CUDA_TRY(c, cudaHostAlloc(&c->misc_h, 8 * 4, cudaHostAllocDefault));
+    if (c->cfg.in_scan_pack) {  // f1 buffers, sized for the narrowest K1 grid (incremental: most rows per warp)
+        const uint64_t w_min = scan_workers(c->n_sms, scan_free_sms(true));
+        const uint64_t w_max = scan_workers(c->n_sms, 0);
+        uint64_t max_rows = 0;
+        for (const Chunk &ch : c->chunks) max_rows = std::max(max_rows, ch.row_end - ch.row_begin);
+        // pages one warp can finalize in a chunk: its rows' worth + the pages cut at both ends
+        uint64_t cap = (max_rows + w_min - 1) / w_min * kRowBytes / P + 3;
+        if (grp) cap = std::max<uint64_t>(cap, ((max_rows * kRowBytes / kGroupBytes) + w_min - 1) / w_min * G + 2 * G);
+        c->isp_cap = (uint32_t)cap;
+        const uint64_t ctas = (w_max + 19) / 20 + 1;
+        CUDA_TRY(c, cudaMalloc(&c->isp_cta, 8 * 2 * ctas));
+        CUDA_TRY(c, cudaMemset(c->isp_cta, 0, 8 * 2 * ctas));
+        CUDA_TRY(c, cudaMalloc(&c->isp_base, 8 * (nch + 2)));
+        CUDA_TRY(c, cudaMemset(c->isp_base, 0, 8 * (nch + 2)));
+        CUDA_TRY(c, cudaMalloc(&c->isp_ready, 4 * (nch + 2)));
+        CUDA_TRY(c, cudaMemset(c->isp_ready, 0, 4 * (nch + 2)));
+        CUDA_TRY(c, cudaMalloc(&c->isp_err, 8));
+        CUDA_TRY(c, cudaMalloc(&c->isp_list, 4 * 2 * w_max * cap));
+    }
     if (c->cfg.compress) {  // f4 scratch: {plan, offsets, 32 mask words} per page of a chunk, per slot
         c->cx_pages = c->cfg.chunk_bytes / P;
         for (size_t k = 0; k < c->slots.size(); k++) {
@@ -712,7 +742,7 @@ gcr_status gcr_config_default(gcr_config *out) {
     out->lock_timeout_ms = 10000;
     out->direct_min_bytes = 16ull << 20;
     out->compress = 0;
-    out->reserved0 = 0;
+    out->in_scan_pack = 1;
     return GCR_OK;
 }
 
@@ -724,7 +754,7 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     if (cfg_in) cfg = *cfg_in;
     if (!valid_page_size(cfg.page_size) || cfg.n_copy_streams < 1 || cfg.n_copy_streams > 8 ||
         cfg.chunk_bytes == 0 || cfg.chunk_bytes % cfg.page_size != 0 || cfg.chunk_bytes % kTileBytes != 0 ||
-        cfg.chunk_bytes > kMaxChunk || cfg.compress > 1 ||
+        cfg.chunk_bytes > kMaxChunk || cfg.compress > 1 || cfg.in_scan_pack > 2 ||
         (cfg.n_staging_slots != 0 && (cfg.n_staging_slots < cfg.n_copy_streams || cfg.n_staging_slots > 16)))
         return GCR_E_INVAL;
     if (!crc_self_test()) return GCR_E_INVAL;
@@ -1022,6 +1052,21 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     const int scan_free = scan_free_sms(mode == GCR_INCREMENTAL);
     sp.workers = scan_workers(c->n_sms, scan_free);
     set_basis(c, sp);
+    // f1: the scan writes PRESENT pages straight into the mapped image
+    const bool isp = !coded && (c->cfg.in_scan_pack == 2 || (c->cfg.in_scan_pack == 1 && mode == GCR_INCREMENTAL));
+    if (isp) {
+        void *dimg = nullptr;
+        CUDA_TRY(c, cudaHostGetDevicePointer(&dimg, img->data, 0));
+        sp.isp.img = static_cast<uint8_t *>(dimg);
+        sp.isp.cta_agg = c->isp_cta;
+        sp.isp.base = c->isp_base;
+        sp.isp.base_ready = c->isp_ready;
+        sp.isp.list = c->isp_list;
+        sp.isp.cap = c->isp_cap;
+        sp.isp.err = c->isp_err;
+        sp.isp_page_alloc = c->page_alloc;
+        CUDA_TRY(c, cudaMemsetAsync(c->isp_err, 0, 8, c->compute));
+    }
     std::vector<cudaEvent_t> k2s(nch), tot(nch), pks(nch), pke(nch), dde(nch);
     static const bool trace = std::getenv("GCR_TRACE") != nullptr;
     cudaEvent_t t0 = c->ev(), k1s = c->ev(), k1m = c->ev();
@@ -1044,7 +1089,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         CUDA_TRY(c, cudaEventRecord(k2s[i], c->post));
         LAUNCH_TRY(c, launch_tile_scan(c->tile_info, ch.tile_begin, ch.tile_end, sp.chunk_done, (uint32_t)i, sp.epoch,
                                        c->tile_rec_map + ch.tile_begin, c->rec_count_map + i, c->totals_map + i,
-                                       c->post));
+                                       isp ? c->isp_base : nullptr, isp ? c->isp_ready : nullptr, c->post));
         CUDA_TRY(c, cudaEventRecord(tot[i], c->post));
         return GCR_OK;
     };
@@ -1113,7 +1158,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         StageItem *items = c->stage_h + ch.tile_begin;
         uint32_t n_items = 0;
         bool any_staged = false;
-        if (T.image_bytes && !coded) {
+        if (T.image_bytes && !coded && !isp) {
             std::memset(flags, 0, ch.tile_end - ch.tile_begin);
             Run run{0, 0, 0, 0, 0};
             bool open = false;
@@ -1225,8 +1270,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
             chunk_stored = *reinterpret_cast<volatile unsigned long long *>(c->ctot_h + i);
             if (chunk_stored > T.image_bytes) return fail(c, GCR_E_CUDA, "checkpoint: coded chunk larger than its pages");
             staged.emplace_back(0, chunk_stored);
-        } else if (coded) {
+        } else if (coded || isp) {  // f1: K1 itself writes the chunk's pages into the image
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
+            if (isp) staged_bytes += T.image_bytes;
         } else if (any_staged) {  // slot i mod NS was last drained by chunk i - NS
             if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
@@ -1304,8 +1350,14 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         CUDA_TRY(c, cudaEventRecord(e, c->copy[s]));
         CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
     }
+    if (isp) {  // f1: the kernel's own consistency: no wait timed out, no list overflowed, bases add up
+        CUDA_TRY(c, cudaMemcpyAsync(c->misc_h, c->isp_err, 8, cudaMemcpyDeviceToHost, c->compute));
+        CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 3, c->isp_base + nch, 8, cudaMemcpyDeviceToHost, c->compute));
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->compute));
     st.drain_ns = ns_since(drain0);
+    if (isp && (c->misc_h[0] != 0 || (nch && c->misc_h[3] != base)))
+        return fail(c, GCR_E_CUDA, "checkpoint: in-scan pack failed (wait timeout, list overflow or offset mismatch)");
     const double host_synced = ns_since(host0) * 1e-6;
 
     // stats from the events

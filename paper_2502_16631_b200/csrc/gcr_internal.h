@@ -101,6 +101,29 @@ struct CrcTables {
     uint32_t fold_m[4096];
 };
 
+// f1 in-scan pack (incremental checkpoints, gcr_config.pack_mode = 1;
+// SURVEY §8(f) f1): K1 itself writes every PRESENT page straight into the
+// pinned host image through mapped memory -- no K4 pack, no staging slot, no
+// D2H of page data.  A page's image offset = base[c] (the chunk's first
+// PRESENT byte: K2(c - 1) computes base[c] = base[c - 1] + its chunk total)
+// + the PRESENT bytes finalized in chunk c by earlier CTAs (per-CTA aggregates
+// published by each CTA's last warp to finish the chunk) + those of earlier
+// warps of the same CTA (shared memory) + the warp's own earlier pages.  A
+// warp finalizes pages in page order and the pages it finalizes form a
+// contiguous run in page order, so these groups tile the image in order.  The
+// write-out of chunk c is deferred until the warp has scanned chunk c + 1 (by
+// then every aggregate of chunk c is published); the last chunk's right after
+// it.
+struct InScanPack {
+    uint8_t *img;                // device-visible address of the image data (null: off)
+    unsigned long long *cta_agg; // [2][n_ctas]: epoch << 40 | PRESENT bytes finalized by the CTA (chunk parity)
+    unsigned long long *base;    // [n_chunks + 1] image offset of each chunk (base[0] = 0), written by K2
+    uint32_t *base_ready;        // [n_chunks + 1] epoch once base[c] is written
+    uint32_t *list;              // [2][workers][cap] PRESENT pages the warp finalized, in page order
+    uint32_t cap;
+    unsigned long long *err;     // set to 1 on a wait timeout or a list overflow (checkpoint fails)
+};
+
 // K1 is ONE persistent launch per checkpoint (or verify): every warp walks
 // the chunks in order, taking its equal share of each chunk's real rows.  The
 // last warp to finish chunk c publishes chunk_done[c] = epoch, on which K2(c),
@@ -137,6 +160,8 @@ struct ScanParams {
     // parameters live in the constant bank: no 148-SM burst on the same L2
     // lines at launch (the global-table staging cost ~4.8 us per launch).
     uint32_t basis[7][32];
+    InScanPack isp;            // f1 (img == nullptr: off)
+    const uint32_t *isp_page_alloc;  // f1: page -> allocation (K0's table)
 };
 
 struct ScatterDesc {
@@ -171,9 +196,11 @@ uint32_t grp_prefetch_block();                                      // K1g prefe
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1 (K1g when p.chunk_groups is set)
 bool scan_uses_groups(uint32_t page_size);                          // K1g for this page size?
 // K2 of one chunk: first waits (bounded) until chunk_done[chunk] == epoch.
+// f1: if isp_base is set, K2(c) also writes isp_base[c + 1] = isp_base[c] +
+// the chunk's PRESENT bytes and isp_ready[c + 1] = epoch.
 int launch_tile_scan(TileInfo *tile_info, uint64_t tile_begin, uint64_t tile_end, const uint32_t *chunk_done,
                      uint32_t chunk, uint32_t epoch, TileRec *host_rec, unsigned long long *rec_count,
-                     ChunkTotals *totals_host, cudaStream_t st);
+                     ChunkTotals *totals_host, unsigned long long *isp_base, uint32_t *isp_ready, cudaStream_t st);
 int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_t *cls, uint64_t tile_begin,
                 uint32_t page_size, uint32_t log2_page, uint8_t *slot, const StageItem *items, uint32_t n_items,
                 int n_sms, int scan_free, const uint32_t *scan_done, uint32_t epoch, uint32_t *decision,

@@ -153,7 +153,7 @@ __device__ __forceinline__ uint64_t tile_of_page(uint64_t tile0, uint64_t pi, ui
 // c.1 steps 3-5 for one page given its raw register and non-zero flag (or
 // the A9 verify comparison), plus the per-tile compaction counters that K2
 // turns into image offsets and chunk totals.  Executed by one lane.
-__device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, uint64_t tile, bool alloc_start,
+__device__ __forceinline__ bool finalize_page(const ScanParams &p, uint64_t g, uint64_t tile, bool alloc_start,
                                               uint32_t len, uint32_t zlen, uint32_t raw, bool nz) {
     const uint32_t d = raw ^ zlen;
     if (p.mode == kScanVerify) {
@@ -161,7 +161,7 @@ __device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, u
             atomicAdd(p.verify_count, 1ull);
             atomicMin(p.first_bad, (unsigned long long)g);
         }
-        return;
+        return false;
     }
     uint8_t c;
     uint32_t inc;
@@ -179,6 +179,141 @@ __device__ __forceinline__ void finalize_page(const ScanParams &p, uint64_t g, u
     atomicAdd(&p.tile_info[tile].counts, inc);
     p.d_out[g] = d;
     p.cls[g] = c | (alloc_start ? kClsAllocStart : 0);
+    return c == kClsPresent;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---- f1 in-scan pack (InScanPack, gcr_internal.h) ---------------------------
+// Lane-held accumulator of the PRESENT pages a warp finalized in the current
+// chunk (K1: lane 0's copy; K1g: every lane's, warp-uniform).
+struct IspAcc {
+    unsigned long long bytes;
+    uint32_t n;
+};
+
+__device__ __forceinline__ uint32_t *isp_list(const ScanParams &p, uint32_t par, uint64_t wid) {
+    return p.isp.list + (par * p.workers + wid) * (uint64_t)p.isp.cap;
+}
+
+// One finalized PRESENT page (executed by the lane that finalized it).
+__device__ __forceinline__ void isp_note(const ScanParams &p, IspAcc &acc, uint32_t *list, uint64_t g, uint32_t len) {
+    if (acc.n < p.isp.cap) list[acc.n] = (uint32_t)g;
+    else *reinterpret_cast<volatile unsigned long long *>(p.isp.err) = 1ull;
+    acc.n++;
+    acc.bytes += len;
+}
+
+constexpr uint64_t kIspWaitNs = 30ull * 1000000000ull;
+
+__device__ __forceinline__ uint64_t isp_tag(uint32_t epoch, uint32_t ch) {
+    return ((uint64_t)(epoch & 0xFFFFu) << 48) | ((uint64_t)(ch & 0xFFFFu) << 32);
+}
+
+// Per-CTA shared state of the in-scan pack (two chunk parities).
+struct IspShared {
+    unsigned long long wagg[2][32];  // PRESENT bytes each warp finalized
+    unsigned long long wpfx[2][32];  // exclusive prefix of those inside the CTA
+    uint32_t wn[2][32];              // pages in each warp's list
+    uint32_t cnt[2];                 // warps of the CTA done with the chunk
+    uint32_t ready[2];               // ch + 1 once wpfx of the chunk is written
+    uint32_t pad[28];
+};
+
+// End of chunk ch for this warp: publish its aggregate in the CTA; the CTA's
+// last warp writes the in-CTA prefixes and the CTA aggregate (global).
+__device__ __forceinline__ void isp_chunk_end(const ScanParams &p, IspShared &ss, IspAcc &acc, uint32_t ch,
+                                              uint32_t lane) {
+    const uint32_t par = ch & 1u, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t arrived = 0;
+    if (lane == 0) {
+        ss.wagg[par][wib] = acc.bytes;
+        ss.wn[par][wib] = acc.n;
+        __threadfence_block();
+        arrived = atomicAdd(&ss.cnt[par], 1u);
+    }
+    arrived = __shfl_sync(kFull, arrived, 0);
+    if (arrived == nw - 1) {  // the CTA's last warp for this chunk
+        __threadfence_block();
+        const unsigned long long v = lane < nw ? *reinterpret_cast<volatile unsigned long long *>(&ss.wagg[par][lane]) : 0ull;
+        unsigned long long inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long o = __shfl_up_sync(kFull, inc, d);
+            if (lane >= (uint32_t)d) inc += o;
+        }
+        if (lane < nw) ss.wpfx[par][lane] = inc - v;
+        const unsigned long long tot = __shfl_sync(kFull, inc, nw - 1);
+        if (lane == 0) {
+            ss.cnt[par] = 0;
+            p.isp.cta_agg[par * gridDim.x + blockIdx.x] = isp_tag(p.epoch, ch) | tot;
+            __threadfence();
+            __threadfence_block();
+            *reinterpret_cast<volatile uint32_t *>(&ss.ready[par]) = ch + 1;
+        }
+    }
+    acc.bytes = 0;
+    acc.n = 0;
+}
+
+// Write chunk ch's PRESENT pages finalized by this warp into the image.
+__device__ __forceinline__ void isp_write(const ScanParams &p, IspShared &ss, uint32_t ch, uint64_t wid,
+                                          uint32_t lane) {
+    const uint32_t par = ch & 1u, wib = threadIdx.x >> 5;
+    const uint64_t t0 = globaltimer_ns();
+    bool ok = true;
+    // the in-CTA prefix of this chunk
+    while (*reinterpret_cast<volatile uint32_t *>(&ss.ready[par]) != ch + 1u)
+        if (globaltimer_ns() - t0 > kIspWaitNs) { ok = false; break; }
+    // PRESENT bytes of the earlier CTAs (their aggregates carry this chunk's tag)
+    unsigned long long before = 0;
+    const uint64_t tag = isp_tag(p.epoch, ch);
+    for (uint32_t b = lane; ok && b < blockIdx.x; b += 32u) {
+        unsigned long long v;
+        while (((v = *reinterpret_cast<volatile unsigned long long *>(p.isp.cta_agg + par * gridDim.x + b)) >> 32) !=
+               tag >> 32)
+            if (globaltimer_ns() - t0 > kIspWaitNs) { ok = false; break; }
+        before += v & 0xFFFFFFFFull;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) before += __shfl_xor_sync(kFull, before, d);
+    // the chunk's image offset, from K2 of the previous chunk
+    if (ch != 0)
+        while (*reinterpret_cast<volatile uint32_t *>(p.isp.base_ready + ch) != p.epoch)
+            if (globaltimer_ns() - t0 > kIspWaitNs) { ok = false; break; }
+    ok = __all_sync(kFull, ok);
+    if (!ok) {
+        if (lane == 0) *reinterpret_cast<volatile unsigned long long *>(p.isp.err) = 1ull;
+        return;
+    }
+    __threadfence();
+    unsigned long long off = (ch ? *reinterpret_cast<volatile unsigned long long *>(p.isp.base + ch) : 0ull) + before +
+                             ss.wpfx[par][wib];
+    const uint32_t n = min(ss.wn[par][wib], p.isp.cap);
+    const uint32_t *list = isp_list(p, par, wid);
+    const uint32_t P = p.page_size, lg = p.log2_page;
+    for (uint32_t k = 0; k < n; k++) {
+        const uint64_t g = __ldg(list + k);
+        const AllocDev *al = p.allocs + __ldg(p.isp_page_alloc + g);
+        const uint64_t pi = g - __ldg(&al->page0);
+        const uint32_t len = pi == (uint64_t)__ldg(&al->n_pages) - 1 ? __ldg(&al->tail_len) : P;
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(__ldg(&al->base) + (pi << lg));
+        uint8_t *dst = p.isp.img + off;
+        uint32_t o = lane * 16u;
+        for (; o + 3 * 512u < len; o += 4 * 512u) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) v[u] = ldg_stream(src + o + u * 512u);
+#pragma unroll
+            for (int u = 0; u < 4; u++) *reinterpret_cast<uint4 *>(dst + o + u * 512u) = v[u];
+        }
+        for (; o < len; o += 512u) *reinterpret_cast<uint4 *>(dst + o) = ldg_stream(src + o);
+        off += len;
+    }
 }
 
 // GF(2) product m (*) v mod P in the reflected representation (bit 31 = x^0):
@@ -196,10 +331,13 @@ __device__ __forceinline__ uint32_t warp_mulmod(uint32_t m, uint32_t v, uint32_t
     return t;
 }
 
-// The chunk a warp is scanning: its real rows and its fold slots.
+// The chunk a warp is scanning: its real rows and its fold slots (+ f1: the
+// warp's list of finalized PRESENT pages and its accumulator, lane 0's copy).
 struct ChunkCtx {
     uint64_t rb, rows;  // first global real row, real rows
     unsigned long long *fs;  // fold slots of this chunk (one per warp)
+    uint32_t *ilist;         // f1: this warp's list for this chunk (null: off)
+    IspAcc acc;
 };
 
 // A piece of a cut page arrives at the page's owner slot (executed by one
@@ -207,7 +345,7 @@ struct ChunkCtx {
 // 64-bit CAS folds {XOR contribution, + rows, + non-zero} (FoldSlots); the
 // arrival that completes the page's Rp - r0 real rows finalizes it from its
 // own CAS result.
-__device__ __forceinline__ void fold_arrive(const ScanParams &p, const ChunkCtx &cc, uint64_t g, uint32_t a,
+__device__ __forceinline__ void fold_arrive(const ScanParams &p, ChunkCtx &cc, uint64_t g, uint32_t a,
                                             uint32_t pi, uint32_t r0, uint32_t rows, uint32_t contrib, bool nz) {
     const uint32_t P = p.page_size, lg = p.log2_page, Rp = P >> kLog2Row;
     const AllocDev *al = p.allocs + a;
@@ -228,8 +366,11 @@ __device__ __forceinline__ void fold_arrive(const ScanParams &p, const ChunkCtx 
     *slot = 0ull;  // every piece arrived: the slot is free for the next launch
     const uint32_t n_pages = __ldg(&al->n_pages);
     const bool tail = pi == n_pages - 1;
-    finalize_page(p, g, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, tail ? __ldg(&al->tail_len) : P,
-                  tail ? __ldg(&al->z_tail) : p.z_page, (uint32_t)nv, (nv >> 48) != 0ull);
+    const uint32_t len = tail ? __ldg(&al->tail_len) : P;
+    if (finalize_page(p, g, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
+                      tail ? __ldg(&al->z_tail) : p.z_page, (uint32_t)nv, (nv >> 48) != 0ull) &&
+        cc.ilist)
+        isp_note(p, cc.acc, cc.ilist, g, len);
 }
 
 // Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
@@ -275,17 +416,13 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
 constexpr int kTileScanThreads = 1024;
 constexpr uint64_t kChunkWaitNs = 30ull * 1000000000ull;
 
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, uint64_t tb, uint64_t te,
                                                                 const uint32_t *chunk_done, uint32_t chunk,
                                                                 uint32_t epoch, TileRec *host_rec,
                                                                 unsigned long long *rec_count,
-                                                                ChunkTotals *totals_host) {
+                                                                ChunkTotals *totals_host,
+                                                                unsigned long long *isp_base, uint32_t *isp_ready) {
     extern __shared__ uint32_t pb[];  // present bytes per tile of the chunk
     __shared__ int timed_out;
     if (threadIdx.x == 0) {
@@ -354,6 +491,12 @@ __global__ void __launch_bounds__(kTileScanThreads) k_tile_scan(TileInfo *ti, ui
         h[2] = tz;
         h[3] = tpa;
         *reinterpret_cast<volatile unsigned long long *>(rec_count) = tot_c;
+        if (isp_base) {  // f1: the next chunk's image offset for the in-scan pack (K2s run in chunk order)
+            const unsigned long long b = chunk ? *reinterpret_cast<volatile unsigned long long *>(isp_base + chunk) : 0ull;
+            *reinterpret_cast<volatile unsigned long long *>(isp_base + chunk + 1) = b + tot_b;
+            __threadfence();
+            *reinterpret_cast<volatile uint32_t *>(isp_ready + chunk + 1) = epoch;
+        }
         __threadfence_system();
     }
 }
@@ -466,7 +609,7 @@ __device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
 }
 
 // Page complete (vr == Rp): digest it (or leave a piece) and move on.
-__device__ __forceinline__ void page_end(const ScanParams &p, const ChunkCtx &cc, ProcCursor &pc, uint32_t (&x)[4],
+__device__ __forceinline__ void page_end(const ScanParams &p, ChunkCtx &cc, ProcCursor &pc, uint32_t (&x)[4],
                                          uint32_t &acc, const uint32_t *small, uint32_t lane) {
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t raw = warp_raw(small, x, lane);
@@ -476,8 +619,11 @@ __device__ __forceinline__ void page_end(const ScanParams &p, const ChunkCtx &cc
         const uint64_t g = pc.al.page0 + pc.pi;
         if (whole) {
             const bool tail = pc.pi == pc.al.n_pages - 1;
-            finalize_page(p, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0,
-                          tail ? pc.al.tail_len : P, tail ? pc.al.z_tail : p.z_page, raw, nz);
+            const uint32_t len = tail ? pc.al.tail_len : P;
+            if (finalize_page(p, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0, len,
+                              tail ? pc.al.z_tail : p.z_page, raw, nz) &&
+                cc.ilist)
+                isp_note(p, cc.acc, cc.ilist, g, len);
         } else {  // the page's last piece: nothing left to advance over
             fold_arrive(p, cc, g, pc.a, pc.pi, pc.r0, (P >> kLog2Row) - pc.vstart, raw, nz);
         }
@@ -493,7 +639,7 @@ __device__ __forceinline__ void page_end(const ScanParams &p, const ChunkCtx &cc
 
 // Digest the next block (the same cnt rows load_rows fetched into w).
 template <int U>
-__device__ __forceinline__ void process_rows(const ScanParams &p, const ChunkCtx &cc, ProcCursor &pc, const uint4 (&w)[U],
+__device__ __forceinline__ void process_rows(const ScanParams &p, ChunkCtx &cc, ProcCursor &pc, const uint4 (&w)[U],
                                              int &left, uint32_t (&x)[4], uint32_t &acc, const uint32_t *small,
                                              uint32_t lane4, uint32_t sb, uint32_t lane) {
     const uint32_t Rp = p.page_size >> kLog2Row;
@@ -547,8 +693,13 @@ __device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) 
 // K1.
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ __align__(128) IspShared isp_sh;  // f1 in-scan pack (unused otherwise)
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
     const uint32_t *small = sm + kBraidSmem / 4;
+    if (threadIdx.x < 2) {
+        isp_sh.cnt[threadIdx.x] = 0;
+        isp_sh.ready[threadIdx.x] = 0;
+    }
 
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u;
@@ -588,6 +739,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         cc.rb = p.chunk_rows[ch];
         cc.rows = p.chunk_rows[ch + 1] - cc.rb;
         cc.fs = p.fold.s + (uint64_t)ch * p.workers;
+        cc.ilist = p.isp.img ? isp_list(p, ch & 1u, wid) : nullptr;
+        cc.acc = IspAcc{0ull, 0u};
         const uint64_t r = cc.rb + cc.rows * wid / p.workers;
         const uint64_t rend = cc.rb + cc.rows * (wid + 1) / p.workers;
         if (r < rend) {
@@ -655,6 +808,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
                     fold_arrive(p, cc, pc.al.page0 + pc.pi, pc.a, pc.pi, pc.r0, pc.vr - pc.vstart, contrib, nz);
             }
         }
+        if (p.isp.img) isp_chunk_end(p, isp_sh, cc.acc, ch, lane);  // f1: the warp's aggregate
         // this warp is done with chunk ch; the last one publishes it for K2
         if (lane == 0) {
             __threadfence();
@@ -666,7 +820,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         }
         __syncwarp();
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
+        // f1: write the previous chunk's PRESENT pages (every aggregate of it is
+        // published by now, normally without waiting)
+        if (p.isp.img && ch >= 1) isp_write(p, isp_sh, ch - 1, wid, lane);
     }
+    if (p.isp.img && p.n_chunks) isp_write(p, isp_sh, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
@@ -720,6 +878,11 @@ template <int G>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p) {
     constexpr uint32_t QL = 32 / G, Wr = kRowBytes / G, Rg = 32, U = 4, NB = Rg / U;
     extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ __align__(128) IspShared isp_sh;  // f1 in-scan pack (unused otherwise)
+    if (threadIdx.x < 2) {
+        isp_sh.cnt[threadIdx.x] = 0;
+        isp_sh.ready[threadIdx.x] = 0;
+    }
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t *small = sm + kBraidSmem / 4;
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
@@ -747,6 +910,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     }
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
+        uint32_t *ilist = p.isp.img ? isp_list(p, ch & 1u, wid) : nullptr;  // f1
+        IspAcc iacc{0ull, 0u};  // warp-uniform
         const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
         const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
         if (g0 < g1) {
@@ -804,10 +969,23 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                 }
                 const uint32_t bal = __ballot_sync(kFull, acc != 0u);
                 const uint32_t nzq = QL == 32 ? bal : (bal >> (q * QL)) & ((1u << QL) - 1u);
+                bool pres = false;
+                uint32_t plen = 0;
                 if (m == 0u && pgl.valid) {
                     const bool tail = pgl.pi == pal.n_pages - 1;
-                    finalize_page(p, pal.page0 + pgl.pi, tile_of_page(pal.tile0, pgl.pi, P, lg), pgl.pi == 0,
-                                  tail ? pal.tail_len : P, tail ? pal.z_tail : p.z_page, v, nzq != 0u);
+                    plen = tail ? pal.tail_len : P;
+                    pres = finalize_page(p, pal.page0 + pgl.pi, tile_of_page(pal.tile0, pgl.pi, P, lg), pgl.pi == 0,
+                                         plen, tail ? pal.z_tail : p.z_page, v, nzq != 0u);
+                }
+                if (ilist) {  // f1: the group's PRESENT pages, in lane (= page) order
+                    const uint32_t bal2 = __ballot_sync(kFull, pres);
+                    if (pres) {
+                        const uint32_t k = iacc.n + __popc(bal2 & ((1u << lane) - 1u));
+                        if (k < p.isp.cap) ilist[k] = (uint32_t)(pal.page0 + pgl.pi);
+                        else *reinterpret_cast<volatile unsigned long long *>(p.isp.err) = 1ull;
+                    }
+                    iacc.n += __popc(bal2);
+                    iacc.bytes += __reduce_add_sync(kFull, pres ? plen : 0u);
                 }
                 x[0] = x[1] = x[2] = x[3] = 0u;
                 acc = 0u;
@@ -834,6 +1012,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                 process_block(wb);
             }
         }
+        if (p.isp.img) isp_chunk_end(p, isp_sh, iacc, ch, lane);  // f1: the warp's aggregate
         // every leader lane's page results visible before lane 0 publishes
         __threadfence();
         __syncwarp();
@@ -846,7 +1025,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
         }
         __syncwarp();
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
+        if (p.isp.img && ch >= 1) isp_write(p, isp_sh, ch - 1, wid, lane);
     }
+    if (p.isp.img && p.n_chunks) isp_write(p, isp_sh, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
@@ -1204,7 +1385,7 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
 
 int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, const uint32_t *chunk_done, uint32_t chunk,
                      uint32_t epoch, TileRec *host_rec, unsigned long long *rec_count, ChunkTotals *totals_host,
-                     cudaStream_t st) {
+                     unsigned long long *isp_base, uint32_t *isp_ready, cudaStream_t st) {
     const size_t smem = (size_t)(te - tb) * 4;
     static bool attr_done[64] = {};
     int dev = 0;
@@ -1215,7 +1396,7 @@ int launch_tile_scan(TileInfo *tile_info, uint64_t tb, uint64_t te, const uint32
         attr_done[dev] = true;
     }
     k_tile_scan<<<1, kTileScanThreads, smem, st>>>(tile_info, tb, te, chunk_done, chunk, epoch, host_rec, rec_count,
-                                                   totals_host);
+                                                   totals_host, isp_base, isp_ready);
     return launched(1);
 }
 

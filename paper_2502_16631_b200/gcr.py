@@ -32,7 +32,7 @@ GCR_PE_PARENT, GCR_PE_PRESENT, GCR_PE_ZERO = 1, 4, 8
 class gcr_config(C.Structure):
     _fields_ = [("page_size", C.c_uint32), ("n_copy_streams", C.c_uint32), ("chunk_bytes", C.c_uint64),
                 ("n_staging_slots", C.c_uint32), ("verify", C.c_uint32), ("lock_timeout_ms", C.c_uint64),
-                ("direct_min_bytes", C.c_uint64), ("compress", C.c_uint32), ("reserved0", C.c_uint32)]
+                ("direct_min_bytes", C.c_uint64), ("compress", C.c_uint32), ("in_scan_pack", C.c_uint32)]
 
 
 _STAT_FIELDS = ["lock_ns", "unlock_ns", "checkpoint_ns", "restore_ns", "scan_dev_ns", "scan_launches", "scan_bytes",
