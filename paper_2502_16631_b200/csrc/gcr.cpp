@@ -1064,6 +1064,10 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         sp.isp.list = c->isp_list;
         sp.isp.cap = c->isp_cap;
         sp.isp.err = c->isp_err;
+        {
+            const char *e = std::getenv("GCR_ISP_WAIT_MS");  // diagnostics: shorter bound on the in-kernel waits
+            sp.isp.wait_ns = (e ? std::strtoull(e, nullptr, 0) : 30000ull) * 1000000ull;
+        }
         sp.isp_page_alloc = c->page_alloc;
         CUDA_TRY(c, cudaMemsetAsync(c->isp_err, 0, 8, c->compute));
     }
@@ -1357,7 +1361,9 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     CUDA_TRY(c, cudaStreamSynchronize(c->compute));
     st.drain_ns = ns_since(drain0);
     if (isp && (c->misc_h[0] != 0 || (nch && c->misc_h[3] != base)))
-        return fail(c, GCR_E_CUDA, "checkpoint: in-scan pack failed (wait timeout, list overflow or offset mismatch)");
+        return fail(c, GCR_E_CUDA, "checkpoint: in-scan pack failed (error word " + std::to_string(c->misc_h[0]) +
+                                       ": 1 CTA prefix / 2 CTA aggregates / 3 chunk base wait timed out, 4 list "
+                                       "overflow; base " + std::to_string(c->misc_h[3]) + " vs " + std::to_string(base) + ")");
     const double host_synced = ns_since(host0) * 1e-6;
 
     // stats from the events

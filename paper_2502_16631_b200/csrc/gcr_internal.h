@@ -121,7 +121,8 @@ struct InScanPack {
     uint32_t *base_ready;        // [n_chunks + 1] epoch once base[c] is written
     uint32_t *list;              // [2][workers][cap] PRESENT pages the warp finalized, in page order
     uint32_t cap;
-    unsigned long long *err;     // set to 1 on a wait timeout or a list overflow (checkpoint fails)
+    unsigned long long *err;     // non-zero on a wait timeout (which | chunk << 8 | CTA << 32) or a list overflow (4)
+    uint64_t wait_ns;            // bound of every wait (GCR_ISP_WAIT_MS, default 30 s)
 };
 
 // K1 is ONE persistent launch per checkpoint (or verify): every warp walks

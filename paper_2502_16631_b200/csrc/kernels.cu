@@ -50,7 +50,8 @@ namespace {
 
 constexpr uint32_t kBraidSmem = 4u * 256u * 32u * 4u;  // 128 KiB
 constexpr uint32_t kSmallTables = 6;                   // t4 a16 a32 a64 a128 a256
-constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u;
+constexpr uint32_t kNibWords = 7u * 4u * 2u * 16u;  // nibble tables of the 7 tables (staging scratch)
+constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u + kNibWords * 4u;
 constexpr uint32_t kLog2Row = 9;
 #ifndef GCR_SCAN_THREADS
 #define GCR_SCAN_THREADS 640
@@ -203,12 +204,11 @@ __device__ __forceinline__ uint32_t *isp_list(const ScanParams &p, uint32_t par,
 // One finalized PRESENT page (executed by the lane that finalized it).
 __device__ __forceinline__ void isp_note(const ScanParams &p, IspAcc &acc, uint32_t *list, uint64_t g, uint32_t len) {
     if (acc.n < p.isp.cap) list[acc.n] = (uint32_t)g;
-    else *reinterpret_cast<volatile unsigned long long *>(p.isp.err) = 1ull;
+    else atomicCAS(p.isp.err, 0ull, 4ull);  // list overflow
     acc.n++;
     acc.bytes += len;
 }
 
-constexpr uint64_t kIspWaitNs = 30ull * 1000000000ull;
 
 __device__ __forceinline__ uint64_t isp_tag(uint32_t epoch, uint32_t ch) {
     return ((uint64_t)(epoch & 0xFFFFu) << 48) | ((uint64_t)(ch & 0xFFFFu) << 32);
@@ -264,30 +264,30 @@ __device__ __forceinline__ void isp_chunk_end(const ScanParams &p, IspShared &ss
 __device__ __forceinline__ void isp_write(const ScanParams &p, IspShared &ss, uint32_t ch, uint64_t wid,
                                           uint32_t lane) {
     const uint32_t par = ch & 1u, wib = threadIdx.x >> 5;
-    const uint64_t t0 = globaltimer_ns();
-    bool ok = true;
+    const uint64_t t0 = globaltimer_ns(), lim = p.isp.wait_ns;
+    uint32_t why = 0;  // which wait timed out (error word: why | chunk << 8 | CTA << 32)
     // the in-CTA prefix of this chunk
     while (*reinterpret_cast<volatile uint32_t *>(&ss.ready[par]) != ch + 1u)
-        if (globaltimer_ns() - t0 > kIspWaitNs) { ok = false; break; }
+        if (globaltimer_ns() - t0 > lim) { why = 1; break; }
     // PRESENT bytes of the earlier CTAs (their aggregates carry this chunk's tag)
     unsigned long long before = 0;
     const uint64_t tag = isp_tag(p.epoch, ch);
-    for (uint32_t b = lane; ok && b < blockIdx.x; b += 32u) {
+    for (uint32_t b = lane; !why && b < blockIdx.x; b += 32u) {
         unsigned long long v;
         while (((v = *reinterpret_cast<volatile unsigned long long *>(p.isp.cta_agg + par * gridDim.x + b)) >> 32) !=
                tag >> 32)
-            if (globaltimer_ns() - t0 > kIspWaitNs) { ok = false; break; }
+            if (globaltimer_ns() - t0 > lim) { why = 2; break; }
         before += v & 0xFFFFFFFFull;
     }
 #pragma unroll
     for (int d = 16; d; d >>= 1) before += __shfl_xor_sync(kFull, before, d);
     // the chunk's image offset, from K2 of the previous chunk
-    if (ch != 0)
+    if (ch != 0 && !why)
         while (*reinterpret_cast<volatile uint32_t *>(p.isp.base_ready + ch) != p.epoch)
-            if (globaltimer_ns() - t0 > kIspWaitNs) { ok = false; break; }
-    ok = __all_sync(kFull, ok);
-    if (!ok) {
-        if (lane == 0) *reinterpret_cast<volatile unsigned long long *>(p.isp.err) = 1ull;
+            if (globaltimer_ns() - t0 > lim) { why = 3; break; }
+    why = __reduce_max_sync(kFull, why);
+    if (why) {
+        if (lane == 0) atomicCAS(p.isp.err, 0ull, (unsigned long long)why | (uint64_t)ch << 8 | (uint64_t)blockIdx.x << 32);
         return;
     }
     __threadfence();
@@ -297,7 +297,7 @@ __device__ __forceinline__ void isp_write(const ScanParams &p, IspShared &ss, ui
     const uint32_t *list = isp_list(p, par, wid);
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t k = 0; k < n; k++) {
-        const uint64_t g = __ldg(list + k);
+        const uint64_t g = __ldcg(list + k);  // written by this warp in this launch: not the read-only path
         const AllocDev *al = p.allocs + __ldg(p.isp_page_alloc + g);
         const uint64_t pi = g - __ldg(&al->page0);
         const uint32_t len = pi == (uint64_t)__ldg(&al->n_pages) - 1 ? __ldg(&al->tail_len) : P;
@@ -666,28 +666,42 @@ __device__ __forceinline__ void process_rows(const ScanParams &p, ChunkCtx &cc, 
 __device__ __forceinline__ uint32_t tab_entry(const uint32_t *b32, uint32_t k, uint32_t e) {
     uint32_t v = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++)
+    for (int i = 0; i < 4; i++)
         if ((e >> i) & 1u) v ^= b32[8 * k + i];
     return v;
 }
 
+// Two phases.  (1) The 7 tables' NIBBLE tables -- entry n of half h of byte
+// position k of table t = XOR of basis[t][8k + 4h + i] over the set bits i of
+// n -- into a 3.5 KiB scratch at the end of the dynamic smem (896 entries,
+// one or two per thread, from the constant bank).  (2) Every table entry =
+// lo-nibble entry ^ hi-nibble entry (two broadcast LDS): the braid table into
+// all 32 lane-private replicas -- 8 threads write one entry's 128 contiguous
+// replica bytes, one conflict-free STS.128 phase -- and the small tables
+// (t4, a16 .. a256) once.  (One thread per replicated entry, 8 stores each,
+// put every lane of a store phase on the same 4 banks: 8-way conflicts, ~4 us
+// per launch; building every entry straight from the 8 basis values cost
+// ~700 instructions per thread.)
 __device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) {
-    // Braid table: the 32 replicas of entry (k, e) are 128 contiguous bytes;
-    // 8 threads write them with one 16-B store each, so every 8-lane phase of a
-    // warp's STS.128 covers 128 contiguous bytes (no bank conflict).  (Thread
-    // per entry, 8 stores each, put all lanes of a phase on the same 4 banks:
-    // 8-way conflicts, ~4 us per launch.)
+    uint32_t *nib = sm + (kBraidSmem + kSmallTables * 4096u) / 4;
+    for (uint32_t i = threadIdx.x; i < kNibWords; i += kScanThreads) {
+        const uint32_t t = i >> 7, k = (i >> 5) & 3u, h = (i >> 4) & 1u, n = i & 15u;
+        nib[i] = tab_entry(p.basis[t] + 4 * h, k, n);  // basis words 8k + 4h + (0..3)
+    }
+    __syncthreads();
     constexpr uint32_t kGroups = kScanThreads / 8;
     const uint32_t sub = threadIdx.x & 7u;
     for (uint32_t ke = threadIdx.x >> 3; ke < 1024u; ke += kGroups) {
         const uint32_t k = ke >> 8, e = ke & 255u;
-        const uint32_t v = tab_entry(p.basis[0], k, e);
+        const uint32_t v = nib[k * 32 + (e & 15u)] ^ nib[k * 32 + 16 + (e >> 4)];
         uint4 *dst = reinterpret_cast<uint4 *>(sm + (k >> 1) * 16384u + e * 64u + (k & 1u) * 32u) + sub;
         *dst = make_uint4(v, v, v, v);
     }
     uint32_t *ss = sm + kBraidSmem / 4;
-    for (uint32_t i = threadIdx.x; i < kSmallTables * 1024u; i += kScanThreads)
-        ss[i] = tab_entry(p.basis[1 + (i >> 10)], (i >> 8) & 3u, i & 255u);
+    for (uint32_t i = threadIdx.x; i < kSmallTables * 1024u; i += kScanThreads) {
+        const uint32_t t = 1 + (i >> 10), k = (i >> 8) & 3u, e = i & 255u;
+        ss[i] = nib[t * 128 + k * 32 + (e & 15u)] ^ nib[t * 128 + k * 32 + 16 + (e >> 4)];
+    }
 }
 
 // K1.
