@@ -596,8 +596,8 @@ gcr_status build_layout(gcr_ctx *c) {
         if (grp) cap = std::max<uint64_t>(cap, ((max_rows * kRowBytes / kGroupBytes) + w_min - 1) / w_min * G + 2 * G);
         c->isp_cap = (uint32_t)cap;
         const uint64_t ctas = (w_max + 19) / 20 + 1;
-        CUDA_TRY(c, cudaMalloc(&c->isp_cta, 8 * 2 * ctas));
-        CUDA_TRY(c, cudaMemset(c->isp_cta, 0, 8 * 2 * ctas));
+        CUDA_TRY(c, cudaMalloc(&c->isp_cta, 8 * (nch + 1) * ctas));
+        CUDA_TRY(c, cudaMemset(c->isp_cta, 0, 8 * (nch + 1) * ctas));
         CUDA_TRY(c, cudaMalloc(&c->isp_base, 8 * (nch + 2)));
         CUDA_TRY(c, cudaMemset(c->isp_base, 0, 8 * (nch + 2)));
         CUDA_TRY(c, cudaMalloc(&c->isp_ready, 4 * (nch + 2)));

@@ -116,7 +116,8 @@ struct CrcTables {
 // it.
 struct InScanPack {
     uint8_t *img;                // device-visible address of the image data (null: off)
-    unsigned long long *cta_agg; // [2][n_ctas]: epoch << 40 | PRESENT bytes finalized by the CTA (chunk parity)
+    unsigned long long *cta_agg; // [n_chunks][n_ctas]: tag(epoch, chunk) | PRESENT bytes finalized by the CTA
+                                 // in the chunk (one slot per chunk: CTAs may be chunks apart)
     unsigned long long *base;    // [n_chunks + 1] image offset of each chunk (base[0] = 0), written by K2
     uint32_t *base_ready;        // [n_chunks + 1] epoch once base[c] is written
     uint32_t *list;              // [2][workers][cap] PRESENT pages the warp finalized, in page order

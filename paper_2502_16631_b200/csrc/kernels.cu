@@ -250,7 +250,7 @@ __device__ __forceinline__ void isp_chunk_end(const ScanParams &p, IspShared &ss
         const unsigned long long tot = __shfl_sync(kFull, inc, nw - 1);
         if (lane == 0) {
             ss.cnt[par] = 0;
-            p.isp.cta_agg[par * gridDim.x + blockIdx.x] = isp_tag(p.epoch, ch) | tot;
+            p.isp.cta_agg[(uint64_t)ch * gridDim.x + blockIdx.x] = isp_tag(p.epoch, ch) | tot;
             __threadfence();
             __threadfence_block();
             *reinterpret_cast<volatile uint32_t *>(&ss.ready[par]) = ch + 1;
@@ -274,7 +274,7 @@ __device__ __forceinline__ void isp_write(const ScanParams &p, IspShared &ss, ui
     const uint64_t tag = isp_tag(p.epoch, ch);
     for (uint32_t b = lane; !why && b < blockIdx.x; b += 32u) {
         unsigned long long v;
-        while (((v = *reinterpret_cast<volatile unsigned long long *>(p.isp.cta_agg + par * gridDim.x + b)) >> 32) !=
+        while (((v = *reinterpret_cast<volatile unsigned long long *>(p.isp.cta_agg + (uint64_t)ch * gridDim.x + b)) >> 32) !=
                tag >> 32)
             if (globaltimer_ns() - t0 > lim) { why = 2; break; }
         before += v & 0xFFFFFFFFull;
