@@ -50,6 +50,7 @@ uint64_t ns_since(Clock::time_point t0) {
 
 constexpr uint64_t kMaxChunk = 2ull << 30;
 constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity
+constexpr uint64_t kGroupMax = 64ull << 20;   // restore: bytes per staged H2D group
 constexpr size_t kDigestChunks = 4;           // checkpoint: chunks per digest D2H
 const char kMagic[8] = {'G', 'C', 'R', 'I', 'M', 'G', 0x00, 0x01};
 
@@ -1609,6 +1610,10 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         uint64_t z_begin, z_end;
     };
     const uint64_t direct_min = c->cfg.direct_min_bytes;
+    // staged groups (one H2D into a slot + scatter / decode) of at most
+    // kGroupMax: the first kernel starts after 64 MiB instead of a whole slot,
+    // and the last group's kernel -- the restore's tail -- is short
+    const uint64_t group_max = std::min<uint64_t>(slot, kGroupMax);
     std::vector<ImgPlan> plans(n);
     std::vector<ScatterDesc> sdesc;
     std::vector<ZeroDesc> zdesc;
@@ -1640,7 +1645,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                     // descriptor per page
                     for (uint64_t q = p; q < last; q++) {
                         const uint32_t L = (uint32_t)page_len(c->reg[a].bytes, P, q), sl = im->stored[ip++];
-                        if (group_open && pl.items.back().bytes + sl > slot) close_group();
+                        if (group_open && pl.items.back().bytes + sl > group_max) close_group();
                         if (!group_open) {
                             pl.items.push_back(Item{false, cursor, 0, 0, ddesc.size(), 0, true});
                             group_open = true;
@@ -1663,13 +1668,13 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                         }
                     } else {
                         while (bytes) {
-                            if (group_open && pl.items.back().bytes + bytes > slot) close_group();
+                            if (group_open && pl.items.back().bytes + bytes > group_max) close_group();
                             if (!group_open) {
                                 pl.items.push_back(Item{false, cursor, 0, 0, sdesc.size(), 0, false});
                                 group_open = true;
                             }
                             Item &g = pl.items.back();
-                            const uint64_t piece = std::min(std::min(bytes, kPieceBytes), slot - g.bytes);
+                            const uint64_t piece = std::min(std::min(bytes, kPieceBytes), group_max - g.bytes);
                             sdesc.push_back(ScatterDesc{dst, cursor - g.img_off, piece});
                             g.bytes += piece;
                             dst += piece;

@@ -1279,40 +1279,128 @@ __global__ void k_pm_entries(const AllocDev *allocs, const uint32_t *page_alloc,
     }
 }
 
-// K6: staged image pieces -> allocation pages.  One CTA per descriptor.
-// kPlain (diagnostic GCR_DIAG_SCATTER_PLAIN=1): coherent ld.global instead of
-// the read-only streaming path, to separate tool artefacts from real hazards.
-__device__ __forceinline__ uint4 ld_plain(const void *p) { return __ldcg(reinterpret_cast<const uint4 *>(p)); }
+// ---- TMA bulk-copy helpers (cp.async.bulk: SASS UBLKCP) --------------------
+// Global <-> shared bulk copies driven by one thread, completion of loads
+// tracked by an mbarrier (transaction bytes), of stores by bulk groups.  Every
+// size and address is a multiple of 16 (R-2).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <bool kPlain>
-__global__ void __launch_bounds__(256) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
-    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const uint64_t dst = desc[i].dst, so = desc[i].src_off, by = desc[i].bytes;
-        const uint8_t *src = slot + so;
-        uint8_t *d = reinterpret_cast<uint8_t *>(dst);
-        constexpr int U = 4;
-        uint64_t off = (uint64_t)threadIdx.x * 16u;
-        const uint32_t stride = blockDim.x * 16u;
-        for (; off + (U - 1) * stride < by; off += U * stride) {
-            uint4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) v[u] = kPlain ? ld_plain(src + off + u * stride) : ldg_stream(src + off + u * stride);
-#pragma unroll
-            for (int u = 0; u < U; u++) *reinterpret_cast<uint4 *>(d + off + u * stride) = v[u];
-        }
-        for (; off < by; off += stride)
-            *reinterpret_cast<uint4 *>(d + off) = kPlain ? ld_plain(src + off) : ldg_stream(src + off);
-    }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
-// K7: zero fill of ZERO runs.
-__global__ void __launch_bounds__(256) k_zero_fill(const ZeroDesc *desc, uint64_t n) {
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {  // at most N committed store groups still reading smem
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// K6: staged image pieces -> allocation pages, through the TMA engine: one
+// elected thread per CTA streams each of its descriptors in 32 KiB pieces
+// through a 4-stage shared-memory ring (bulk load -> mbarrier -> bulk store),
+// keeping up to 4 loads and 3 stores in flight; the SM's other threads stay
+// out of the way (the copy needs no ALU and no registers).
+constexpr uint32_t kTmaStage = 32768, kTmaStages = 4;
+
+__global__ void __launch_bounds__(32) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
+    extern __shared__ __align__(128) uint8_t buf[];  // kTmaStages x kTmaStage
+    __shared__ __align__(8) uint64_t bar[kTmaStages];
+    if (threadIdx.x != 0) return;
+    for (uint32_t s = 0; s < kTmaStages; s++) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the piece sequence of this CTA: descriptors i = blockIdx.x + k*gridDim.x, cut into stage-sized pieces
+    uint64_t li = blockIdx.x, lo = 0;  // load cursor: descriptor, offset
+    uint64_t si = blockIdx.x, so = 0;  // store cursor
+    uint32_t issued = 0, done = 0;
+    auto next = [&](uint64_t &i, uint64_t &o, uint32_t &len) -> bool {
+        while (i < n && o >= desc[i].bytes) {
+            i += gridDim.x;
+            o = 0;
+        }
+        if (i >= n) return false;
+        len = (uint32_t)(desc[i].bytes - o < kTmaStage ? desc[i].bytes - o : kTmaStage);
+        return true;
+    };
+    uint32_t len;
+    // ring of kTmaStages stages: piece k is loaded into stage k % S; loads run
+    // S - 1 pieces ahead of the stores; before a stage is refilled, the store
+    // that last read it (one piece earlier) must have finished reading
+    while (issued < kTmaStages - 1 && next(li, lo, len)) {
+        const uint32_t s = issued % kTmaStages;
+        mbar_expect_tx(&bar[s], len);
+        bulk_load(buf + s * kTmaStage, slot + desc[li].src_off + lo, len, &bar[s]);
+        lo += len;
+        issued++;
+    }
+    while (done < issued) {
+        const uint32_t s = done % kTmaStages;
+        mbar_wait(&bar[s], (done / kTmaStages) & 1u);
+        uint32_t sl;
+        next(si, so, sl);
+        bulk_store(reinterpret_cast<uint8_t *>(desc[si].dst) + so, buf + s * kTmaStage, sl);
+        bulk_commit();
+        so += sl;
+        done++;
+        if (next(li, lo, len)) {  // piece `issued` goes into the stage piece done - 2 used
+            bulk_wait_read<1>();
+            const uint32_t t = issued % kTmaStages;
+            mbar_expect_tx(&bar[t], len);
+            bulk_load(buf + t * kTmaStage, slot + desc[li].src_off + lo, len, &bar[t]);
+            lo += len;
+            issued++;
+        }
+    }
+    bulk_wait_all();
+}
+
+// K7: zero fill of ZERO runs: bulk stores from one zeroed 32 KiB smem buffer.
+__global__ void __launch_bounds__(128) k_zero_fill(const ZeroDesc *desc, uint64_t n) {
+    __shared__ __align__(128) uint4 zero[kTmaStage / 16];
+    for (uint32_t i = threadIdx.x; i < kTmaStage / 16; i += blockDim.x) zero[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy zeros visible to the bulk copies
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    uint32_t groups = 0;
     for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
         uint8_t *d = reinterpret_cast<uint8_t *>(desc[i].dst);
         const uint64_t by = desc[i].bytes;
-        for (uint64_t off = (uint64_t)threadIdx.x * 16u; off < by; off += blockDim.x * 16u)
-            *reinterpret_cast<uint4 *>(d + off) = make_uint4(0, 0, 0, 0);
+        for (uint64_t off = 0; off < by; off += kTmaStage) {
+            bulk_store(d + off, zero, (uint32_t)(by - off < kTmaStage ? by - off : kTmaStage));
+            if (++groups % 8 == 0) bulk_commit();
+        }
     }
+    bulk_commit();
+    bulk_wait_all();
 }
 
 }  // namespace
@@ -1452,20 +1540,25 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
-    uint64_t g = n < (uint64_t)n_sms * 8 ? n : (uint64_t)n_sms * 8;
-    static const bool plain = [] {
-        const char *e = std::getenv("GCR_DIAG_SCATTER_PLAIN");
-        return e && e[0] == '1';
-    }();
-    if (plain) k_scatter<true><<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
-    else k_scatter<false><<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
+    static bool attr_done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev]) {
+        if (cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTmaStages * kTmaStage)) !=
+            cudaSuccess)
+            return -1;
+        attr_done[dev] = true;
+    }
+    // one CTA (one issuing thread, 128 KiB ring) per SM, or per descriptor if fewer
+    const uint64_t g = n < (uint64_t)n_sms ? n : (uint64_t)n_sms;
+    k_scatter<<<(unsigned)g, 32, kTmaStages * kTmaStage, st>>>(desc, n, slot);
     return launched(1);
 }
 
 int launch_zero_fill(const ZeroDesc *desc, uint64_t n, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
-    uint64_t g = n < (uint64_t)n_sms * 8 ? n : (uint64_t)n_sms * 8;
-    k_zero_fill<<<(unsigned)g, 256, 0, st>>>(desc, n);
+    const uint64_t g = n < (uint64_t)n_sms * 2 ? n : (uint64_t)n_sms * 2;
+    k_zero_fill<<<(unsigned)g, 128, 0, st>>>(desc, n);
     return launched(1);
 }
 
