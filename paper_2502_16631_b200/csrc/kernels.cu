@@ -221,8 +221,24 @@ struct IspShared {
     uint32_t wn[2][32];              // pages in each warp's list
     uint32_t cnt[2];                 // warps of the CTA done with the chunk
     uint32_t ready[2];               // ch + 1 once wpfx of the chunk is written
-    uint32_t pad[28];
+    uint32_t wdone;                  // chunk write-outs finished by the CTA's warps (monotonic)
+    uint32_t pad[27];
 };
+
+// Before a warp records pages of chunk ch (ch >= 2) into the list slot of
+// chunk ch - 2 (two parities), every warp of the CTA must be done writing
+// chunk ch - 2 out: the write-out of a chunk is shared by the CTA's warps and
+// reads all of their lists.  Bounded; a timeout is reported like the others.
+__device__ __forceinline__ void isp_lists_free(const ScanParams &p, IspShared &ss, uint32_t ch) {
+    if (ch < 2) return;
+    const uint32_t need = (blockDim.x >> 5) * (ch - 1);
+    const uint64_t t0 = globaltimer_ns();
+    while (*reinterpret_cast<volatile uint32_t *>(&ss.wdone) < need)
+        if (globaltimer_ns() - t0 > p.isp.wait_ns) {
+            if ((threadIdx.x & 31u) == 0) atomicCAS(p.isp.err, 0ull, 5ull | (uint64_t)ch << 8);
+            break;
+        }
+}
 
 // End of chunk ch for this warp: publish its aggregate in the CTA; the CTA's
 // last warp writes the in-CTA prefixes and the CTA aggregate (global).
@@ -287,33 +303,54 @@ __device__ __forceinline__ void isp_write(const ScanParams &p, IspShared &ss, ui
             if (globaltimer_ns() - t0 > lim) { why = 3; break; }
     why = __reduce_max_sync(kFull, why);
     if (why) {
-        if (lane == 0) atomicCAS(p.isp.err, 0ull, (unsigned long long)why | (uint64_t)ch << 8 | (uint64_t)blockIdx.x << 32);
+        if (lane == 0) {
+            atomicCAS(p.isp.err, 0ull, (unsigned long long)why | (uint64_t)ch << 8 | (uint64_t)blockIdx.x << 32);
+            atomicAdd(&ss.wdone, 1u);
+        }
         return;
     }
     __threadfence();
-    unsigned long long off = (ch ? *reinterpret_cast<volatile unsigned long long *>(p.isp.base + ch) : 0ull) + before +
-                             ss.wpfx[par][wib];
-    const uint32_t n = min(ss.wn[par][wib], p.isp.cap);
-    const uint32_t *list = isp_list(p, par, wid);
+    // The CTA's chunk-ch pages (its warps' lists in warp order) cover image
+    // bytes [cta0, cta0 + T); warp wib writes the 512-B-aligned share
+    // [s0, s1) of them, so one CTA's pages are written by all its warps
+    // (a single warp writing a few 64 KiB pages over PCIe would otherwise
+    // trail the chunk by tens of microseconds).
+    const uint32_t nw = blockDim.x >> 5;
+    const unsigned long long cta0 = (ch ? *reinterpret_cast<volatile unsigned long long *>(p.isp.base + ch) : 0ull) + before;
+    const unsigned long long T = ss.wpfx[par][nw - 1] + ss.wagg[par][nw - 1];
+    const unsigned long long s0 = (T * wib / nw) & ~511ull, s1 = wib + 1 == nw ? T : (T * (wib + 1) / nw) & ~511ull;
     const uint32_t P = p.page_size, lg = p.log2_page;
-    for (uint32_t k = 0; k < n; k++) {
-        const uint64_t g = __ldcg(list + k);  // written by this warp in this launch: not the read-only path
-        const AllocDev *al = p.allocs + __ldg(p.isp_page_alloc + g);
-        const uint64_t pi = g - __ldg(&al->page0);
-        const uint32_t len = pi == (uint64_t)__ldg(&al->n_pages) - 1 ? __ldg(&al->tail_len) : P;
-        const uint8_t *src = reinterpret_cast<const uint8_t *>(__ldg(&al->base) + (pi << lg));
-        uint8_t *dst = p.isp.img + off;
-        uint32_t o = lane * 16u;
-        for (; o + 3 * 512u < len; o += 4 * 512u) {
-            uint4 v[4];
+    for (uint32_t v = 0; v < nw && s0 < s1; v++) {
+        unsigned long long r = ss.wpfx[par][v];
+        if (r >= s1) break;
+        if (r + ss.wagg[par][v] <= s0) continue;
+        const uint32_t n = min(ss.wn[par][v], p.isp.cap);
+        const uint32_t *list = isp_list(p, par, (uint64_t)blockIdx.x * nw + v);
+        for (uint32_t k = 0; k < n && r < s1; k++) {
+            const uint64_t g = __ldcg(list + k);  // written in this launch: not the read-only path
+            const AllocDev *al = p.allocs + __ldg(p.isp_page_alloc + g);
+            const uint64_t pi = g - __ldg(&al->page0);
+            const uint32_t len = pi == (uint64_t)__ldg(&al->n_pages) - 1 ? __ldg(&al->tail_len) : P;
+            const unsigned long long a = max(r, s0), b = min(r + len, s1);
+            if (a < b) {
+                const uint8_t *src = reinterpret_cast<const uint8_t *>(__ldg(&al->base) + (pi << lg)) + (a - r);
+                uint8_t *dst = p.isp.img + cta0 + a;
+                const uint32_t m = (uint32_t)(b - a);
+                uint32_t o = lane * 16u;
+                for (; o + 3 * 512u < m; o += 4 * 512u) {
+                    uint4 x[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) v[u] = ldg_stream(src + o + u * 512u);
+                    for (int u = 0; u < 4; u++) x[u] = ldg_stream(src + o + u * 512u);
 #pragma unroll
-            for (int u = 0; u < 4; u++) *reinterpret_cast<uint4 *>(dst + o + u * 512u) = v[u];
+                    for (int u = 0; u < 4; u++) *reinterpret_cast<uint4 *>(dst + o + u * 512u) = x[u];
+                }
+                for (; o < m; o += 512u) *reinterpret_cast<uint4 *>(dst + o) = ldg_stream(src + o);
+            }
+            r += len;
         }
-        for (; o < len; o += 512u) *reinterpret_cast<uint4 *>(dst + o) = ldg_stream(src + o);
-        off += len;
     }
+    __syncwarp();
+    if (lane == 0) atomicAdd(&ss.wdone, 1u);  // this warp is done with the CTA's lists of chunk ch
 }
 
 // GF(2) product m (*) v mod P in the reflected representation (bit 31 = x^0):
@@ -713,29 +750,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     if (threadIdx.x < 2) {
         isp_sh.cnt[threadIdx.x] = 0;
         isp_sh.ready[threadIdx.x] = 0;
+        isp_sh.wdone = 0;
     }
 
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t lane4 = lane * 4u;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    // Before building the tables: request the first bytes of this warp's
-    // chunk-0 range into L2, so the first loads after staging hit L2 instead
-    // of paying the HBM round trip (real rows of an allocation are contiguous:
-    // row r lives at base + (r - row0) * 512).
-    if (p.prefetch != 0u && p.n_chunks != 0 && wid < p.workers) {
-        const uint64_t rb = p.chunk_rows[0], rows = p.chunk_rows[1] - rb;
-        const uint64_t r = rb + rows * wid / p.workers, re = rb + rows * (wid + 1) / p.workers;
-        if (r < re) {
-            const AllocDev *al = p.allocs + alloc_of_row(p.allocs, p.n_allocs, r, lane);
-            if (lane == 0) {
-                const uint64_t a0 = __ldg(&al->base) + ((r - __ldg(&al->row0)) << kLog2Row);
-                const uint64_t e = min(min(a0 + p.prefetch, __ldg(&al->base) + __ldg(&al->bytes)),
-                                       a0 + ((re - r) << kLog2Row));
-                if (e > a0) prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(e - a0));
-            }
-        }
-    }
     stage_tables(sm, p);
     __syncthreads();
     if (wid >= p.workers) return;
@@ -755,6 +776,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         cc.fs = p.fold.s + (uint64_t)ch * p.workers;
         cc.ilist = p.isp.img ? isp_list(p, ch & 1u, wid) : nullptr;
         cc.acc = IspAcc{0ull, 0u};
+        if (p.isp.img) isp_lists_free(p, isp_sh, ch);
         const uint64_t r = cc.rb + cc.rows * wid / p.workers;
         const uint64_t rend = cc.rb + cc.rows * (wid + 1) / p.workers;
         if (r < rend) {
@@ -896,25 +918,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     if (threadIdx.x < 2) {
         isp_sh.cnt[threadIdx.x] = 0;
         isp_sh.ready[threadIdx.x] = 0;
+        isp_sh.wdone = 0;
     }
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t *small = sm + kBraidSmem / 4;
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    // before building the tables: the warp's first group of chunk 0 into L2
-    if (p.prefetch != 0u && p.n_chunks != 0 && wid < p.workers) {
-        const uint64_t cb = p.chunk_groups[0], n = p.chunk_groups[1] - cb;
-        const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
-        if (g0 < g1) {
-            const AllocDev *al = p.allocs + alloc_of_group(p.allocs, p.n_allocs, g0, lane);
-            if (lane == 0) {
-                const uint64_t a0 = __ldg(&al->base) + ((g0 - __ldg(&al->grp0)) * G << p.log2_page);
-                const uint64_t e = min(a0 + (uint64_t)G * p.page_size, __ldg(&al->base) + __ldg(&al->bytes));
-                if (e > a0) prefetch_l2(reinterpret_cast<const void *>(a0), (uint32_t)(e - a0));
-            }
-        }
-    }
     stage_tables(sm, p);  // the host put adv_{512/G} (a128 / a256) in basis[0]
     __syncthreads();
     if (wid >= p.workers) return;
@@ -926,6 +936,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
         uint32_t *ilist = p.isp.img ? isp_list(p, ch & 1u, wid) : nullptr;  // f1
         IspAcc iacc{0ull, 0u};  // warp-uniform
+        if (p.isp.img) isp_lists_free(p, isp_sh, ch);
         const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
         const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
         if (g0 < g1) {
