@@ -564,6 +564,8 @@ def run_ours(args):
                         "what": "nvidia-smi during the timed region on every rank's GPU; sm_mhz = the lowest rank median"}
     result["placement"] = {"ranks": world, "gpus_visible": n_dev, "shared_gpus": world > n_dev,
                            "numa": [c["numa"] for c in allc]}
+    if args.sub_c4_gib and not incremental and args.config == "C2":
+        result["c4_incremental"] = c4_sub_record(args, torch, gcr, synth, local, pg)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_seconds)
     if rank == 0:
@@ -571,6 +573,61 @@ def run_ours(args):
     ctx.close()
     if pg is not None:
         pg.destroy_process_group()
+
+
+def c4_sub_record(args, torch, gcr, synth, dev, pg):
+    """The balanced case of SURVEY §8(d) d.3 as a sub-record of the default line:
+    C4-shaped state (1 GiB RANDOM allocations, --sub-c4-gib of them), a full
+    checkpoint (untimed), then per step 1 % of the pages dirtied and an
+    incremental checkpoint (lock -> checkpoint -> unlock) timed with CUDA events;
+    reported against max(scan, drain) = the step's roofline."""
+    w = synth.make_workload("C4", gib=args.sub_c4_gib)
+    ts = w.materialize()
+    torch.cuda.synchronize()
+    ctx = gcr.Context(dev, page_size=w.page_size, compress=0, in_scan_pack=args.in_scan_pack)
+    try:
+        for t in ts:
+            ctx.register_tensor(t)
+        R = w.total_bytes
+        ctx.reserve_host(R + (2 << 30))
+        st = torch.cuda.ExternalStream(ctx.stream())
+        ctx.lock()
+        ctx.checkpoint().free()
+        ctx.unlock()
+        times, scans, imgs = [], [], []
+        for k in range(3 + 5):
+            muts = synth.dirty_mutations(w, 0.01, rng_seed=777 + k)
+            synth.gpu_xor_batch([ts[a].data_ptr() + o for (a, o, x) in muts], [x for (a, o, x) in muts])
+            torch.cuda.synchronize()
+            _barrier(pg)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            ctx.lock()
+            im = ctx.checkpoint(gcr.GCR_INCREMENTAL)
+            ctx.unlock()
+            e1.record(st)
+            e1.synchronize()
+            s = ctx.stats()
+            if k >= 3:
+                times.append(e0.elapsed_time(e1) * 1e-3)
+                scans.append(s["scan_dev_ns"] * 1e-9)
+                imgs.append(s["image_bytes"])
+            im.free()
+        d2h, _ = ctx.probe_link(1 << 30)
+        t = _max_over_ranks(pg, sum(times) / len(times))
+        scan = sum(scans) / len(scans)
+        img = sum(imgs) / len(imgs)
+        roof = max(R / (_peaks()["hbm_gbs"] * 1e9), img / (d2h * 1e9))
+        return {"what": f"C4-shaped {args.sub_c4_gib} x 1 GiB, 1 % of pages dirty per step, incremental checkpoint "
+                        f"(5 timed steps, 3 warm-up; in_scan_pack={args.in_scan_pack})",
+                "registered_bytes": R, "ms_per_step": round(t * 1e3, 3), "GBps_registered": round(R / t / 1e9, 1),
+                "scan_ms": round(scan * 1e3, 3), "image_bytes": int(img), "d2h_probe_GBps": round(d2h, 2),
+                "roofline_ms": round(roof * 1e3, 3), "frac_of_roofline": round(roof / t, 3),
+                "roofline": "max(R / MEASURED_PEAKS hbm_gbs, image bytes / pool D2H probe)"}
+    finally:
+        ctx.close()
+        del ts
+        torch.cuda.empty_cache()
 
 
 def _workload_desc(name, w):
@@ -727,6 +784,8 @@ def main():
     ap.add_argument("--dirty", type=float, default=0.01)
     ap.add_argument("--clustered", action="store_true", help="dirty pages in 64-page runs instead of scattered")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sub-c4-gib", type=int, default=8,
+                    help="default C2 line: add a C4-shaped 1 %% incremental sub-record of this many GiB (0 = off)")
     ap.add_argument("--in-scan-pack", type=int, default=1, choices=[0, 1, 2],
                     help="f1: 1 = incremental checkpoints written by the scan kernel itself (default), 0 = staged "
                          "pipeline, 2 = every checkpoint")

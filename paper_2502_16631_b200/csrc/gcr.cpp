@@ -989,6 +989,7 @@ static gcr_status fence_caller_work(gcr_ctx *c) {
 // The launch's table bases (ScanParams::basis): the braid step is adv_512
 // for K1, adv_{512/G} for K1g (a128 at 4 KiB pages, a256 at 8 KiB).
 static void set_basis(const gcr_ctx *c, ScanParams &sp) {
+    sp.t4rep = sp.chunk_groups != nullptr && grp_t4rep();
     int braid = 0;
     if (sp.chunk_groups != nullptr) braid = sp.page_size == kGroupBytes / 4 ? 5 : 6;
     std::memcpy(sp.basis[0], c->basis[braid], sizeof sp.basis[0]);

@@ -163,6 +163,7 @@ struct ScanParams {
     // lines at launch (the global-table staging cost ~4.8 us per launch).
     uint32_t basis[7][32];
     InScanPack isp;            // f1 (img == nullptr: off)
+    uint32_t t4rep;            // K1g: 8x-replicated raw16 table (see kernels.cu kT4RepBytes)
     const uint32_t *isp_page_alloc;  // f1: page -> allocation (K0's table)
 };
 
@@ -195,6 +196,7 @@ int scan_free_sms(bool incremental);                                // SMs K1 le
 uint64_t scan_workers(int n_sms, int free_sms);                      // K1 warps (a full persistent grid)
 uint32_t scan_prefetch_bytes();                                     // K1 L2 prefetch distance (GCR_SCAN_PREFETCH)
 uint32_t grp_prefetch_block();                                      // K1g prefetch trigger block (GCR_GRP_PF_BLOCK)
+bool grp_t4rep();                                                   // K1g 8x raw16 table (GCR_GRP_T4REP)
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st);  // K1 (K1g when p.chunk_groups is set)
 bool scan_uses_groups(uint32_t page_size);                          // K1g for this page size?
 // K2 of one chunk: first waits (bounded) until chunk_done[chunk] == epoch.

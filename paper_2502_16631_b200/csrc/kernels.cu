@@ -52,6 +52,16 @@ constexpr uint32_t kBraidSmem = 4u * 256u * 32u * 4u;  // 128 KiB
 constexpr uint32_t kSmallTables = 6;                   // t4 a16 a32 a64 a128 a256
 constexpr uint32_t kNibWords = 7u * 4u * 2u * 16u;  // nibble tables of the 7 tables (staging scratch)
 constexpr uint32_t kScanSmem = kBraidSmem + kSmallTables * 4096u + kNibWords * 4u;
+// K1g option (ScanParams::t4rep): the raw16 table t4 replicated 8x, entry e of
+// sub-table k for lane-group c = lane & 7 at word (256k + e) * 8 + c: bank =
+// (8e + c) mod 32, so only the 4 lanes sharing c can collide (the unreplicated
+// table puts 32 random lookups on 32 banks: ~3.5-way conflicts).
+constexpr uint32_t kT4RepBytes = 8u * 1024u * 4u;
+
+__device__ __forceinline__ uint32_t apply_t4rep(const uint32_t *t, uint32_t v, uint32_t c) {
+    return t[((v & 255u) << 3) + c] ^ t[((256u + ((v >> 8) & 255u)) << 3) + c] ^
+           t[((512u + ((v >> 16) & 255u)) << 3) + c] ^ t[((768u + (v >> 24)) << 3) + c];
+}
 constexpr uint32_t kLog2Row = 9;
 #ifndef GCR_SCAN_THREADS
 #define GCR_SCAN_THREADS 640
@@ -739,6 +749,14 @@ __device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) 
         const uint32_t t = 1 + (i >> 10), k = (i >> 8) & 3u, e = i & 255u;
         ss[i] = nib[t * 128 + k * 32 + (e & 15u)] ^ nib[t * 128 + k * 32 + 16 + (e >> 4)];
     }
+    if (p.t4rep) {  // K1g: t4 x 8 after the nibble scratch; two 16-B stores per entry, contiguous per warp
+        uint32_t *tr = sm + kScanSmem / 4;
+        for (uint32_t h = threadIdx.x; h < 2048u; h += kScanThreads) {
+            const uint32_t i = h >> 1, k = i >> 8, e = i & 255u;
+            const uint32_t v = nib[128 + k * 32 + (e & 15u)] ^ nib[128 + k * 32 + 16 + (e >> 4)];
+            *reinterpret_cast<uint4 *>(tr + i * 8u + (h & 1u) * 4u) = make_uint4(v, v, v, v);
+        }
+    }
 }
 
 // K1.
@@ -982,11 +1000,20 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                 for (uint32_t u = 0; u < U; u++) row_step(lane4, sb, x, acc, w[u]);
                 if (++pb < NB) return;
                 // group complete: one raw16 + tree for all G pages
-                const uint32_t *t4 = small + kT4 * 1024u;
-                uint32_t v = apply_tab(t4, x[0]);
-                v = apply_tab(t4, v ^ x[1]);
-                v = apply_tab(t4, v ^ x[2]);
-                v = apply_tab(t4, v ^ x[3]);
+                uint32_t v;
+                if (p.t4rep) {
+                    const uint32_t *tr = sm + kScanSmem / 4, c = lane & 7u;
+                    v = apply_t4rep(tr, x[0], c);
+                    v = apply_t4rep(tr, v ^ x[1], c);
+                    v = apply_t4rep(tr, v ^ x[2], c);
+                    v = apply_t4rep(tr, v ^ x[3], c);
+                } else {
+                    const uint32_t *t4 = small + kT4 * 1024u;
+                    v = apply_tab(t4, x[0]);
+                    v = apply_tab(t4, v ^ x[1]);
+                    v = apply_tab(t4, v ^ x[2]);
+                    v = apply_tab(t4, v ^ x[3]);
+                }
 #pragma unroll
                 for (uint32_t j = 0; (1u << j) < QL; j++) {
                     const uint32_t o = __shfl_down_sync(kFull, v, 1u << j);
@@ -1447,6 +1474,12 @@ uint64_t scan_workers(int n_sms, int free) {
 // block 0 (16 KiB ahead) 4-9 % of the prefetched lines were evicted before use
 // and re-read from DRAM (ncu: 1.56-1.62 GB read for 1.49 GB); at block 4 the
 // reads are 1.0010x the algorithmic bytes (profiles/r1n_grp_prefetch.jsonl).
+// K1g: replicate t4 8x for the per-group raw16 (GCR_GRP_T4REP=0: unreplicated)
+bool grp_t4rep() {
+    const char *e = std::getenv("GCR_GRP_T4REP");  // read per checkpoint (A/B in one process)
+    return !(e && e[0] == '0');
+}
+
 uint32_t grp_prefetch_block() {
     static const uint32_t v = [] {
         const char *e = std::getenv("GCR_GRP_PF_BLOCK");
@@ -1477,9 +1510,9 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_done[dev]) {
         if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
-            cudaFuncSetAttribute(k_scan_grp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) !=
+            cudaFuncSetAttribute(k_scan_grp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kScanSmem + kT4RepBytes)) !=
                 cudaSuccess ||
-            cudaFuncSetAttribute(k_scan_grp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) !=
+            cudaFuncSetAttribute(k_scan_grp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kScanSmem + kT4RepBytes)) !=
                 cudaSuccess)
             return -1;
         attr_done[dev] = true;
@@ -1488,9 +1521,9 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     const uint64_t wpb = kScanThreads / 32;
     const uint64_t grid = (p.workers + wpb - 1) / wpb;
     if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 4)
-        k_scan_grp<4><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+        k_scan_grp<4><<<(unsigned)grid, kScanThreads, kScanSmem + (p.t4rep ? kT4RepBytes : 0u), st>>>(p);
     else if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 2)
-        k_scan_grp<2><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+        k_scan_grp<2><<<(unsigned)grid, kScanThreads, kScanSmem + (p.t4rep ? kT4RepBytes : 0u), st>>>(p);
     else
         k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
     return launched(1);
