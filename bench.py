@@ -786,9 +786,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sub-c4-gib", type=int, default=8,
                     help="default C2 line: add a C4-shaped 1 %% incremental sub-record of this many GiB (0 = off)")
-    ap.add_argument("--in-scan-pack", type=int, default=1, choices=[0, 1, 2],
-                    help="f1: 1 = incremental checkpoints written by the scan kernel itself (default), 0 = staged "
-                         "pipeline, 2 = every checkpoint")
+    ap.add_argument("--in-scan-pack", type=int, default=0, choices=[0, 1, 2],
+                    help="f1: 1 = incremental checkpoints written by the scan kernel itself, 0 = staged pipeline "
+                         "(default: measured faster), 2 = every checkpoint")
     ap.add_argument("--compress", type=int, default=1, choices=[0, 1],
                     help="1: f4 page codec (PRESENT pages stored in byte-plane dictionary form, GPU encode/decode)")
     ap.add_argument("--dry-run", action="store_true", help="launch the ranks and report them; no GPU work")

@@ -106,14 +106,16 @@ typedef struct {
                                  Digests, classes and the pagemap are unchanged; the image gets a
                                  stored-length table and header flag bit 1.  All PRESENT data then
                                  moves through the staging slots (direct_min_bytes is unused). */
-    uint32_t in_scan_pack;    /* f1: 0 = PRESENT pages reach the image through the
-                                 staged / direct pipeline (K2 plan, K4 pack, copy-engine D2H);
-                                 1 (default) = incremental checkpoints let the scan kernel itself write
+    uint32_t in_scan_pack;    /* f1: 0 (default) = PRESENT pages reach the image
+                                 through the staged / direct pipeline (K2 plan, K4 pack, copy-engine
+                                 D2H); 1 = incremental checkpoints let the scan kernel itself write
                                  every PRESENT page straight into the pinned image (mapped memory;
                                  image offsets from per-CTA aggregates + a per-chunk base, no pack, no
-                                 staging, no data D2H); 2 = every checkpoint does (full ones too:
-                                 slower than the copy engines at 100 % PRESENT; for tests).  Ignored
-                                 when compress = 1.  The image bytes are identical either way. */
+                                 staging, no data D2H); 2 = every checkpoint does (full ones too).
+                                 Measured: 1 is 3-7 % slower than 0 on C4 1-5 %
+                                 dirty -- the scan's own PCIe stores couple it to the link -- so 0 is
+                                 the default.  Ignored when compress = 1.  The image bytes are
+                                 identical either way. */
 } gcr_config;
 
 /* Statistics of the most recent lock / checkpoint / restore / unlock

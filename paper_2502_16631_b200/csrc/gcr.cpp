@@ -743,7 +743,7 @@ gcr_status gcr_config_default(gcr_config *out) {
     out->lock_timeout_ms = 10000;
     out->direct_min_bytes = 16ull << 20;
     out->compress = 0;
-    out->in_scan_pack = 1;
+    out->in_scan_pack = 0;
     return GCR_OK;
 }
 

@@ -1363,60 +1363,78 @@ __device__ __forceinline__ void bulk_wait_read() {  // at most N committed store
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// K6: staged image pieces -> allocation pages, through the TMA engine: one
-// elected thread per CTA streams each of its descriptors in 32 KiB pieces
-// through a 4-stage shared-memory ring (bulk load -> mbarrier -> bulk store),
-// keeping up to 4 loads and 3 stores in flight; the SM's other threads stay
-// out of the way (the copy needs no ALU and no registers).
-constexpr uint32_t kTmaStage = 32768, kTmaStages = 4;
+// K6: staged image pieces -> allocation pages, through the TMA engine.  The
+// group's descriptors are cut into 16 KiB pieces; CTA c takes pieces c, c +
+// grid, c + 2 grid, ... (piece indices run over the descriptors in order), so
+// every SM holds several CTAs whatever the descriptor count.  One elected
+// thread per CTA streams its pieces through a 2-stage shared-memory ring (bulk
+// load -> mbarrier -> bulk store); four 32 KiB CTAs per SM keep ~128 KiB in
+// flight.  (A first version gave each CTA whole 1 MiB descriptors: a 64 MiB
+// group had 64 issuing threads and copied at 0.3 TB/s.)
+constexpr uint32_t kTmaStage = 16384, kTmaStages = 2;
 
 __global__ void __launch_bounds__(32) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
-    extern __shared__ __align__(128) uint8_t buf[];  // kTmaStages x kTmaStage
+    __shared__ __align__(128) uint8_t buf[kTmaStages * kTmaStage];
     __shared__ __align__(8) uint64_t bar[kTmaStages];
     if (threadIdx.x != 0) return;
     for (uint32_t s = 0; s < kTmaStages; s++) mbar_init(&bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // the piece sequence of this CTA: descriptors i = blockIdx.x + k*gridDim.x, cut into stage-sized pieces
-    uint64_t li = blockIdx.x, lo = 0;  // load cursor: descriptor, offset
-    uint64_t si = blockIdx.x, so = 0;  // store cursor
-    uint32_t issued = 0, done = 0;
-    auto next = [&](uint64_t &i, uint64_t &o, uint32_t &len) -> bool {
-        while (i < n && o >= desc[i].bytes) {
-            i += gridDim.x;
-            o = 0;
-        }
-        if (i >= n) return false;
-        len = (uint32_t)(desc[i].bytes - o < kTmaStage ? desc[i].bytes - o : kTmaStage);
-        return true;
+    // walk (descriptor, piece) in order, keeping this CTA's pieces: a load
+    // cursor and a store cursor over the same sequence
+    struct Cur {
+        uint64_t i, o, g;  // descriptor, offset in it, global piece index of (i, o)
     };
-    uint32_t len;
-    // ring of kTmaStages stages: piece k is loaded into stage k % S; loads run
-    // S - 1 pieces ahead of the stores; before a stage is refilled, the store
-    // that last read it (one piece earlier) must have finished reading
-    while (issued < kTmaStages - 1 && next(li, lo, len)) {
-        const uint32_t s = issued % kTmaStages;
-        mbar_expect_tx(&bar[s], len);
-        bulk_load(buf + s * kTmaStage, slot + desc[li].src_off + lo, len, &bar[s]);
-        lo += len;
-        issued++;
+    Cur lc{0, 0, 0}, sc{0, 0, 0};
+    const uint64_t G = gridDim.x, me = blockIdx.x;
+    auto seek = [&](Cur &c) -> bool {  // advance c to this CTA's next piece
+        for (;;) {
+            while (c.i < n && c.o >= desc[c.i].bytes) {
+                c.i++;
+                c.o = 0;
+            }
+            if (c.i >= n) return false;
+            if (c.g % G == me) return true;
+            const uint64_t skip = (me + G - c.g % G) % G;  // pieces to the next one of mine
+            const uint64_t left = (desc[c.i].bytes - c.o + kTmaStage - 1) / kTmaStage;
+            const uint64_t k = skip < left ? skip : left;
+            c.o += k * kTmaStage;
+            c.g += k;
+        }
+    };
+    auto step = [&](Cur &c) {
+        c.o += kTmaStage;
+        c.g++;
+    };
+    auto len_of = [&](const Cur &c) -> uint32_t {
+        const uint64_t r = desc[c.i].bytes - c.o;
+        return (uint32_t)(r < kTmaStage ? r : kTmaStage);
+    };
+    uint32_t issued = 0, done = 0;
+    if (seek(lc)) {
+        const uint32_t len = len_of(lc);
+        mbar_expect_tx(&bar[0], len);
+        bulk_load(buf, slot + desc[lc.i].src_off + lc.o, len, &bar[0]);
+        step(lc);
+        issued = 1;
     }
     while (done < issued) {
         const uint32_t s = done % kTmaStages;
-        mbar_wait(&bar[s], (done / kTmaStages) & 1u);
-        uint32_t sl;
-        next(si, so, sl);
-        bulk_store(reinterpret_cast<uint8_t *>(desc[si].dst) + so, buf + s * kTmaStage, sl);
-        bulk_commit();
-        so += sl;
-        done++;
-        if (next(li, lo, len)) {  // piece `issued` goes into the stage piece done - 2 used
-            bulk_wait_read<1>();
+        // issue the next load into the other stage once the store that read it is done
+        if (issued == done + 1 && seek(lc)) {
             const uint32_t t = issued % kTmaStages;
+            bulk_wait_read<0>();
+            const uint32_t len = len_of(lc);
             mbar_expect_tx(&bar[t], len);
-            bulk_load(buf + t * kTmaStage, slot + desc[li].src_off + lo, len, &bar[t]);
-            lo += len;
+            bulk_load(buf + t * kTmaStage, slot + desc[lc.i].src_off + lc.o, len, &bar[t]);
+            step(lc);
             issued++;
         }
+        mbar_wait(&bar[s], (done / kTmaStages) & 1u);
+        seek(sc);
+        bulk_store(reinterpret_cast<uint8_t *>(desc[sc.i].dst) + sc.o, buf + s * kTmaStage, len_of(sc));
+        bulk_commit();
+        step(sc);
+        done++;
     }
     bulk_wait_all();
 }
@@ -1584,18 +1602,7 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
-    static bool attr_done[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && !attr_done[dev]) {
-        if (cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kTmaStages * kTmaStage)) !=
-            cudaSuccess)
-            return -1;
-        attr_done[dev] = true;
-    }
-    // one CTA (one issuing thread, 128 KiB ring) per SM, or per descriptor if fewer
-    const uint64_t g = n < (uint64_t)n_sms ? n : (uint64_t)n_sms;
-    k_scatter<<<(unsigned)g, 32, kTmaStages * kTmaStage, st>>>(desc, n, slot);
+    k_scatter<<<(unsigned)(n_sms * 4), 32, 0, st>>>(desc, n, slot);  // 4 CTAs (32 KiB ring each) per SM
     return launched(1);
 }
 
