@@ -12,9 +12,10 @@
 //                       each plane (lane-private bitmaps in shared memory,
 //                       warp-reduced), the page's stored length, its 4x256-bit
 //                       presence masks (scratch for KC)
-//  KB  k_codec_offsets  one CTA per chunk: exclusive scan of the stored lengths
-//                       (chunk-local slot offsets), the compact stored-length
-//                       table of the image, the chunk's coded total -> mapped host
+//  KB  k_codec_offsets  one CTA per sub-chunk: exclusive scan of the stored
+//                       lengths (slot offsets from the sub-chunk's base), its
+//                       entries of the compact stored-length table, its stored
+//                       total and PRESENT count -> mapped host
 //  KC  k_codec_encode   one warp per PRESENT page: header, dictionaries, packed
 //                       ranks / raw planes into the staging slot
 //  KD  k_codec_decode   restore: one warp per PRESENT page of a staged group,
@@ -173,7 +174,7 @@ __device__ __forceinline__ unsigned long long block_scan(unsigned long long v, u
 // written to mapped host memory.
 __global__ void __launch_bounds__(1024) k_codec_offsets(const uint32_t *plan, uint32_t np, uint32_t *off,
                                                         uint32_t *stored_compact, uint64_t present_base,
-                                                        unsigned long long *total_host) {
+                                                        uint64_t slot_base, unsigned long long *total_host) {
     const uint32_t per = (np + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = min(np, per * threadIdx.x), hi = min(np, lo + per);
     unsigned long long s = 0, c = 0;
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(1024) k_codec_offsets(const uint32_t *plan, ui
         c += v != 0u;
     }
     unsigned long long tot, totc;
-    unsigned long long o = block_scan(s, &tot);
+    unsigned long long o = block_scan(s, &tot) + slot_base;
     unsigned long long k = block_scan(c, &totc);
     for (uint32_t p = lo; p < hi; p++) {
         const uint32_t v = plan[p];
@@ -192,7 +193,8 @@ __global__ void __launch_bounds__(1024) k_codec_offsets(const uint32_t *plan, ui
         o += v;
     }
     if (threadIdx.x == 0) {
-        *reinterpret_cast<volatile unsigned long long *>(total_host) = tot;
+        reinterpret_cast<volatile unsigned long long *>(total_host)[0] = tot;
+        reinterpret_cast<volatile unsigned long long *>(total_host)[1] = totc;
         __threadfence_system();
     }
 }
@@ -481,8 +483,8 @@ int launch_codec_plan(const AllocDev *allocs, const uint32_t *page_alloc, const 
 }
 
 int launch_codec_offsets(const uint32_t *plan, uint32_t n_pages, uint32_t *off, uint32_t *stored_compact,
-                         uint64_t present_base, unsigned long long *total_host, cudaStream_t st) {
-    k_codec_offsets<<<1, 1024, 0, st>>>(plan, n_pages, off, stored_compact, present_base, total_host);
+                         uint64_t present_base, uint64_t slot_base, unsigned long long *total_host, cudaStream_t st) {
+    k_codec_offsets<<<1, 1024, 0, st>>>(plan, n_pages, off, stored_compact, present_base, slot_base, total_host);
     return codec_launched(1);
 }
 

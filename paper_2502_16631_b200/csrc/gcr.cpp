@@ -51,6 +51,7 @@ uint64_t ns_since(Clock::time_point t0) {
 constexpr uint64_t kMaxChunk = 2ull << 30;
 constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity
 constexpr uint64_t kGroupMax = 64ull << 20;   // restore: bytes per staged H2D group
+constexpr uint64_t kCodecSub = 256ull << 20;  // f4 checkpoint: page bytes per encode + D2H sub-chunk
 constexpr size_t kDigestChunks = 4;           // checkpoint: chunks per digest D2H
 const char kMagic[8] = {'G', 'C', 'R', 'I', 'M', 'G', 0x00, 0x01};
 
@@ -614,7 +615,7 @@ gcr_status build_layout(gcr_ctx *c) {
             c->cx_scratch.push_back(x);
         }
         CUDA_TRY(c, cudaMalloc(&c->stored_d, 4 * std::max<uint64_t>(g, 1)));
-        CUDA_TRY(c, cudaHostAlloc(&c->ctot_h, 8 * std::max<uint64_t>(nch, 1), cudaHostAllocMapped));
+        CUDA_TRY(c, cudaHostAlloc(&c->ctot_h, 16, cudaHostAllocMapped));  // {sub-chunk stored bytes, PRESENT pages}
         CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->ctot_map), c->ctot_h, 0));
     }
     CUDA_TRY(c, cudaMemcpyAsync(c->allocs_d, c->allocs_h.data(), sizeof(AllocDev) * na, cudaMemcpyHostToDevice,
@@ -1252,30 +1253,57 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         CUDA_TRY(c, cudaStreamWaitEvent(c->packs, tot[i], 0));
         uint64_t chunk_stored = T.image_bytes;
         if (coded && T.n_present) {
-            // f4: KA (stored length + presence masks per page), KB (slot offsets,
-            // stored-length table, chunk total -> mapped host), then -- once
-            // slot i mod NS is drained -- KC encodes the chunk's PRESENT pages
-            // into it; ONE D2H of the chunk's stored bytes follows.  All on the
-            // packs stream (in order: KC(i - NS) is done with the scratch before
-            // KA(i) overwrites it).
+            // f4, per SUB-chunk of <= kCodecSub bytes of pages (so the link starts
+            // after the first 256 MiB is coded, not the whole chunk): KA (stored
+            // length + presence masks per page), KB (slot offsets from the
+            // sub-chunk's slot base, stored-length table entries, sub total and
+            // PRESENT count -> mapped host), then KC encodes the sub-chunk into
+            // slot i mod NS (the first one after that slot's previous drain) and
+            // its D2H follows on the chunk's copy stream.  All kernels on the
+            // packs stream, in order (KC(i - NS) is done with the scratch before
+            // KA(i) overwrites it); the host waits for each KB to size the D2H.
             uint32_t *x = c->cx_scratch[i % NS];
             uint32_t *plan = x, *off = x + c->cx_pages, *masks = x + 2 * c->cx_pages;
-            const uint32_t npg = (uint32_t)(ch.page_end - ch.page_begin);
-            cudaEvent_t ca = c->ev(), kb = c->ev();
-            CUDA_TRY(c, cudaEventRecord(ca, c->packs));
-            LAUNCH_TRY(c, launch_codec_plan(c->allocs_d, c->page_alloc, c->cls, ch.page_begin, npg, P, c->lg, plan,
-                                            masks, c->n_sms, c->packs));
-            LAUNCH_TRY(c, launch_codec_offsets(plan, npg, off, c->stored_d, present_base, c->ctot_map + i, c->packs));
-            CUDA_TRY(c, cudaEventRecord(kb, c->packs));
-            if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
-            CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
-            LAUNCH_TRY(c, launch_codec_encode(c->allocs_d, c->page_alloc, c->cls, ch.page_begin, npg, P, c->lg, plan,
-                                              off, masks, c->slots[i % NS], c->n_sms, c->packs));
-            codec_ev.emplace_back(ca, kb);
-            CUDA_TRY(c, cudaEventSynchronize(kb));
-            chunk_stored = *reinterpret_cast<volatile unsigned long long *>(c->ctot_h + i);
-            if (chunk_stored > T.image_bytes) return fail(c, GCR_E_CUDA, "checkpoint: coded chunk larger than its pages");
-            staged.emplace_back(0, chunk_stored);
+            const uint64_t npg = ch.page_end - ch.page_begin;
+            static const uint64_t sub_bytes_cfg = [] {  // GCR_CODEC_SUB_MB: tests exercise many sub-chunks
+                const char *e = std::getenv("GCR_CODEC_SUB_MB");
+                return e ? std::strtoull(e, nullptr, 0) << 20 : kCodecSub;
+            }();
+            const uint64_t sub_pages = std::max<uint64_t>(1, sub_bytes_cfg / P);
+            uint64_t slot_base = 0, pres_base = present_base;
+            for (uint64_t p0 = 0; p0 < npg; p0 += sub_pages) {
+                const uint32_t n = (uint32_t)std::min(sub_pages, npg - p0);
+                cudaEvent_t ca = c->ev(), kb = c->ev(), kc = c->ev();
+                CUDA_TRY(c, cudaEventRecord(ca, c->packs));
+                LAUNCH_TRY(c, launch_codec_plan(c->allocs_d, c->page_alloc, c->cls, ch.page_begin + p0, n, P, c->lg,
+                                                plan + p0, masks + 32 * p0, c->n_sms, c->packs));
+                LAUNCH_TRY(c, launch_codec_offsets(plan + p0, n, off + p0, c->stored_d, pres_base, slot_base,
+                                                   c->ctot_map, c->packs));
+                CUDA_TRY(c, cudaEventRecord(kb, c->packs));
+                if (p0 == 0) {
+                    if (i >= NS) CUDA_TRY(c, cudaStreamWaitEvent(c->packs, dde[i - NS], 0));
+                    CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
+                }
+                LAUNCH_TRY(c, launch_codec_encode(c->allocs_d, c->page_alloc, c->cls, ch.page_begin + p0, n, P, c->lg,
+                                                  plan + p0, off + p0, masks + 32 * p0, c->slots[i % NS], c->n_sms,
+                                                  c->packs));
+                CUDA_TRY(c, cudaEventRecord(kc, c->packs));
+                codec_ev.emplace_back(ca, kb);
+                CUDA_TRY(c, cudaEventSynchronize(kb));
+                const unsigned long long sub_bytes = reinterpret_cast<volatile unsigned long long *>(c->ctot_h)[0];
+                const unsigned long long sub_present = reinterpret_cast<volatile unsigned long long *>(c->ctot_h)[1];
+                if (sub_bytes) {
+                    CUDA_TRY(c, cudaStreamWaitEvent(cs, kc, 0));
+                    CUDA_TRY(c, cudaMemcpyAsync(img->data + base + slot_base, c->slots[i % NS] + slot_base, sub_bytes,
+                                                cudaMemcpyDeviceToHost, cs));
+                }
+                slot_base += sub_bytes;
+                pres_base += sub_present;
+            }
+            chunk_stored = slot_base;
+            staged_bytes += slot_base;
+            if (chunk_stored > T.image_bytes || pres_base != n_present)
+                return fail(c, GCR_E_CUDA, "checkpoint: coded chunk inconsistent with its pages");
         } else if (coded || isp) {  // f1: K1 itself writes the chunk's pages into the image
             CUDA_TRY(c, cudaEventRecord(pks[i], c->packs));
             if (isp) staged_bytes += T.image_bytes;

@@ -227,10 +227,10 @@ size_t scan_smem_bytes();
 int launch_codec_plan(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls, uint64_t page_begin,
                       uint32_t n_pages, uint32_t page_size, uint32_t log2_page, uint32_t *plan, uint32_t *masks,
                       int n_sms, cudaStream_t st);
-// KB: chunk-local slot offsets, the image's compact stored-length table from
-// present_base on, the chunk's stored total into mapped host memory.
+// KB: slot offsets (from slot_base), the image's compact stored-length table
+// from present_base on, {stored total, PRESENT count} into mapped host memory.
 int launch_codec_offsets(const uint32_t *plan, uint32_t n_pages, uint32_t *off, uint32_t *stored_compact,
-                         uint64_t present_base, unsigned long long *total_host, cudaStream_t st);
+                         uint64_t present_base, uint64_t slot_base, unsigned long long *total_host, cudaStream_t st);
 // KC: stored forms of the chunk's PRESENT pages into the slot.
 int launch_codec_encode(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls, uint64_t page_begin,
                         uint32_t n_pages, uint32_t page_size, uint32_t log2_page, const uint32_t *plan,

@@ -239,3 +239,18 @@ def test_compressed_full_size_every_page(G, orc, cfg):
         ctx.unlock()
     finally:
         ctx.close()
+
+
+def test_codec_sub_chunks_in_a_subprocess(G):
+    """f4 checkpoints encode and drain each chunk in sub-chunks (default 256
+    MiB): force 1 MiB sub-chunks (GCR_CODEC_SUB_MB, read once per process) in
+    a child process and require the codec stream tests to pass there too."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GCR_CODEC_SUB_MB="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x", "-p", "no:cacheprovider",
+                        os.path.abspath(__file__) + "::test_compressed_stream_equals_oracle_and_restores",
+                        os.path.abspath(__file__) + "::test_compressed_incremental_chain"],
+                       capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
