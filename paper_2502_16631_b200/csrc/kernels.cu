@@ -200,25 +200,9 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 // ---- f1 in-scan pack (InScanPack, gcr_internal.h) ---------------------------
-// Lane-held accumulator of the PRESENT pages a warp finalized in the current
-// chunk (K1: lane 0's copy; K1g: every lane's, warp-uniform).
-struct IspAcc {
-    unsigned long long bytes;
-    uint32_t n;
-};
-
 __device__ __forceinline__ uint32_t *isp_list(const ScanParams &p, uint32_t par, uint64_t wid) {
     return p.isp.list + (par * p.workers + wid) * (uint64_t)p.isp.cap;
 }
-
-// One finalized PRESENT page (executed by the lane that finalized it).
-__device__ __forceinline__ void isp_note(const ScanParams &p, IspAcc &acc, uint32_t *list, uint64_t g, uint32_t len) {
-    if (acc.n < p.isp.cap) list[acc.n] = (uint32_t)g;
-    else atomicCAS(p.isp.err, 0ull, 4ull);  // list overflow
-    acc.n++;
-    acc.bytes += len;
-}
-
 
 __device__ __forceinline__ uint64_t isp_tag(uint32_t epoch, uint32_t ch) {
     return ((uint64_t)(epoch & 0xFFFFu) << 48) | ((uint64_t)(ch & 0xFFFFu) << 32);
@@ -232,8 +216,43 @@ struct IspShared {
     uint32_t cnt[2];                 // warps of the CTA done with the chunk
     uint32_t ready[2];               // ch + 1 once wpfx of the chunk is written
     uint32_t wdone;                  // chunk write-outs finished by the CTA's warps (monotonic)
+    uint32_t par[32];                // each warp's current chunk parity
     uint32_t pad[27];
 };
+
+// One per CTA of K1 / K1g (file scope: the device functions below reach it
+// without a parameter, so the scan's hot loop carries no f1 state in
+// registers -- an earlier version kept an accumulator in the chunk context
+// and the compiler scheduled the row loop's lookups with less latency slack).
+__shared__ __align__(128) IspShared g_isp;
+
+__device__ __forceinline__ void isp_init() {
+    if (threadIdx.x < 2) {
+        g_isp.cnt[threadIdx.x] = 0;
+        g_isp.ready[threadIdx.x] = 0;
+    }
+    if (threadIdx.x == 0) g_isp.wdone = 0;
+}
+
+// Start of chunk ch for this warp: its counters of the chunk's parity.
+__device__ __forceinline__ void isp_chunk_begin(uint32_t ch, uint32_t lane) {
+    if (lane == 0) {
+        const uint32_t wib = threadIdx.x >> 5, par = ch & 1u;
+        g_isp.wagg[par][wib] = 0;
+        g_isp.wn[par][wib] = 0;
+        g_isp.par[wib] = par;
+    }
+    __syncwarp();
+}
+
+// One finalized PRESENT page (K1: lane 0, the only lane that finalizes).
+__device__ __forceinline__ void isp_note(const ScanParams &p, uint64_t g, uint32_t len) {
+    const uint32_t wib = threadIdx.x >> 5, par = g_isp.par[wib], n = g_isp.wn[par][wib];
+    if (n < p.isp.cap) isp_list(p, par, (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib)[n] = (uint32_t)g;
+    else atomicCAS(p.isp.err, 0ull, 4ull);  // list overflow
+    g_isp.wn[par][wib] = n + 1;
+    g_isp.wagg[par][wib] += len;
+}
 
 // Before a warp records pages of chunk ch (ch >= 2) into the list slot of
 // chunk ch - 2 (two parities), every warp of the CTA must be done writing
@@ -252,13 +271,10 @@ __device__ __forceinline__ void isp_lists_free(const ScanParams &p, IspShared &s
 
 // End of chunk ch for this warp: publish its aggregate in the CTA; the CTA's
 // last warp writes the in-CTA prefixes and the CTA aggregate (global).
-__device__ __forceinline__ void isp_chunk_end(const ScanParams &p, IspShared &ss, IspAcc &acc, uint32_t ch,
-                                              uint32_t lane) {
-    const uint32_t par = ch & 1u, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+__device__ __forceinline__ void isp_chunk_end(const ScanParams &p, IspShared &ss, uint32_t ch, uint32_t lane) {
+    const uint32_t par = ch & 1u, nw = blockDim.x >> 5;
     uint32_t arrived = 0;
-    if (lane == 0) {
-        ss.wagg[par][wib] = acc.bytes;
-        ss.wn[par][wib] = acc.n;
+    if (lane == 0) {  // the warp's counters are final (isp_note, in this warp)
         __threadfence_block();
         arrived = atomicAdd(&ss.cnt[par], 1u);
     }
@@ -282,8 +298,6 @@ __device__ __forceinline__ void isp_chunk_end(const ScanParams &p, IspShared &ss
             *reinterpret_cast<volatile uint32_t *>(&ss.ready[par]) = ch + 1;
         }
     }
-    acc.bytes = 0;
-    acc.n = 0;
 }
 
 // Write chunk ch's PRESENT pages finalized by this warp into the image.
@@ -378,13 +392,10 @@ __device__ __forceinline__ uint32_t warp_mulmod(uint32_t m, uint32_t v, uint32_t
     return t;
 }
 
-// The chunk a warp is scanning: its real rows and its fold slots (+ f1: the
-// warp's list of finalized PRESENT pages and its accumulator, lane 0's copy).
+// The chunk a warp is scanning: its real rows and its fold slots.
 struct ChunkCtx {
     uint64_t rb, rows;  // first global real row, real rows
     unsigned long long *fs;  // fold slots of this chunk (one per warp)
-    uint32_t *ilist;         // f1: this warp's list for this chunk (null: off)
-    IspAcc acc;
 };
 
 // A piece of a cut page arrives at the page's owner slot (executed by one
@@ -416,8 +427,8 @@ __device__ __forceinline__ void fold_arrive(const ScanParams &p, ChunkCtx &cc, u
     const uint32_t len = tail ? __ldg(&al->tail_len) : P;
     if (finalize_page(p, g, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
                       tail ? __ldg(&al->z_tail) : p.z_page, (uint32_t)nv, (nv >> 48) != 0ull) &&
-        cc.ilist)
-        isp_note(p, cc.acc, cc.ilist, g, len);
+        p.isp.img)
+        isp_note(p, g, len);
 }
 
 // Block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024).
@@ -669,8 +680,8 @@ __device__ __forceinline__ void page_end(const ScanParams &p, ChunkCtx &cc, Proc
             const uint32_t len = tail ? pc.al.tail_len : P;
             if (finalize_page(p, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0, len,
                               tail ? pc.al.z_tail : p.z_page, raw, nz) &&
-                cc.ilist)
-                isp_note(p, cc.acc, cc.ilist, g, len);
+                p.isp.img)
+                isp_note(p, g, len);
         } else {  // the page's last piece: nothing left to advance over
             fold_arrive(p, cc, g, pc.a, pc.pi, pc.r0, (P >> kLog2Row) - pc.vstart, raw, nz);
         }
@@ -762,14 +773,9 @@ __device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) 
 // K1.
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ __align__(128) IspShared isp_sh;  // f1 in-scan pack (unused otherwise)
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
     const uint32_t *small = sm + kBraidSmem / 4;
-    if (threadIdx.x < 2) {
-        isp_sh.cnt[threadIdx.x] = 0;
-        isp_sh.ready[threadIdx.x] = 0;
-        isp_sh.wdone = 0;
-    }
+    if (p.isp.img) isp_init();
 
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u;
@@ -792,9 +798,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         cc.rb = p.chunk_rows[ch];
         cc.rows = p.chunk_rows[ch + 1] - cc.rb;
         cc.fs = p.fold.s + (uint64_t)ch * p.workers;
-        cc.ilist = p.isp.img ? isp_list(p, ch & 1u, wid) : nullptr;
-        cc.acc = IspAcc{0ull, 0u};
-        if (p.isp.img) isp_lists_free(p, isp_sh, ch);
+        if (p.isp.img) {
+            isp_lists_free(p, g_isp, ch);
+            isp_chunk_begin(ch, lane);
+        }
         const uint64_t r = cc.rb + cc.rows * wid / p.workers;
         const uint64_t rend = cc.rb + cc.rows * (wid + 1) / p.workers;
         if (r < rend) {
@@ -862,7 +869,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
                     fold_arrive(p, cc, pc.al.page0 + pc.pi, pc.a, pc.pi, pc.r0, pc.vr - pc.vstart, contrib, nz);
             }
         }
-        if (p.isp.img) isp_chunk_end(p, isp_sh, cc.acc, ch, lane);  // f1: the warp's aggregate
+        if (p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
         // this warp is done with chunk ch; the last one publishes it for K2
         if (lane == 0) {
             __threadfence();
@@ -876,9 +883,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
         // f1: write the previous chunk's PRESENT pages (every aggregate of it is
         // published by now, normally without waiting)
-        if (p.isp.img && ch >= 1) isp_write(p, isp_sh, ch - 1, wid, lane);
+        if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
     }
-    if (p.isp.img && p.n_chunks) isp_write(p, isp_sh, p.n_chunks - 1, wid, lane);
+    if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
@@ -932,12 +939,7 @@ template <int G>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p) {
     constexpr uint32_t QL = 32 / G, Wr = kRowBytes / G, Rg = 32, U = 4, NB = Rg / U;
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ __align__(128) IspShared isp_sh;  // f1 in-scan pack (unused otherwise)
-    if (threadIdx.x < 2) {
-        isp_sh.cnt[threadIdx.x] = 0;
-        isp_sh.ready[threadIdx.x] = 0;
-        isp_sh.wdone = 0;
-    }
+    if (p.isp.img) isp_init();
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
     const uint32_t *small = sm + kBraidSmem / 4;
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
@@ -952,9 +954,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     }
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
-        uint32_t *ilist = p.isp.img ? isp_list(p, ch & 1u, wid) : nullptr;  // f1
-        IspAcc iacc{0ull, 0u};  // warp-uniform
-        if (p.isp.img) isp_lists_free(p, isp_sh, ch);
+        if (p.isp.img) {
+            isp_lists_free(p, g_isp, ch);
+            isp_chunk_begin(ch, lane);
+        }
         const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
         const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
         if (g0 < g1) {
@@ -1029,15 +1032,21 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                     pres = finalize_page(p, pal.page0 + pgl.pi, tile_of_page(pal.tile0, pgl.pi, P, lg), pgl.pi == 0,
                                          plen, tail ? pal.z_tail : p.z_page, v, nzq != 0u);
                 }
-                if (ilist) {  // f1: the group's PRESENT pages, in lane (= page) order
+                if (p.isp.img) {  // f1: the group's PRESENT pages, in lane (= page) order
                     const uint32_t bal2 = __ballot_sync(kFull, pres);
+                    const uint32_t wib = threadIdx.x >> 5, par = ch & 1u, n0 = g_isp.wn[par][wib];
+                    const uint32_t bytes = __reduce_add_sync(kFull, pres ? plen : 0u);
                     if (pres) {
-                        const uint32_t k = iacc.n + __popc(bal2 & ((1u << lane) - 1u));
-                        if (k < p.isp.cap) ilist[k] = (uint32_t)(pal.page0 + pgl.pi);
-                        else *reinterpret_cast<volatile unsigned long long *>(p.isp.err) = 1ull;
+                        const uint32_t k = n0 + __popc(bal2 & ((1u << lane) - 1u));
+                        if (k < p.isp.cap) isp_list(p, par, wid)[k] = (uint32_t)(pal.page0 + pgl.pi);
+                        else atomicCAS(p.isp.err, 0ull, 4ull);
                     }
-                    iacc.n += __popc(bal2);
-                    iacc.bytes += __reduce_add_sync(kFull, pres ? plen : 0u);
+                    __syncwarp();
+                    if (lane == 0) {
+                        g_isp.wn[par][wib] = n0 + __popc(bal2);
+                        g_isp.wagg[par][wib] += bytes;
+                    }
+                    __syncwarp();
                 }
                 x[0] = x[1] = x[2] = x[3] = 0u;
                 acc = 0u;
@@ -1064,7 +1073,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                 process_block(wb);
             }
         }
-        if (p.isp.img) isp_chunk_end(p, isp_sh, iacc, ch, lane);  // f1: the warp's aggregate
+        if (p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
         // every leader lane's page results visible before lane 0 publishes
         __threadfence();
         __syncwarp();
@@ -1077,9 +1086,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
         }
         __syncwarp();
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
-        if (p.isp.img && ch >= 1) isp_write(p, isp_sh, ch - 1, wid, lane);
+        if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
     }
-    if (p.isp.img && p.n_chunks) isp_write(p, isp_sh, p.n_chunks - 1, wid, lane);
+    if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
