@@ -1501,10 +1501,13 @@ uint64_t scan_workers(int n_sms, int free) {
 // block 0 (16 KiB ahead) 4-9 % of the prefetched lines were evicted before use
 // and re-read from DRAM (ncu: 1.56-1.62 GB read for 1.49 GB); at block 4 the
 // reads are 1.0010x the algorithmic bytes (profiles/r1n_grp_prefetch.jsonl).
-// K1g: replicate t4 8x for the per-group raw16 (GCR_GRP_T4REP=0: unreplicated)
+// K1g: replicate t4 8x for the per-group raw16 (GCR_GRP_T4REP=1).  Off by
+// default: same-box A/B at 4 KiB pages (profiles/r2l_t4rep_ab.jsonl) showed no
+// gain -- ncu: bank conflicts 3.95 M -> 3.63 M of 54 M shared wavefronts; the
+// 32 KiB it takes comes out of L1.
 bool grp_t4rep() {
     const char *e = std::getenv("GCR_GRP_T4REP");  // read per checkpoint (A/B in one process)
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }
 
 uint32_t grp_prefetch_block() {
