@@ -49,7 +49,7 @@ uint64_t ns_since(Clock::time_point t0) {
 }
 
 constexpr uint64_t kMaxChunk = 2ull << 30;
-constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity
+constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity (K6 assumes <= 1 MiB)
 constexpr uint64_t kGroupMax = 64ull << 20;   // restore: bytes per staged H2D group
 constexpr uint64_t kCodecSub = 256ull << 20;  // f4 checkpoint: page bytes per encode + D2H sub-chunk
 constexpr size_t kDigestChunks = 4;           // checkpoint: chunks per digest D2H

@@ -1372,15 +1372,20 @@ __device__ __forceinline__ void bulk_wait_read() {  // at most N committed store
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// K6: staged image pieces -> allocation pages, through the TMA engine.  The
-// group's descriptors are cut into 16 KiB pieces; CTA c takes pieces c, c +
-// grid, c + 2 grid, ... (piece indices run over the descriptors in order), so
-// every SM holds several CTAs whatever the descriptor count.  One elected
-// thread per CTA streams its pieces through a 2-stage shared-memory ring (bulk
-// load -> mbarrier -> bulk store); four 32 KiB CTAs per SM keep ~128 KiB in
-// flight.  (A first version gave each CTA whole 1 MiB descriptors: a 64 MiB
-// group had 64 issuing threads and copied at 0.3 TB/s.)
+// K6: staged image pieces -> allocation pages, through the TMA engine.
+// Every descriptor is at most kScatterDescMax bytes (the restore planner cuts
+// runs into 1 MiB descriptors), so piece u of the launch is piece u mod M of
+// descriptor u / M (M = kScatterDescMax / kTmaStage; pieces past a short
+// descriptor's end are skipped): CTA c takes pieces c, c + grid, ... with no
+// search.  One elected thread per CTA streams its pieces through a 2-stage
+// shared-memory ring (bulk load -> mbarrier -> bulk store); four 32 KiB CTAs
+// per SM keep ~128 KiB in flight.  (A first version gave each CTA whole
+// descriptors -- 64 issuing threads for a 64 MiB group, 0.3 TB/s -- and a
+// second found its pieces by walking the descriptor list, ~25 us of dependent
+// loads per piece.)
 constexpr uint32_t kTmaStage = 16384, kTmaStages = 2;
+constexpr uint64_t kScatterDescMax = 1ull << 20;
+constexpr uint64_t kPiecesPerDesc = kScatterDescMax / kTmaStage;
 
 __global__ void __launch_bounds__(32) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
     __shared__ __align__(128) uint8_t buf[kTmaStages * kTmaStage];
@@ -1388,61 +1393,43 @@ __global__ void __launch_bounds__(32) k_scatter(const ScatterDesc *desc, uint64_
     if (threadIdx.x != 0) return;
     for (uint32_t s = 0; s < kTmaStages; s++) mbar_init(&bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // walk (descriptor, piece) in order, keeping this CTA's pieces: a load
-    // cursor and a store cursor over the same sequence
-    struct Cur {
-        uint64_t i, o, g;  // descriptor, offset in it, global piece index of (i, o)
+    const uint64_t total = n * kPiecesPerDesc, G = gridDim.x;
+    // next piece of this CTA at or after u that lies inside its descriptor
+    auto seek = [&](uint64_t u) -> uint64_t {
+        for (; u < total; u += G)
+            if ((u % kPiecesPerDesc) * kTmaStage < desc[u / kPiecesPerDesc].bytes) return u;
+        return total;
     };
-    Cur lc{0, 0, 0}, sc{0, 0, 0};
-    const uint64_t G = gridDim.x, me = blockIdx.x;
-    auto seek = [&](Cur &c) -> bool {  // advance c to this CTA's next piece
-        for (;;) {
-            while (c.i < n && c.o >= desc[c.i].bytes) {
-                c.i++;
-                c.o = 0;
-            }
-            if (c.i >= n) return false;
-            if (c.g % G == me) return true;
-            const uint64_t skip = (me + G - c.g % G) % G;  // pieces to the next one of mine
-            const uint64_t left = (desc[c.i].bytes - c.o + kTmaStage - 1) / kTmaStage;
-            const uint64_t k = skip < left ? skip : left;
-            c.o += k * kTmaStage;
-            c.g += k;
-        }
-    };
-    auto step = [&](Cur &c) {
-        c.o += kTmaStage;
-        c.g++;
-    };
-    auto len_of = [&](const Cur &c) -> uint32_t {
-        const uint64_t r = desc[c.i].bytes - c.o;
+    auto len_of = [&](uint64_t u) -> uint32_t {
+        const uint64_t r = desc[u / kPiecesPerDesc].bytes - (u % kPiecesPerDesc) * kTmaStage;
         return (uint32_t)(r < kTmaStage ? r : kTmaStage);
     };
+    auto src_of = [&](uint64_t u) { return slot + desc[u / kPiecesPerDesc].src_off + (u % kPiecesPerDesc) * kTmaStage; };
+    auto dst_of = [&](uint64_t u) {
+        return reinterpret_cast<uint8_t *>(desc[u / kPiecesPerDesc].dst) + (u % kPiecesPerDesc) * kTmaStage;
+    };
+    uint64_t lu = seek(blockIdx.x), su = lu;
     uint32_t issued = 0, done = 0;
-    if (seek(lc)) {
-        const uint32_t len = len_of(lc);
-        mbar_expect_tx(&bar[0], len);
-        bulk_load(buf, slot + desc[lc.i].src_off + lc.o, len, &bar[0]);
-        step(lc);
+    if (lu < total) {
+        mbar_expect_tx(&bar[0], len_of(lu));
+        bulk_load(buf, src_of(lu), len_of(lu), &bar[0]);
+        lu = seek(lu + G);
         issued = 1;
     }
     while (done < issued) {
         const uint32_t s = done % kTmaStages;
-        // issue the next load into the other stage once the store that read it is done
-        if (issued == done + 1 && seek(lc)) {
+        if (lu < total) {  // the next load into the other stage, once the store that read it is done
             const uint32_t t = issued % kTmaStages;
             bulk_wait_read<0>();
-            const uint32_t len = len_of(lc);
-            mbar_expect_tx(&bar[t], len);
-            bulk_load(buf + t * kTmaStage, slot + desc[lc.i].src_off + lc.o, len, &bar[t]);
-            step(lc);
+            mbar_expect_tx(&bar[t], len_of(lu));
+            bulk_load(buf + t * kTmaStage, src_of(lu), len_of(lu), &bar[t]);
+            lu = seek(lu + G);
             issued++;
         }
         mbar_wait(&bar[s], (done / kTmaStages) & 1u);
-        seek(sc);
-        bulk_store(reinterpret_cast<uint8_t *>(desc[sc.i].dst) + sc.o, buf + s * kTmaStage, len_of(sc));
+        bulk_store(dst_of(su), buf + s * kTmaStage, len_of(su));
         bulk_commit();
-        step(sc);
+        su = seek(su + G);
         done++;
     }
     bulk_wait_all();
