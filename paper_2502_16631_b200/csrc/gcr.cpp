@@ -1288,7 +1288,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                                                   plan + p0, off + p0, masks + 32 * p0, c->slots[i % NS], c->n_sms,
                                                   c->packs));
                 CUDA_TRY(c, cudaEventRecord(kc, c->packs));
-                codec_ev.emplace_back(ca, kb);
+                codec_ev.emplace_back(ca, kc);  // KA + KB + KC of the sub-chunk
                 CUDA_TRY(c, cudaEventSynchronize(kb));
                 const unsigned long long sub_bytes = reinterpret_cast<volatile unsigned long long *>(c->ctot_h)[0];
                 const unsigned long long sub_present = reinterpret_cast<volatile unsigned long long *>(c->ctot_h)[1];
@@ -1413,7 +1413,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         CUDA_TRY(c, cudaEventElapsedTime(&ms, ce.first, ce.second));
         st.codec_dev_ns += (uint64_t)(ms * 1e6);
     }
-    if (coded) st.codec_dev_ns += st.pack_dev_ns;  // KC ran between pks / pke
+    if (coded) st.pack_dev_ns = 0;  // no K4 pack: the codec kernels (codec_dev_ns) staged the data
     st.present_raw_bytes = raw_present;
     const double host_stats = ns_since(host0) * 1e-6;
     if (trace) {  // GCR_TRACE=1: per-chunk timeline (ms from the checkpoint's first event) on stderr

@@ -1326,38 +1326,10 @@ __global__ void k_pm_entries(const AllocDev *allocs, const uint32_t *page_alloc,
     }
 }
 
-// ---- TMA bulk-copy helpers (cp.async.bulk: SASS UBLKCP) --------------------
-// Global <-> shared bulk copies driven by one thread, completion of loads
-// tracked by an mbarrier (transaction bytes), of stores by bulk groups.  Every
-// size and address is a multiple of 16 (R-2).
+// ---- TMA bulk stores (cp.async.bulk shared -> global: SASS UBLKCP) ---------
+// Driven by one thread, completion tracked by bulk groups.  Every size and
+// address is a multiple of 16 (R-2).
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(sdst)),
-                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 
 __device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
@@ -1366,79 +1338,39 @@ __device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_
 }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {  // at most N committed store groups still reading smem
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// K6: staged image pieces -> allocation pages, through the TMA engine.
-// Every descriptor is at most kScatterDescMax bytes (the restore planner cuts
-// runs into 1 MiB descriptors), so piece u of the launch is piece u mod M of
-// descriptor u / M (M = kScatterDescMax / kTmaStage; pieces past a short
-// descriptor's end are skipped): CTA c takes pieces c, c + grid, ... with no
-// search.  One elected thread per CTA streams its pieces through a 2-stage
-// shared-memory ring (bulk load -> mbarrier -> bulk store); four 32 KiB CTAs
-// per SM keep ~128 KiB in flight.  (A first version gave each CTA whole
-// descriptors -- 64 issuing threads for a 64 MiB group, 0.3 TB/s -- and a
-// second found its pieces by walking the descriptor list, ~25 us of dependent
-// loads per piece.)
-constexpr uint32_t kTmaStage = 16384, kTmaStages = 2;
-constexpr uint64_t kScatterDescMax = 1ull << 20;
-constexpr uint64_t kPiecesPerDesc = kScatterDescMax / kTmaStage;
+// K6: staged image pieces -> allocation pages (16-B vector copy, 256-thread
+// CTAs grid-striding over the descriptors, 4 loads in flight per thread).
+// A TMA version (one issuing thread per CTA streaming 16 KiB pieces through
+// a 2-stage bulk-load / bulk-store ring, 4 CTAs per SM) was built and
+// measured at 0.41-0.47 TB/s on staged C2 restores against ~5 TB/s for this
+// loop (profiles/r2m_bench_staged.json, r2n_bench_staged.json): reverted.
+constexpr uint32_t kTmaStage = 16384;
 
-__global__ void __launch_bounds__(32) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
-    __shared__ __align__(128) uint8_t buf[kTmaStages * kTmaStage];
-    __shared__ __align__(8) uint64_t bar[kTmaStages];
-    if (threadIdx.x != 0) return;
-    for (uint32_t s = 0; s < kTmaStages; s++) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint64_t total = n * kPiecesPerDesc, G = gridDim.x;
-    // next piece of this CTA at or after u that lies inside its descriptor
-    auto seek = [&](uint64_t u) -> uint64_t {
-        for (; u < total; u += G)
-            if ((u % kPiecesPerDesc) * kTmaStage < desc[u / kPiecesPerDesc].bytes) return u;
-        return total;
-    };
-    auto len_of = [&](uint64_t u) -> uint32_t {
-        const uint64_t r = desc[u / kPiecesPerDesc].bytes - (u % kPiecesPerDesc) * kTmaStage;
-        return (uint32_t)(r < kTmaStage ? r : kTmaStage);
-    };
-    auto src_of = [&](uint64_t u) { return slot + desc[u / kPiecesPerDesc].src_off + (u % kPiecesPerDesc) * kTmaStage; };
-    auto dst_of = [&](uint64_t u) {
-        return reinterpret_cast<uint8_t *>(desc[u / kPiecesPerDesc].dst) + (u % kPiecesPerDesc) * kTmaStage;
-    };
-    uint64_t lu = seek(blockIdx.x), su = lu;
-    uint32_t issued = 0, done = 0;
-    if (lu < total) {
-        mbar_expect_tx(&bar[0], len_of(lu));
-        bulk_load(buf, src_of(lu), len_of(lu), &bar[0]);
-        lu = seek(lu + G);
-        issued = 1;
-    }
-    while (done < issued) {
-        const uint32_t s = done % kTmaStages;
-        if (lu < total) {  // the next load into the other stage, once the store that read it is done
-            const uint32_t t = issued % kTmaStages;
-            bulk_wait_read<0>();
-            mbar_expect_tx(&bar[t], len_of(lu));
-            bulk_load(buf + t * kTmaStage, src_of(lu), len_of(lu), &bar[t]);
-            lu = seek(lu + G);
-            issued++;
+__global__ void __launch_bounds__(256) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint64_t dst = desc[i].dst, so = desc[i].src_off, by = desc[i].bytes;
+        const uint8_t *src = slot + so;
+        uint8_t *d = reinterpret_cast<uint8_t *>(dst);
+        constexpr int U = 4;
+        uint64_t off = (uint64_t)threadIdx.x * 16u;
+        const uint32_t stride = blockDim.x * 16u;
+        for (; off + (U - 1) * stride < by; off += U * stride) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) v[u] = ldg_stream(src + off + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; u++) *reinterpret_cast<uint4 *>(d + off + u * stride) = v[u];
         }
-        mbar_wait(&bar[s], (done / kTmaStages) & 1u);
-        bulk_store(dst_of(su), buf + s * kTmaStage, len_of(su));
-        bulk_commit();
-        su = seek(su + G);
-        done++;
+        for (; off < by; off += stride) *reinterpret_cast<uint4 *>(d + off) = ldg_stream(src + off);
     }
-    bulk_wait_all();
 }
 
 // K7: zero fill of ZERO runs: bulk stores from one zeroed 32 KiB smem buffer.
 __global__ void __launch_bounds__(128) k_zero_fill(const ZeroDesc *desc, uint64_t n) {
-    __shared__ __align__(128) uint4 zero[kTmaStage / 16];
-    for (uint32_t i = threadIdx.x; i < kTmaStage / 16; i += blockDim.x) zero[i] = make_uint4(0, 0, 0, 0);
+    __shared__ __align__(128) uint4 zero[2 * kTmaStage / 16];
+    for (uint32_t i = threadIdx.x; i < 2 * kTmaStage / 16; i += blockDim.x) zero[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy zeros visible to the bulk copies
     __syncthreads();
     if (threadIdx.x != 0) return;
@@ -1446,8 +1378,8 @@ __global__ void __launch_bounds__(128) k_zero_fill(const ZeroDesc *desc, uint64_
     for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
         uint8_t *d = reinterpret_cast<uint8_t *>(desc[i].dst);
         const uint64_t by = desc[i].bytes;
-        for (uint64_t off = 0; off < by; off += kTmaStage) {
-            bulk_store(d + off, zero, (uint32_t)(by - off < kTmaStage ? by - off : kTmaStage));
+        for (uint64_t off = 0; off < by; off += 2 * kTmaStage) {
+            bulk_store(d + off, zero, (uint32_t)(by - off < 2 * kTmaStage ? by - off : 2 * kTmaStage));
             if (++groups % 8 == 0) bulk_commit();
         }
     }
@@ -1601,7 +1533,8 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
-    k_scatter<<<(unsigned)(n_sms * 4), 32, 0, st>>>(desc, n, slot);  // 4 CTAs (32 KiB ring each) per SM
+    const uint64_t g = n < (uint64_t)n_sms * 8 ? n : (uint64_t)n_sms * 8;
+    k_scatter<<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
     return launched(1);
 }
 
