@@ -31,6 +31,16 @@ namespace gcr {
 namespace {
 
 constexpr int kCodecThreads = 256;  // 8 warps per CTA
+// A page of more than kSliceValues words (128 KiB) is worked on by several
+// warps, one per SLICE of kSliceValues values (32 blocks of 1024): a 2 MiB page
+// has 16.  Blocks are independent once the page's dictionaries are known, so
+// KC / KD slices need no coordination; KA slices OR their presence masks into
+// the page's (zeroed) masks and the last one to finish computes the size.
+constexpr uint32_t kSliceValues = 32u * 1024u;
+
+__host__ __device__ __forceinline__ uint32_t slices_of(uint32_t P) {
+    return P / 4u > kSliceValues ? P / 4u / kSliceValues : 1u;
+}
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t pad16(uint32_t x) { return (x + 15u) & ~15u; }
@@ -94,26 +104,33 @@ __device__ __forceinline__ void plane_counts(uint32_t mword, uint32_t (&d)[4]) {
 
 // KA.  plan[p] = stored length of chunk-local page p (0 if not PRESENT);
 // masks[32 p + w] = presence word w (plane w>>3, values 32(w&7) .. +31).
+// `done` (sliced pages only) counts the finished slices of each page (zeroed
+// by the host, re-zeroed by the page's last slice; KB reuses the array).
 __global__ void __launch_bounds__(kCodecThreads) k_codec_plan(const AllocDev *allocs, const uint32_t *page_alloc,
                                                               const uint8_t *cls, uint64_t pb, uint32_t np,
                                                               uint32_t P, uint32_t lg, uint32_t *plan,
-                                                              uint32_t *masks) {
+                                                              uint32_t *masks, uint32_t *done) {
     __shared__ uint32_t bm[kCodecThreads / 32][32 * 32];  // per warp: word (k*8+j) of lane l at [(k*8+j)*32 + l]
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     uint32_t *sm = bm[wib];
-    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t p = blockIdx.x * (blockDim.x >> 5) + wib; p < np; p += nw) {
+    const uint32_t S = slices_of(P);
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5), items = (uint64_t)np * S;
+    for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; u < items; u += nw) {
+        const uint32_t p = (uint32_t)(u / S), sl = (uint32_t)(u % S);
         const uint64_t g = pb + p;
         if ((cls[g] & 3u) != kClsPresent) {
-            if (lane == 0) plan[p] = 0u;
+            if (lane == 0 && sl == 0) plan[p] = 0u;
             continue;
         }
         const PageGeo q = page_geo(allocs, page_alloc, g, P, lg);
         const uint32_t n = q.len >> 2;
+        const uint32_t v0 = sl * kSliceValues;
+        if (v0 >= n) continue;  // a short tail page has fewer slices
+        const uint32_t v1 = min(n, v0 + kSliceValues);
 #pragma unroll
         for (int w = 0; w < 32; w++) sm[w * 32 + lane] = 0u;
         const uint4 *src = reinterpret_cast<const uint4 *>(q.base);
-        for (uint32_t i = lane; i < (n >> 2); i += 32u) {
+        for (uint32_t i = (v0 >> 2) + lane; i < (v1 >> 2); i += 32u) {
             const uint4 v = __ldg(src + i);
             const uint32_t xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -132,10 +149,21 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_plan(const AllocDev *al
 #pragma unroll 8
         for (uint32_t t = 0; t < 32; t++) acc |= sm[lane * 32 + ((t + lane) & 31u)];
         __syncwarp();
+        if (S > 1) {  // sliced page: merge into the page's masks; the last slice sizes the page
+            atomicOr(masks + (uint64_t)p * 32 + lane, acc);
+            __threadfence();
+            uint32_t last = 0;
+            if (lane == 0) last = atomicAdd(done + p, 1u) == (n + kSliceValues - 1) / kSliceValues - 1;
+            if (!__shfl_sync(kFull, last, 0)) continue;
+            __threadfence();
+            acc = __ldcg(masks + (uint64_t)p * 32 + lane);
+            if (lane == 0) done[p] = 0u;
+        } else {
+            masks[(uint64_t)p * 32 + lane] = acc;
+        }
         uint32_t d[4], mode[4];
         plane_counts(acc, d);
         const uint32_t C = coded_len(n, d, mode);
-        masks[(uint64_t)p * 32 + lane] = acc;
         if (lane == 0) plan[p] = C < q.len ? C : q.len;
     }
 }
@@ -262,18 +290,22 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_encode(const AllocDev *
     __shared__ uint8_t lut[kCodecThreads / 32][4][256];   // rank of each byte value, per plane
     __shared__ uint8_t dict[kCodecThreads / 32][4][128];  // dictionary (ascending), per plane
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
-    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
-    for (uint32_t p = blockIdx.x * (blockDim.x >> 5) + wib; p < np; p += nw) {
+    const uint32_t S = slices_of(P);
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5), items = (uint64_t)np * S;
+    for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; u < items; u += nw) {
+        const uint32_t p = (uint32_t)(u / S), sl = (uint32_t)(u % S);
         const uint64_t g = pb + p;
         if ((cls[g] & 3u) != kClsPresent) continue;
         const PageGeo q = page_geo(allocs, page_alloc, g, P, lg);
         const uint32_t stored = plan[p];
         uint8_t *dst = slot + off[p];
-        if (stored == q.len) {  // raw page
-            warp_copy16(dst, q.base, q.len, lane);
+        const uint32_t n = q.len >> 2;
+        if (sl * kSliceValues >= n) continue;
+        if (stored == q.len) {  // raw page: this slice's bytes
+            const uint32_t b0 = sl * kSliceValues * 4u, b1 = min(q.len, b0 + kSliceValues * 4u);
+            warp_copy16(dst + b0, q.base + b0, b1 - b0, lane);
             continue;
         }
-        const uint32_t n = q.len >> 2;
         const uint32_t mw = masks[(uint64_t)p * 32 + lane];
         uint32_t d[4], mode[4], so[4];
         plane_counts(mw, d);
@@ -295,8 +327,9 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_encode(const AllocDev *
                 if (r < 128u) dict[wib][k0][r] = (uint8_t)(32 * j0 + t);
             }
         __syncwarp();
-        // header (16 B) and the dictionaries of packed planes (zero-padded to 16)
-        if (lane == 0) {
+        // header (16 B), the dictionaries of packed planes (zero-padded to 16)
+        // and the code sections' tail padding: slice 0 of the page
+        if (lane == 0 && sl == 0) {
             uint4 h;
             h.x = mode[0] | mode[1] << 8 | mode[2] << 16 | mode[3] << 24;
             const uint32_t dm[4] = {mode[0] < 8 ? d[0] - 1 : 0u, mode[1] < 8 ? d[1] - 1 : 0u,
@@ -306,7 +339,7 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_encode(const AllocDev *
             *reinterpret_cast<uint4 *>(dst) = h;
         }
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < 4 && sl == 0; k++) {
             if (mode[k] == 8u) continue;
             const uint32_t dp = pad16(d[k]);
             if (4 * lane < dp) {
@@ -322,9 +355,9 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_encode(const AllocDev *
             const uint32_t cw = (n * mode[k] + 31u) / 32u, cb = pad16((n * mode[k] + 7u) / 8u) / 4u;
             if (lane < cb - cw) *reinterpret_cast<uint32_t *>(dst + so[k] + dp + 4 * (cw + lane)) = 0u;
         }
-        // blocks of 1024 values: lane l takes values [32 l, 32 l + 32) of the block
-        const uint32_t nblk = (n + 1023u) / 1024u;
-        for (uint32_t blk = 0; blk < nblk; blk++) {
+        // this slice's blocks of 1024 values: lane l takes values [32 l, 32 l + 32) of a block
+        const uint32_t nblk = (n + 1023u) / 1024u, bpsl = kSliceValues / 1024u;
+        for (uint32_t blk = sl * bpsl; blk < min(nblk, (sl + 1) * bpsl); blk++) {
             const uint32_t i0 = blk * 1024u + 32u * lane;
             uint32_t wv[32];
             const uint4 *s4 = reinterpret_cast<const uint4 *>(q.base) + (i0 >> 2);
@@ -374,17 +407,21 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_encode(const AllocDev *
 
 // KD.  One warp per descriptor: stored form at slot + src_off -> the page at dst.
 __global__ void __launch_bounds__(kCodecThreads) k_codec_decode(const DecodeDesc *desc, uint64_t n_desc,
-                                                                const uint8_t *slot) {
+                                                                const uint8_t *slot, uint32_t S) {
     __shared__ uint8_t dict[kCodecThreads / 32][4][128];
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
-    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < n_desc; i += nw) {
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5), items = n_desc * S;
+    for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wib; u < items; u += nw) {
+        const uint64_t i = u / S;
+        const uint32_t sl = (uint32_t)(u % S);
         const DecodeDesc dd = desc[i];
         uint8_t *dst = reinterpret_cast<uint8_t *>(dd.dst);
         const uint8_t *src = slot + dd.src_off;
         const uint32_t len = dd.len, stored = dd.stored, n = len >> 2;
+        if (sl * kSliceValues >= n) continue;
+        const uint32_t b0 = sl * kSliceValues * 4u, b1 = min(len, b0 + kSliceValues * 4u);  // this slice's bytes
         if (stored == len) {
-            warp_copy16(dst, src, len, lane);
+            warp_copy16(dst + b0, src + b0, b1 - b0, lane);
             continue;
         }
         // header + validation (R-19 malformed rule: the page restores as zeros)
@@ -409,7 +446,7 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_decode(const DecodeDesc
         }
         if (o != stored) bad = true;
         if (bad) {
-            for (uint32_t x = lane * 16u; x < len; x += 512u) *reinterpret_cast<uint4 *>(dst + x) = make_uint4(0, 0, 0, 0);
+            for (uint32_t x = b0 + lane * 16u; x < b1; x += 512u) *reinterpret_cast<uint4 *>(dst + x) = make_uint4(0, 0, 0, 0);
             continue;
         }
 #pragma unroll
@@ -418,8 +455,8 @@ __global__ void __launch_bounds__(kCodecThreads) k_codec_decode(const DecodeDesc
             for (uint32_t e = lane; e < 128u; e += 32u) dict[wib][k][e] = e < d[k] ? src[so[k] + e] : (uint8_t)0;
         }
         __syncwarp();
-        const uint32_t nblk = (n + 1023u) / 1024u;
-        for (uint32_t blk = 0; blk < nblk; blk++) {
+        const uint32_t nblk = (n + 1023u) / 1024u, bpsl = kSliceValues / 1024u;
+        for (uint32_t blk = sl * bpsl; blk < min(nblk, (sl + 1) * bpsl); blk++) {
             const uint32_t i0 = blk * 1024u + 32u * lane;
             uint32_t wv[32];
 #pragma unroll
@@ -474,11 +511,18 @@ static unsigned codec_grid(uint64_t items, int n_sms) {
 }
 
 int launch_codec_plan(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls, uint64_t page_begin,
-                      uint32_t n_pages, uint32_t P, uint32_t lg, uint32_t *plan, uint32_t *masks, int n_sms,
-                      cudaStream_t st) {
+                      uint32_t n_pages, uint32_t P, uint32_t lg, uint32_t *plan, uint32_t *masks, uint32_t *done,
+                      int n_sms, cudaStream_t st) {
     if (n_pages == 0) return 0;
-    k_codec_plan<<<codec_grid(n_pages, n_sms), kCodecThreads, 0, st>>>(allocs, page_alloc, cls, page_begin, n_pages,
-                                                                        P, lg, plan, masks);
+    const uint32_t S = slices_of(P);
+    if (S > 1) {  // sliced pages merge presence masks with atomics: start from zero
+        if (cudaMemsetAsync(masks, 0, 128ull * n_pages, st) != cudaSuccess ||
+            cudaMemsetAsync(done, 0, 4ull * n_pages, st) != cudaSuccess)
+            return -1;
+    }
+    k_codec_plan<<<codec_grid((uint64_t)n_pages * S, n_sms), kCodecThreads, 0, st>>>(allocs, page_alloc, cls,
+                                                                                    page_begin, n_pages, P, lg, plan,
+                                                                                    masks, done);
     return codec_launched(1);
 }
 
@@ -492,14 +536,16 @@ int launch_codec_encode(const AllocDev *allocs, const uint32_t *page_alloc, cons
                         uint32_t n_pages, uint32_t P, uint32_t lg, const uint32_t *plan, const uint32_t *off,
                         const uint32_t *masks, uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n_pages == 0) return 0;
-    k_codec_encode<<<codec_grid(n_pages, n_sms), kCodecThreads, 0, st>>>(allocs, page_alloc, cls, page_begin,
+    k_codec_encode<<<codec_grid((uint64_t)n_pages * slices_of(P), n_sms), kCodecThreads, 0, st>>>(allocs, page_alloc, cls, page_begin,
                                                                           n_pages, P, lg, plan, off, masks, slot);
     return codec_launched(1);
 }
 
-int launch_codec_decode(const DecodeDesc *desc, uint64_t n_desc, const uint8_t *slot, int n_sms, cudaStream_t st) {
+int launch_codec_decode(const DecodeDesc *desc, uint64_t n_desc, const uint8_t *slot, uint32_t page_size, int n_sms,
+                        cudaStream_t st) {
     if (n_desc == 0) return 0;
-    k_codec_decode<<<codec_grid(n_desc, n_sms), kCodecThreads, 0, st>>>(desc, n_desc, slot);
+    const uint32_t S = slices_of(page_size);
+    k_codec_decode<<<codec_grid(n_desc * S, n_sms), kCodecThreads, 0, st>>>(desc, n_desc, slot, S);
     return codec_launched(1);
 }
 

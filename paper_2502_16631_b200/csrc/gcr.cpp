@@ -1276,7 +1276,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                 cudaEvent_t ca = c->ev(), kb = c->ev(), kc = c->ev();
                 CUDA_TRY(c, cudaEventRecord(ca, c->packs));
                 LAUNCH_TRY(c, launch_codec_plan(c->allocs_d, c->page_alloc, c->cls, ch.page_begin + p0, n, P, c->lg,
-                                                plan + p0, masks + 32 * p0, c->n_sms, c->packs));
+                                                plan + p0, masks + 32 * p0, off + p0, c->n_sms, c->packs));
                 LAUNCH_TRY(c, launch_codec_offsets(plan + p0, n, off + p0, c->stored_d, pres_base, slot_base,
                                                    c->ctot_map, c->packs));
                 CUDA_TRY(c, cudaEventRecord(kb, c->packs));
@@ -1759,7 +1759,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
             cudaEvent_t a = c->ev(), b = c->ev();
             CUDA_TRY(c, cudaEventRecord(a, cs));
             if (it.decode)
-                LAUNCH_TRY(c, launch_codec_decode(dd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
+                LAUNCH_TRY(c, launch_codec_decode(dd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], P, c->n_sms, cs));
             else
                 LAUNCH_TRY(c, launch_scatter(sd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
             CUDA_TRY(c, cudaEventRecord(b, cs));

@@ -226,7 +226,7 @@ size_t scan_smem_bytes();
 // per page (0 if not PRESENT) and presence masks (32 u32 per page).
 int launch_codec_plan(const AllocDev *allocs, const uint32_t *page_alloc, const uint8_t *cls, uint64_t page_begin,
                       uint32_t n_pages, uint32_t page_size, uint32_t log2_page, uint32_t *plan, uint32_t *masks,
-                      int n_sms, cudaStream_t st);
+                      uint32_t *done, int n_sms, cudaStream_t st);
 // KB: slot offsets (from slot_base), the image's compact stored-length table
 // from present_base on, {stored total, PRESENT count} into mapped host memory.
 int launch_codec_offsets(const uint32_t *plan, uint32_t n_pages, uint32_t *off, uint32_t *stored_compact,
@@ -236,7 +236,8 @@ int launch_codec_encode(const AllocDev *allocs, const uint32_t *page_alloc, cons
                         uint32_t n_pages, uint32_t page_size, uint32_t log2_page, const uint32_t *plan,
                         const uint32_t *off, const uint32_t *masks, uint8_t *slot, int n_sms, cudaStream_t st);
 // KD: restore a staged group of stored pages.
-int launch_codec_decode(const DecodeDesc *desc, uint64_t n_desc, const uint8_t *slot, int n_sms, cudaStream_t st);
+int launch_codec_decode(const DecodeDesc *desc, uint64_t n_desc, const uint8_t *slot, uint32_t page_size, int n_sms,
+                        cudaStream_t st);
 
 // ---- host CRC32C math (crc_host.cpp), independent of oracle/ --------------
 void build_tables(CrcTables *out);

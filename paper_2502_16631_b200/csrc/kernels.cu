@@ -1102,19 +1102,6 @@ __global__ void k_build_page_table(const AllocDev *allocs, uint32_t *page_alloc,
 }
 
 // Warp-cooperative 16-byte-vector copy of `bytes` (multiple of 16).
-__device__ __forceinline__ void warp_copy(uint8_t *dst, const uint8_t *src, uint64_t bytes, uint32_t lane) {
-    constexpr int U = 8;
-    uint64_t off = (uint64_t)lane * 16u;
-    for (; off + (U - 1) * 512u < bytes; off += U * 512u) {
-        uint4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) v[u] = ldg_stream(src + off + u * 512u);
-#pragma unroll
-        for (int u = 0; u < U; u++) *reinterpret_cast<uint4 *>(dst + off + u * 512u) = v[u];
-    }
-    for (; off < bytes; off += 512u)
-        *reinterpret_cast<uint4 *>(dst + off) = ldg_stream(src + off);
-}
 
 // K1 leaves kFreeSMs SMs unoccupied so that K2/K4 (and the restore's K6)
 // start the moment they are enqueued instead of waiting
