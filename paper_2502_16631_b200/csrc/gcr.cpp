@@ -1646,7 +1646,21 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     std::vector<ImgPlan> plans(n);
     std::vector<ScatterDesc> sdesc;
     std::vector<ZeroDesc> zdesc;
-    std::vector<DecodeDesc> ddesc;
+    // f4 decode descriptors (one per PRESENT page of a coded image) are written
+    // straight into the pinned descriptor buffer, ahead of the scatter / zero
+    // descriptors (a 4 KiB-page C2 image has 364 k of them: building a vector
+    // and copying it cost ~10 ms of host time per restore)
+    uint64_t n_dec = 0, desc_bound = 0;
+    for (uint32_t k = 0; k < n; k++) {
+        const gcr_image_hdr &h = chain[k]->hdr;
+        if (h.flags & 2u) n_dec += h.n_present;
+        else desc_bound += h.n_entries + h.image_bytes / kPieceBytes + h.image_bytes / kGroupMax + 2;
+        desc_bound += h.n_entries + h.n_zero * (P / kPieceBytes + 1) + 1;
+    }
+    s = ensure_desc(c, sizeof(DecodeDesc) * n_dec + sizeof(ScatterDesc) * desc_bound + 64);
+    if (s != GCR_OK) return s;
+    DecodeDesc *ddh = reinterpret_cast<DecodeDesc *>(c->desc_h);
+    uint64_t nd = 0;
     uint64_t h2d_bytes = 0, direct_bytes = 0;
     for (uint32_t k = 0; k < n; k++) {
         const gcr_image *im = chain[k];
@@ -1656,7 +1670,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         const bool coded = im->hdr.flags & 2u;
         bool group_open = false;
         auto close_group = [&]() {
-            if (group_open) pl.items.back().d_end = coded ? ddesc.size() : sdesc.size();
+            if (group_open) pl.items.back().d_end = coded ? nd : sdesc.size();
             group_open = false;
         };
         for (uint32_t a = 0; a < im->hdr.n_allocs; a++) {
@@ -1672,15 +1686,17 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                     // f4: every page's stored form goes through a slot; groups of
                     // consecutive stored forms up to one slot, one decode
                     // descriptor per page
+                    const uint64_t base_a = c->reg[a].dptr;
+                    const uint32_t tail = (uint32_t)page_len(c->reg[a].bytes, P, m - 1);
                     for (uint64_t q = p; q < last; q++) {
-                        const uint32_t L = (uint32_t)page_len(c->reg[a].bytes, P, q), sl = im->stored[ip++];
+                        const uint32_t L = q == m - 1 ? tail : P, sl = im->stored[ip++];
                         if (group_open && pl.items.back().bytes + sl > group_max) close_group();
                         if (!group_open) {
-                            pl.items.push_back(Item{false, cursor, 0, 0, ddesc.size(), 0, true});
+                            pl.items.push_back(Item{false, cursor, 0, 0, nd, 0, true});
                             group_open = true;
                         }
                         Item &g = pl.items.back();
-                        ddesc.push_back(DecodeDesc{c->reg[a].dptr + q * P, cursor - g.img_off, L, sl});
+                        ddh[nd++] = DecodeDesc{base_a + q * P, cursor - g.img_off, L, sl};
                         g.bytes += sl;
                         cursor += sl;
                     }
@@ -1727,16 +1743,15 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         h2d_bytes += im->hdr.image_bytes;
     }
     const uint64_t sbytes = sizeof(ScatterDesc) * sdesc.size(), zbytes = sizeof(ZeroDesc) * zdesc.size();
-    const uint64_t dbytes = sizeof(DecodeDesc) * ddesc.size();
-    s = ensure_desc(c, sbytes + zbytes + dbytes + 16);
-    if (s != GCR_OK) return s;
-    std::memcpy(c->desc_h, sdesc.data(), sbytes);
-    std::memcpy(c->desc_h + sbytes, zdesc.data(), zbytes);
-    std::memcpy(c->desc_h + sbytes + zbytes, ddesc.data(), dbytes);
-    const ScatterDesc *sd = reinterpret_cast<const ScatterDesc *>(c->desc_d);
-    const ZeroDesc *zd = reinterpret_cast<const ZeroDesc *>(c->desc_d + sbytes);
-    const DecodeDesc *dd = reinterpret_cast<const DecodeDesc *>(c->desc_d + sbytes + zbytes);
-    CUDA_TRY(c, cudaMemcpyAsync(c->desc_d, c->desc_h, sbytes + zbytes + dbytes, cudaMemcpyHostToDevice, c->compute));
+    const uint64_t dbytes = sizeof(DecodeDesc) * nd;  // already in place at the buffer's start
+    if (nd != n_dec || dbytes + sbytes + zbytes + 64 > c->desc_cap)
+        return fail(c, GCR_E_CUDA, "restore: descriptor plan exceeds its bound");
+    std::memcpy(c->desc_h + dbytes, sdesc.data(), sbytes);
+    std::memcpy(c->desc_h + dbytes + sbytes, zdesc.data(), zbytes);
+    const DecodeDesc *dd = reinterpret_cast<const DecodeDesc *>(c->desc_d);
+    const ScatterDesc *sd = reinterpret_cast<const ScatterDesc *>(c->desc_d + dbytes);
+    const ZeroDesc *zd = reinterpret_cast<const ZeroDesc *>(c->desc_d + dbytes + sbytes);
+    CUDA_TRY(c, cudaMemcpyAsync(c->desc_d, c->desc_h, dbytes + sbytes + zbytes, cudaMemcpyHostToDevice, c->compute));
 
     // ---- apply the chain ----------------------------------------------------
     std::vector<cudaEvent_t> sc0, sc1, dc0, dc1;  // scatter+zero / f4 decode spans

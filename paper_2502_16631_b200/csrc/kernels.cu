@@ -1327,28 +1327,37 @@ __device__ __forceinline__ void bulk_store(void *gdst, const void *ssrc, uint32_
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// K6: staged image pieces -> allocation pages (16-B vector copy, 256-thread
-// CTAs grid-striding over the descriptors, 4 loads in flight per thread).
-// A TMA version (one issuing thread per CTA streaming 16 KiB pieces through
-// a 2-stage bulk-load / bulk-store ring, 4 CTAs per SM) was built and
-// measured at 0.41-0.47 TB/s on staged C2 restores against ~5 TB/s for this
-// loop (profiles/r2m_bench_staged.json, r2n_bench_staged.json): reverted.
+// K6: staged image pieces -> allocation pages.  Descriptors are at most
+// kScatterDescMax (1 MiB: the restore planner's piece size), so work piece u
+// of a launch is the 64 KiB piece u mod 16 of descriptor u / 16 (pieces past a
+// short descriptor's end are empty): CTAs grid-stride over pieces, not
+// descriptors, so a 64 MiB group (64 descriptors) still spreads over every SM.
+// 256 threads x 4 x 16 B per step, loads before stores.  (One CTA per
+// descriptor left a 64 MiB group on 64 CTAs: 0.25 TB/s.  A TMA ring -- one
+// issuing thread per CTA, bulk load -> mbarrier -> bulk store -- measured
+// 0.41-0.47 TB/s: profiles/r2m_bench_staged.json, r2n_bench_staged.json.)
 constexpr uint32_t kTmaStage = 16384;
+constexpr uint64_t kScatterDescMax = 1ull << 20, kScatterPiece = 65536;
+constexpr uint64_t kPiecesPerDesc = kScatterDescMax / kScatterPiece;
 
 __global__ void __launch_bounds__(256) k_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot) {
-    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const uint64_t dst = desc[i].dst, so = desc[i].src_off, by = desc[i].bytes;
-        const uint8_t *src = slot + so;
-        uint8_t *d = reinterpret_cast<uint8_t *>(dst);
+    const uint64_t total = n * kPiecesPerDesc;
+    for (uint64_t u = blockIdx.x; u < total; u += gridDim.x) {
+        const ScatterDesc dd = desc[u / kPiecesPerDesc];
+        const uint64_t p0 = (u % kPiecesPerDesc) * kScatterPiece;
+        if (p0 >= dd.bytes) continue;
+        const uint64_t by = min(dd.bytes - p0, kScatterPiece);
+        const uint8_t *src = slot + dd.src_off + p0;
+        uint8_t *d = reinterpret_cast<uint8_t *>(dd.dst) + p0;
         constexpr int U = 4;
         uint64_t off = (uint64_t)threadIdx.x * 16u;
         const uint32_t stride = blockDim.x * 16u;
         for (; off + (U - 1) * stride < by; off += U * stride) {
             uint4 v[U];
 #pragma unroll
-            for (int u = 0; u < U; u++) v[u] = ldg_stream(src + off + u * stride);
+            for (int w = 0; w < U; w++) v[w] = ldg_stream(src + off + w * stride);
 #pragma unroll
-            for (int u = 0; u < U; u++) *reinterpret_cast<uint4 *>(d + off + u * stride) = v[u];
+            for (int w = 0; w < U; w++) *reinterpret_cast<uint4 *>(d + off + w * stride) = v[w];
         }
         for (; off < by; off += stride) *reinterpret_cast<uint4 *>(d + off) = ldg_stream(src + off);
     }
@@ -1520,8 +1529,8 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
-    const uint64_t g = n < (uint64_t)n_sms * 8 ? n : (uint64_t)n_sms * 8;
-    k_scatter<<<(unsigned)g, 256, 0, st>>>(desc, n, slot);
+    const uint64_t pieces = n * kPiecesPerDesc, cap = (uint64_t)n_sms * 8;
+    k_scatter<<<(unsigned)(pieces < cap ? pieces : cap), 256, 0, st>>>(desc, n, slot);
     return launched(1);
 }
 
