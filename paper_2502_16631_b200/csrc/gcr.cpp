@@ -1109,7 +1109,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     // pinned image; the other PRESENT tiles are packed (K4) into the chunk's
     // staging slot and copied out in contiguous ranges.
     uint64_t base = 0, n_present = 0, n_zero = 0, n_parent = 0, raw_present = 0;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> codec_ev;  // f4: KA+KB and KC spans
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> codec_ev;  // f4: KA+KB+KC span per sub-chunk
+    struct SubTrace {  // GCR_TRACE: per f4 sub-chunk
+        size_t chunk;
+        cudaEvent_t ka, kb, kc, d2h;
+        double host_enq;
+    };
+    std::vector<SubTrace> subs;
     Clock::time_point drain0;
     const size_t S = c->copy.size(), NS = c->slots.size();
     const uint64_t direct_min = c->cfg.direct_min_bytes;
@@ -1297,6 +1303,11 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                     CUDA_TRY(c, cudaMemcpyAsync(img->data + base + slot_base, c->slots[i % NS] + slot_base, sub_bytes,
                                                 cudaMemcpyDeviceToHost, cs));
                 }
+                if (trace) {
+                    cudaEvent_t e = c->ev();
+                    CUDA_TRY(c, cudaEventRecord(e, cs));
+                    subs.push_back(SubTrace{i, ca, kb, kc, e, ns_since(host0) * 1e-6});
+                }
                 slot_base += sub_bytes;
                 pres_base += sub_present;
             }
@@ -1428,8 +1439,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
         for (size_t i = 0; i < nch; i++)
             std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %.3f, %.3f, %.3f]", i ? ", " : "", rel(k2s[i]),
                          rel(tot[i]), rel(pks[i]), rel(pke[i]), rel(dde[i]), host_seen[i], host_enq[i]);
+        std::fprintf(stderr, "], \"subs\": [");
+        for (size_t k = 0; k < subs.size(); k++)
+            std::fprintf(stderr, "%s[%zu, %.3f, %.3f, %.3f, %.3f, %.3f]", k ? ", " : "", subs[k].chunk, rel(subs[k].ka),
+                         rel(subs[k].kb), rel(subs[k].kc), rel(subs[k].d2h), subs[k].host_enq);
         std::fprintf(stderr, "], \"pagemap\": [%.3f, %.3f], \"fields\": {\"scans\": \"chunk_lo chunk_hi k1_start "
-                             "k1_end\", \"chunks\": \"k2_start k2_end pack_start pack_end d2h_end host_saw_k2 host_enqueued\"}}\n",
+                             "k1_end\", \"chunks\": \"k2_start k2_end pack_start pack_end d2h_end host_saw_k2 host_enqueued\", "
+                             "\"subs\": \"chunk codec_start kb_done kc_done d2h_done host_enqueued\"}}\n",
                      rel(pm0), rel(pm1));
     }
     st.scan_launches = 1;
@@ -1713,7 +1729,10 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                         }
                     } else {
                         while (bytes) {
-                            if (group_open && pl.items.back().bytes + bytes > group_max) close_group();
+                            // a group closes when full: runs are cut across groups as needed (a
+                            // test against the whole remaining run closed a group per 1 MiB piece
+                            // of any run longer than a group)
+                            if (group_open && pl.items.back().bytes >= group_max) close_group();
                             if (!group_open) {
                                 pl.items.push_back(Item{false, cursor, 0, 0, sdesc.size(), 0, false});
                                 group_open = true;
