@@ -49,7 +49,7 @@ def main():
         n = mib << 20
         t = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda")
         torch.cuda.synchronize()
-        for P in (65536, 2097152):
+        for P in (4096, 65536, 2097152):
             res = {"cur": [], "old": []}
             for rep in range(4):
                 for k in ("old", "cur"):
