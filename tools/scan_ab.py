@@ -34,8 +34,10 @@ def main():
         for f in ("kernels.cu", "gcr_internal.h", "crc_host.cpp"):
             data = subprocess.check_output(["git", "-C", ROOT, "show", f"{rev}:paper_2502_16631_b200/csrc/{f}"])
             open(os.path.join(old_dir, f), "wb").write(data)
-        build("old", old_dir, ["-DSCAN_AB_R1"])
-        open(os.path.join(ROOT, "tools", "scan_ab", "old", "REV"), "w").write(rev)
+        has_basis = b"table_basis" in open(os.path.join(old_dir, "crc_host.cpp"), "rb").read()
+        build("old", old_dir, [] if has_basis else ["-DSCAN_AB_R1"])
+        full = subprocess.check_output(["git", "-C", ROOT, "rev-parse", "--short", rev]).decode().strip()
+        open(os.path.join(ROOT, "tools", "scan_ab", "old", "REV"), "w").write(full)
         return
     rev = open(os.path.join(ROOT, "tools", "scan_ab", "old", "REV")).read().strip()
     sizes = [int(x) for x in sys.argv[1:]] or [1024, 4096]
