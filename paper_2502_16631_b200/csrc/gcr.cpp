@@ -27,6 +27,7 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: a no-op unless a tool (nsys) injects itself
 #include <cuda.h>  // VMM types only: entry points come from cudaGetDriverEntryPoint (no -lcuda)
 
 #include "../../include/gcr.h"
@@ -44,6 +45,16 @@ static_assert(sizeof(gcr_alloc_rec) == 24 && sizeof(gcr_pagemap_entry) == 16, "r
 namespace {
 
 using Clock = std::chrono::steady_clock;
+// NVTX range over an API call or a pipeline stage (gcr.lock, gcr.checkpoint,
+// gcr.checkpoint.pagemap, gcr.restore, gcr.restore.verify, ...): nsys shows
+// the library's phases on the host timeline next to its kernels and copies.
+struct NvtxScope {
+    explicit NvtxScope(const char *name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+    NvtxScope(const NvtxScope &) = delete;
+    NvtxScope &operator=(const NvtxScope &) = delete;
+};
+
 uint64_t ns_since(Clock::time_point t0) {
     return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count();
 }
@@ -895,6 +906,7 @@ gcr_status gcr_reserve_host(gcr_ctx *c, uint64_t bytes) {
 }
 
 gcr_status gcr_lock(gcr_ctx *c) {
+    NvtxScope nvtx_("gcr.lock");
     if (!c) return GCR_E_INVAL;
     if (c->phase != GCR_RUNNING) return fail(c, GCR_E_STATE, "lock: not RUNNING");
     auto t0 = Clock::now();
@@ -963,6 +975,7 @@ gcr_status gcr_lock(gcr_ctx *c) {
 }
 
 gcr_status gcr_unlock(gcr_ctx *c) {
+    NvtxScope nvtx_("gcr.unlock");
     if (!c) return GCR_E_INVAL;
     if (c->phase == GCR_RELEASED) return fail(c, GCR_E_STATE, "unlock: device memory is released; restore first");
     if (c->phase != GCR_LOCKED && c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "unlock: not locked");
@@ -1376,6 +1389,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     }
     // K3 pagemap over all pages (maximal runs, independent of chunking): every
     // class is final once the last K1 (same stream) has ended.
+    NvtxScope nvtx_finish("gcr.checkpoint.pagemap_meta");
     auto pm0 = c->ev(), pm1 = c->ev();
     CUDA_TRY(c, cudaEventRecord(pm0, c->compute));
     LAUNCH_TRY(c, launch_pagemap_count(c->cls, c->n_pages, c->pm_blk_cnt, c->pm_blk_off, c->nent_map, c->compute));
@@ -1496,6 +1510,7 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
 }
 
 gcr_status gcr_checkpoint(gcr_ctx *c, gcr_mode mode, gcr_image **out) {
+    NvtxScope nvtx_("gcr.checkpoint");
     if (!c) return GCR_E_INVAL;
     if (!out) return fail(c, GCR_E_INVAL, "checkpoint: out is NULL");
     *out = nullptr;
@@ -1816,6 +1831,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     }
     st.restore_direct_bytes = direct_bytes;
     // ---- verify: recompute every digest and compare with D_k (R-11) ---------
+    NvtxScope nvtx_verify("gcr.restore.verify");
     const gcr_image *last = chain[n - 1];
     const int scratch = c->have_parent ? 1 - c->parent_idx : 0;
     CUDA_TRY(c, cudaMemcpyAsync(c->D[scratch], last->digests, 4 * c->n_pages, cudaMemcpyHostToDevice, c->compute));
@@ -1945,6 +1961,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
 }
 
 gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
+    NvtxScope nvtx_("gcr.restore");
     if (!c) return GCR_E_INVAL;
     const gcr_phase ph0 = c->phase;
     bool writes_began = false;
@@ -2010,6 +2027,7 @@ gcr_status gcr_mem_free(gcr_ctx *c, uint64_t dptr) {
 }
 
 gcr_status gcr_release(gcr_ctx *c) {
+    NvtxScope nvtx_("gcr.release");
     if (!c) return GCR_E_INVAL;
     if (c->phase != GCR_CHECKPOINTED) return fail(c, GCR_E_STATE, "release: not CHECKPOINTED");
     // every registered allocation inside a block; every touched block fully registered
@@ -2049,6 +2067,7 @@ gcr_status gcr_release(gcr_ctx *c) {
 }
 
 gcr_status gcr_probe_link(gcr_ctx *c, uint64_t bytes, double *d2h_gbs, double *h2d_gbs) {
+    NvtxScope nvtx_("gcr.probe_link");
     if (!c) return GCR_E_INVAL;
     if (!d2h_gbs || !h2d_gbs || bytes == 0 || bytes > c->cfg.chunk_bytes || c->slots.empty())
         return fail(c, GCR_E_INVAL, "probe_link: null output, or bytes not in (0, chunk_bytes]");
@@ -2186,6 +2205,7 @@ gcr_status gcr_image_serialize(const gcr_image *img, void *dst, uint64_t cap) {
 }
 
 gcr_status gcr_image_import(gcr_ctx *c, const void *stream, uint64_t bytes, gcr_image **out) {
+    NvtxScope nvtx_("gcr.import");
     if (!c) return GCR_E_INVAL;
     if (!stream || !out) return fail(c, GCR_E_INVAL, "import: null argument");
     *out = nullptr;
@@ -2296,6 +2316,7 @@ int parallel_io(int fd, const std::vector<IoSeg> &segs, uint32_t n_threads, bool
 extern "C" {
 
 gcr_status gcr_image_write_file(const gcr_image *img, const char *path, uint32_t n_threads, uint32_t flags) {
+    NvtxScope nvtx_("gcr.write_file");
     if (!img || !path) return GCR_E_INVAL;
     gcr_ctx *c = img->ctx;
     const gcr_image_hdr &h = img->hdr;
@@ -2336,6 +2357,7 @@ gcr_status gcr_image_write_file(const gcr_image *img, const char *path, uint32_t
 }
 
 gcr_status gcr_image_read_file(gcr_ctx *c, const char *path, uint32_t n_threads, gcr_image **out) {
+    NvtxScope nvtx_("gcr.read_file");
     if (!c) return GCR_E_INVAL;
     if (!path || !out) return fail(c, GCR_E_INVAL, "read_file: null argument");
     *out = nullptr;
