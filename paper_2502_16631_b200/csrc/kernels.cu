@@ -966,9 +966,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             AllocView lal = load_alloc(p.allocs + la, P);
             uint64_t lgi = g0 - __ldg(&p.allocs[la].grp0), lgg = g0;
             GroupLane<G> lgl = group_lane<G>(lal, lgi, P, lg, q, m);
-            // every page of the group present and full length (no tail padding):
-            // unpredicated loads (the common case; warp-uniform)
-            bool lfull = __all_sync(kFull, lgl.valid && lgl.pad == 0u);
             uint32_t lb = 0;
             uint32_t pa = la;
             AllocView pal = lal;
@@ -982,15 +979,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                     const uint64_t e = min(nx + (uint64_t)G * P, lal.base + __ldg(&p.allocs[la].bytes));
                     if (e > nx) prefetch_l2(reinterpret_cast<const void *>(nx), (uint32_t)(e - nx));
                 }
-                if (lfull) {
 #pragma unroll
-                    for (uint32_t u = 0; u < U; u++) w[u] = ldg_stream(lgl.ptr + (lb * U + u) * Wr);
-                } else {
-#pragma unroll
-                    for (uint32_t u = 0; u < U; u++) {
-                        const uint32_t off = (lb * U + u) * Wr;
-                        w[u] = lgl.valid && off + m * 16u >= lgl.pad ? ldg_stream(lgl.ptr + off) : make_uint4(0, 0, 0, 0);
-                    }
+                for (uint32_t u = 0; u < U; u++) {
+                    const uint32_t off = (lb * U + u) * Wr;
+                    w[u] = lgl.valid && off + m * 16u >= lgl.pad ? ldg_stream(lgl.ptr + off) : make_uint4(0, 0, 0, 0);
                 }
                 if (++lb == NB) {  // next group
                     lb = 0;
@@ -1002,7 +994,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                             lgi = 0;
                         }
                         lgl = group_lane<G>(lal, lgi, P, lg, q, m);
-                        lfull = __all_sync(kFull, lgl.valid && lgl.pad == 0u);
                     }
                 }
             };

@@ -29,9 +29,6 @@ extern "C" int scan_ab_time(uint64_t dptr, uint64_t bytes, uint32_t P, int iters
     a.tail_len = (uint32_t)(bytes - (uint64_t)(a.n_pages - 1) * P);
     a.z_tail = zero_digest(a.tail_len);
     a.n_rows = (uint64_t)(a.n_pages - 1) * (P / kRowBytes) + (a.tail_len + kRowBytes - 1) / kRowBytes;
-    const bool grp = P == kGroupBytes / 4 || P == kGroupBytes / 2;  // K1g for 4 / 8 KiB pages
-    const uint64_t G = grp ? kGroupBytes / P : 1, groups = (a.n_pages + G - 1) / G;
-    a.grp0 = 0;
     AllocDev *ad;
     cudaMalloc(&ad, sizeof a);
     cudaMemcpy(ad, &a, sizeof a, cudaMemcpyHostToDevice);
@@ -54,15 +51,7 @@ extern "C" int scan_ab_time(uint64_t dptr, uint64_t bytes, uint32_t P, int iters
     cudaMalloc(&misc, 16);
     cudaMalloc(&dref, 4ull * a.n_pages);
     cudaMemset(dref, 0, 4ull * a.n_pages);
-    uint64_t cg[2] = {0, groups};
-    uint64_t *cgd = nullptr;
-    if (grp) {
-        cudaMalloc(&cgd, 16);
-        cudaMemcpy(cgd, cg, 16, cudaMemcpyHostToDevice);
-    }
     ScanParams sp{};
-    sp.chunk_groups = cgd;
-    sp.grp_pf_block = grp_prefetch_block();
     sp.allocs = ad;
     sp.n_allocs = 1;
     sp.chunk_rows = crd;
@@ -83,7 +72,7 @@ extern "C" int scan_ab_time(uint64_t dptr, uint64_t bytes, uint32_t P, int iters
     sp.tables = td;
     sp.prefetch = scan_prefetch_bytes();
 #ifndef SCAN_AB_R1
-    table_basis(P == kGroupBytes / 4 ? th->a128 : P == kGroupBytes / 2 ? th->a256 : th->braid, sp.basis[0]);
+    table_basis(th->braid, sp.basis[0]);
     table_basis(th->t4, sp.basis[1]);
     table_basis(th->a16, sp.basis[2]);
     table_basis(th->a32, sp.basis[3]);
@@ -108,7 +97,6 @@ extern "C" int scan_ab_time(uint64_t dptr, uint64_t bytes, uint32_t P, int iters
         if (it) total += ms;  // first launch: warm-up
     }
     *ms_out = total / iters;
-    if (cgd) cudaFree(cgd);
     cudaFree(ad); cudaFree(crd); cudaFree(td); cudaFree(fold); cudaFree(sync); cudaFree(misc); cudaFree(dref);
     delete th;
     cudaStreamDestroy(st);
