@@ -63,6 +63,7 @@ constexpr uint64_t kMaxChunk = 2ull << 30;
 constexpr uint64_t kPieceBytes = 1ull << 20;  // restore descriptor granularity (K6 assumes <= 1 MiB)
 constexpr uint64_t kGroupMax = 64ull << 20;   // restore: bytes per staged H2D group
 constexpr uint64_t kCodecSub = 256ull << 20;  // f4 checkpoint: page bytes per encode + D2H sub-chunk
+constexpr uint64_t kCodecSubFirst = 32ull << 20;  // f4 checkpoint: the first chunk's first sub-chunk (ramp start)
 constexpr size_t kDigestChunks = 4;           // checkpoint: chunks per digest D2H
 const char kMagic[8] = {'G', 'C', 'R', 'I', 'M', 'G', 0x00, 0x01};
 
@@ -349,6 +350,7 @@ struct gcr_ctx {
     uint64_t prev_parent_gen = 0, prev_next_gen = 1;
 
     std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t ev_spec = nullptr;  // restore: the speculative prefix H2D (outlives the pool's per-call reset)
     size_t ev_used = 0;
     cudaEvent_t ev() {
         if (ev_used == ev_pool.size()) {
@@ -790,6 +792,7 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     if (cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     if (cudaStreamCreateWithFlags(&c->post, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     if (cudaStreamCreateWithFlags(&c->packs, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
+    if (cudaEventCreate(&c->ev_spec) != cudaSuccess) return bail(GCR_E_CUDA);
     for (uint32_t i = 0; i < cfg.n_copy_streams; i++) {
         cudaStream_t s;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
@@ -838,6 +841,7 @@ gcr_status gcr_destroy(gcr_ctx *c) {
     if (c->compute) cudaStreamDestroy(c->compute);
     if (c->post) cudaStreamDestroy(c->post);
     if (c->packs) cudaStreamDestroy(c->packs);
+    if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     if (c->tables_d) cudaFree(c->tables_d);
     if (c->desc_d) cudaFree(c->desc_d);
     if (c->desc_h) cudaFreeHost(c->desc_h);
@@ -1289,9 +1293,13 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
                 return e ? std::strtoull(e, nullptr, 0) << 20 : kCodecSub;
             }();
             const uint64_t sub_pages = std::max<uint64_t>(1, sub_bytes_cfg / P);
+            // the first chunk ramps its sub-chunks up (32, 64, 128 MiB, then the
+            // configured size): the link starts after 32 MiB is coded, not 256
+            uint64_t ramp_pages = i == 0 ? std::max<uint64_t>(1, std::min<uint64_t>(kCodecSubFirst, sub_bytes_cfg) / P)
+                                         : sub_pages;
             uint64_t slot_base = 0, pres_base = present_base;
-            for (uint64_t p0 = 0; p0 < npg; p0 += sub_pages) {
-                const uint32_t n = (uint32_t)std::min(sub_pages, npg - p0);
+            for (uint64_t p0 = 0, step = ramp_pages; p0 < npg; p0 += step, step = std::min(2 * step, sub_pages)) {
+                const uint32_t n = (uint32_t)std::min(step, npg - p0);
                 cudaEvent_t ca = c->ev(), kb = c->ev(), kc = c->ev();
                 CUDA_TRY(c, cudaEventRecord(ca, c->packs));
                 LAUNCH_TRY(c, launch_codec_plan(c->allocs_d, c->page_alloc, c->cls, ch.page_begin + p0, n, P, c->lg,
@@ -1602,6 +1610,26 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         if (!chain[k] || chain[k]->ctx != c) return fail(c, GCR_E_INVAL, "restore: image of another ctx or NULL");
     auto t0 = Clock::now();
     gcr_stats &st = c->stats;
+    // Speculative first H2D (f4 chains): the first staged group of a coded
+    // image is its data prefix [0, <= group_max) and lands in region 0 of the
+    // staging slots -- not in registered memory -- so it is issued before the
+    // host validates and plans (~0.5 ms on C2) and used if the plan agrees.
+    // Every failure path below syncs the streams before returning (gcr_restore).
+    const uint64_t group_max = c->slots.empty() ? 0 : std::min<uint64_t>(c->cfg.chunk_bytes, kGroupMax);
+    uint64_t spec_bytes = 0;
+    cudaEvent_t spec_landed = nullptr;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    {  // before the speculative H2D: a whole-device fence would wait for it
+        const gcr_status fs = fence_caller_work(c);
+        if (fs != GCR_OK) return fs;
+    }
+    if (group_max && (chain[0]->hdr.flags & 2u) && chain[0]->data && chain[0]->hdr.image_bytes &&
+        chain[0]->data_cap >= std::min<uint64_t>(chain[0]->hdr.image_bytes, group_max)) {
+        spec_bytes = std::min<uint64_t>(chain[0]->hdr.image_bytes, group_max);
+        CUDA_TRY(c, cudaMemcpyAsync(c->slots[0], chain[0]->data, spec_bytes, cudaMemcpyHostToDevice, c->copy[0]));
+        spec_landed = c->ev_spec;
+        CUDA_TRY(c, cudaEventRecord(spec_landed, c->copy[0]));
+    }
     // ---- validation, in order: meta CRC, version, layout, chain (c.2 step 1)
     for (uint32_t k = 0; k < n; k++) {
         const gcr_image *im = chain[k];
@@ -1626,11 +1654,6 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
             return fail(c, GCR_E_CHAIN, "restore: chain must start with a full image");
         if (k > 0 && (!(h.flags & 1u) || h.parent_generation != chain[k - 1]->hdr.generation))
             return fail(c, GCR_E_CHAIN, "restore: parent_generation link broken");
-    }
-    CUDA_TRY(c, cudaSetDevice(c->device));
-    {
-        const gcr_status fs = fence_caller_work(c);
-        if (fs != GCR_OK) return fs;
     }
     st.remap_ns = 0;
     writes_began = true;  // from here on a failure leaves the memory content undefined
@@ -1673,7 +1696,6 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     // staged groups (one H2D into a slot + scatter / decode) of at most
     // kGroupMax: the first kernel starts after 64 MiB instead of a whole slot,
     // and the last group's kernel -- the restore's tail -- is short
-    const uint64_t group_max = std::min<uint64_t>(slot, kGroupMax);
     std::vector<ImgPlan> plans(n);
     std::vector<ScatterDesc> sdesc;
     std::vector<ZeroDesc> zdesc;
@@ -1788,7 +1810,32 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     CUDA_TRY(c, cudaMemcpyAsync(c->desc_d, c->desc_h, dbytes + sbytes + zbytes, cudaMemcpyHostToDevice, c->compute));
 
     // ---- apply the chain ----------------------------------------------------
+    // Staged groups land in a ring of group_max-sized REGIONS carved out of the
+    // staging slots (2 x 1 GiB = 32 regions of 64 MiB by default).  The H2Ds
+    // alternate over the copy streams; every scatter / decode runs on the packs
+    // stream once its group's H2D is done, and the H2D into a region waits only
+    // for the kernel that last read that region.  (Group j's H2D used to follow
+    // group j - S's kernel on the same copy stream: the link idled for one
+    // decode every S groups, ~0.9 ms of a C2 f4 restore.)  A ZERO fill goes to
+    // the packs stream at the image's start, beside the first H2D.
     std::vector<cudaEvent_t> sc0, sc1, dc0, dc1;  // scatter+zero / f4 decode spans
+    const uint64_t regions_per_slot = std::max<uint64_t>(1, slot / group_max);
+    const uint64_t NR = regions_per_slot * c->slots.size();
+    std::vector<cudaEvent_t> region_free(NR, nullptr);  // kernel that last read the region
+    uint64_t q = 0;                                      // staged groups issued (all images)
+    bool spec_used = false;
+    static const bool trace = std::getenv("GCR_TRACE") != nullptr;
+    const bool ring = [] {  // read per call (tests flip it)
+        const char *e = std::getenv("GCR_RESTORE_RING");
+        return !(e && e[0] == '0');
+    }();
+    struct TraceGroup {  // GCR_TRACE: per staged group
+        cudaEvent_t issued, landed, k0, k1;
+        uint64_t bytes;
+    };
+    std::vector<TraceGroup> tg;
+    cudaEvent_t rt0 = c->ev();
+    CUDA_TRY(c, cudaEventRecord(rt0, c->compute));
     auto h2d0 = Clock::now();
     for (uint32_t k = 0; k < n; k++) {
         const gcr_image *im = chain[k];
@@ -1796,6 +1843,15 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
         cudaEvent_t start = c->ev();
         CUDA_TRY(c, cudaEventRecord(start, c->compute));
         for (size_t i = 0; i < S; i++) CUDA_TRY(c, cudaStreamWaitEvent(c->copy[i], start, 0));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->packs, start, 0));
+        if (pl.z_end > pl.z_begin) {  // disjoint from this image's PRESENT pages: beside its H2Ds
+            cudaEvent_t a = c->ev(), b = c->ev();
+            CUDA_TRY(c, cudaEventRecord(a, c->packs));
+            LAUNCH_TRY(c, launch_zero_fill(zd + pl.z_begin, pl.z_end - pl.z_begin, c->n_sms, c->packs));
+            CUDA_TRY(c, cudaEventRecord(b, c->packs));
+            sc0.push_back(a);
+            sc1.push_back(b);
+        }
         for (size_t j = 0; j < pl.items.size(); j++) {
             const Item &it = pl.items[j];
             cudaStream_t cs = c->copy[j % S];
@@ -1804,28 +1860,47 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                                             cudaMemcpyHostToDevice, cs));
                 continue;
             }
-            CUDA_TRY(c, cudaMemcpyAsync(c->slots[j % S], im->data + it.img_off, it.bytes, cudaMemcpyHostToDevice, cs));
-            cudaEvent_t a = c->ev(), b = c->ev();
-            CUDA_TRY(c, cudaEventRecord(a, cs));
+            // GCR_RESTORE_RING=0 (A/B knob): round 2's first layout -- group j in
+            // slot j mod S, its kernel on its own copy stream
+            const uint64_t r = ring ? q++ % NR : j % S;
+            uint8_t *reg = ring ? c->slots[r / regions_per_slot] + (r % regions_per_slot) * group_max : c->slots[j % S];
+            cudaStream_t ks = ring ? c->packs : cs;
+            if (ring && region_free[r]) CUDA_TRY(c, cudaStreamWaitEvent(cs, region_free[r], 0));
+            cudaEvent_t issued = nullptr;
+            if (trace) {
+                issued = c->ev();
+                CUDA_TRY(c, cudaEventRecord(issued, cs));
+            }
+            cudaEvent_t landed, a = c->ev(), b = c->ev();
+            if (k == 0 && it.img_off == 0 && it.bytes <= spec_bytes && reg == c->slots[0]) {
+                landed = spec_landed;  // the speculative prefix H2D already brought this group
+                spec_used = true;
+                if (!ring) CUDA_TRY(c, cudaStreamWaitEvent(ks, landed, 0));
+            } else {
+                CUDA_TRY(c, cudaMemcpyAsync(reg, im->data + it.img_off, it.bytes, cudaMemcpyHostToDevice, cs));
+                landed = c->ev();
+                CUDA_TRY(c, cudaEventRecord(landed, cs));
+            }
+            if (trace) tg.push_back(TraceGroup{issued, landed, a, b, it.bytes});
+            if (ring) CUDA_TRY(c, cudaStreamWaitEvent(ks, landed, 0));
+            CUDA_TRY(c, cudaEventRecord(a, ks));
             if (it.decode)
-                LAUNCH_TRY(c, launch_codec_decode(dd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], P, c->n_sms, cs));
+                LAUNCH_TRY(c, launch_codec_decode(dd + it.d_begin, it.d_end - it.d_begin, reg, P, c->n_sms, ks));
             else
-                LAUNCH_TRY(c, launch_scatter(sd + it.d_begin, it.d_end - it.d_begin, c->slots[j % S], c->n_sms, cs));
-            CUDA_TRY(c, cudaEventRecord(b, cs));
+                LAUNCH_TRY(c, launch_scatter(sd + it.d_begin, it.d_end - it.d_begin, reg, c->n_sms, ks));
+            CUDA_TRY(c, cudaEventRecord(b, ks));
+            region_free[r] = b;
             (it.decode ? dc0 : sc0).push_back(a);
             (it.decode ? dc1 : sc1).push_back(b);
-        }
-        if (pl.z_end > pl.z_begin) {
-            cudaEvent_t a = c->ev(), b = c->ev();
-            CUDA_TRY(c, cudaEventRecord(a, c->copy[0]));
-            LAUNCH_TRY(c, launch_zero_fill(zd + pl.z_begin, pl.z_end - pl.z_begin, c->n_sms, c->copy[0]));
-            CUDA_TRY(c, cudaEventRecord(b, c->copy[0]));
-            sc0.push_back(a);
-            sc1.push_back(b);
         }
         for (size_t i = 0; i < S; i++) {
             cudaEvent_t e = c->ev();
             CUDA_TRY(c, cudaEventRecord(e, c->copy[i]));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
+        }
+        {
+            cudaEvent_t e = c->ev();
+            CUDA_TRY(c, cudaEventRecord(e, c->packs));
             CUDA_TRY(c, cudaStreamWaitEvent(c->compute, e, 0));
         }
     }
@@ -1927,6 +2002,20 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
     CUDA_TRY(c, cudaStreamSynchronize(c->compute));
     st.restore_h2d_ns = ns_since(h2d0);
     float ms;
+    if (trace) {  // GCR_TRACE=1: per-group restore timeline (ms from the first H2D's enqueue point) on stderr
+        auto rel = [&](cudaEvent_t e) {
+            float m = 0;
+            cudaEventElapsedTime(&m, rt0, e);
+            return m;
+        };
+        std::fprintf(stderr, "{\"gcr_trace\": \"restore\", \"groups\": [");
+        for (size_t g = 0; g < tg.size(); g++)
+            std::fprintf(stderr, "%s[%.3f, %.3f, %.3f, %.3f, %llu]", g ? ", " : "", rel(tg[g].issued), rel(tg[g].landed),
+                         rel(tg[g].k0), rel(tg[g].k1), (unsigned long long)tg[g].bytes);
+        std::fprintf(stderr, "], \"verify\": [%.3f, %.3f], \"host_ms\": %.3f, \"speculative_prefix\": %d, \"fields\": {\"groups\": \"h2d_enqueued "
+                             "h2d_landed kernel_start kernel_end bytes\"}}\n",
+                     c->cfg.verify ? rel(v0) : 0.f, c->cfg.verify ? rel(v1) : 0.f, ns_since(h2d0) * 1e-6, (int)spec_used);
+    }
     st.scatter_dev_ns = 0;
     for (size_t i = 0; i < sc0.size(); i++) {
         CUDA_TRY(c, cudaEventElapsedTime(&ms, sc0[i], sc1[i]));
@@ -1966,6 +2055,7 @@ gcr_status gcr_restore(gcr_ctx *c, gcr_image *const *chain, uint32_t n) {
     const gcr_phase ph0 = c->phase;
     bool writes_began = false;
     const gcr_status s = restore_impl(c, chain, n, writes_began);
+    if (s != GCR_OK) sync_all(c);  // nothing of this call (e.g. the speculative H2D) outlives it
     if (s != GCR_OK && writes_began) {
         // memory content undefined: no incremental may diff against it, and
         // memory re-backed after a release stays RELEASED (unlock refused)

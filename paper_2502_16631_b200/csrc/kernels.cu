@@ -1383,6 +1383,259 @@ __global__ void __launch_bounds__(128) k_zero_fill(const ZeroDesc *desc, uint64_
     bulk_wait_all();
 }
 
+// ---- TMA bulk-copy ring (K4 pack and K6 scatter) ---------------------------
+// One issuing lane per warp streams (src, dst, len <= kTStg) pieces through a
+// ring of kTStages shared-memory stages: cp.async.bulk global -> shared
+// (mbarrier complete_tx), then cp.async.bulk shared -> global (bulk_group).
+// A stage is reloaded only once the store that read it has finished reading
+// (cp.async.bulk.wait_group.read): at most kTStages - 1 loads and the stores
+// behind them in flight per warp.  3 warps x 4 x 16 KiB = 192 KiB per CTA,
+// one CTA per SM.  Measured on 64 KiB pieces (tools/tma_copy, r2v): 6.10-6.17
+// TB/s of copy (read + write) against 5.88-5.98 for the 16-B vector copy and
+// 6.62 for a contiguous cudaMemcpyAsync D2D.
+constexpr uint32_t kTStg = 16384, kTStages = 4, kTWarps = 3;
+constexpr uint32_t kTSmem = kTWarps * kTStages * kTStg + kTWarps * kTStages * 8 + kTWarps * kTStages * 16 +
+                            kTWarps * 32 * 24;
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MW_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra MW_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *sdst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+struct TRing {  // lane 0 of a warp only
+    uint8_t *buf;
+    uint64_t *bar;
+    unsigned long long *sdst;  // per stage: destination of the loaded piece
+    uint32_t *slen;            // per stage: its length
+    uint32_t nload, nstore;
+
+    __device__ __forceinline__ void init(uint8_t *b, uint64_t *br, unsigned long long *sd, uint32_t *sl) {
+        buf = b;
+        bar = br;
+        sdst = sd;
+        slen = sl;
+        nload = nstore = 0;
+        for (uint32_t s = 0; s < kTStages; s++) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __device__ __forceinline__ void pop() {  // oldest loaded piece -> its destination
+        const uint32_t s = nstore % kTStages;
+        mbar_wait(&bar[s], (nstore / kTStages) & 1u);
+        bulk_store(reinterpret_cast<void *>(sdst[s]), buf + s * kTStg, slen[s]);
+        bulk_commit();
+        nstore++;
+    }
+    __device__ __forceinline__ void push(const uint8_t *src, uint8_t *dst, uint32_t len) {
+        while (nload - nstore >= kTStages - 1) pop();
+        const uint32_t s = nload % kTStages;
+        // the last store out of stage s is store nload - kTStages; >= 1 store was
+        // committed after it (nstore >= nload - kTStages + 2), so read<1> covers it
+        if (nload >= kTStages) bulk_wait_read<1>();
+        sdst[s] = reinterpret_cast<unsigned long long>(dst);
+        slen[s] = len;
+        mbar_expect_tx(&bar[s], len);
+        bulk_load(buf + s * kTStg, src, len, &bar[s]);
+        nload++;
+    }
+    __device__ __forceinline__ void push_run(const uint8_t *src, uint8_t *dst, uint64_t len) {
+        for (uint64_t o = 0; o < len; o += kTStg) push(src + o, dst + o, (uint32_t)(len - o < kTStg ? len - o : (uint64_t)kTStg));
+    }
+    __device__ __forceinline__ void drain() {
+        while (nstore < nload) pop();
+        bulk_wait_all();  // every store performed before the kernel ends (the D2H / verify read them next)
+    }
+};
+
+// Per-warp pieces of the CTA's shared memory: stages, barriers, stage metadata, item table.
+struct TWarpSmem {
+    uint8_t *buf;
+    uint64_t *bar;
+    unsigned long long *sdst;
+    uint32_t *slen;
+    unsigned long long *item;  // 32 x 3 u64 per warp
+};
+__device__ __forceinline__ TWarpSmem twarp_smem(uint8_t *sm, uint32_t w) {
+    TWarpSmem t;
+    t.buf = sm + (size_t)w * kTStages * kTStg;
+    uint8_t *p = sm + (size_t)kTWarps * kTStages * kTStg;
+    t.bar = reinterpret_cast<uint64_t *>(p) + w * kTStages;
+    p += kTWarps * kTStages * 8;
+    t.sdst = reinterpret_cast<unsigned long long *>(p) + w * kTStages;
+    p += kTWarps * kTStages * 8;
+    t.slen = reinterpret_cast<uint32_t *>(p) + w * kTStages * 2;
+    p += kTWarps * kTStages * 8;
+    t.item = reinterpret_cast<unsigned long long *>(p) + w * 32 * 3;
+    return t;
+}
+
+// K4 (TMA): the same items and image layout as k_pack.  Each lane of a
+// working warp describes one item (interleaved over the warps) as
+// (source base, destination base, PRESENT-unit mask | unit size | short last
+// unit) in shared memory, then lane 0 streams the PRESENT units of the
+// warp's 32 items -- maximal runs of consecutive units, each run contiguous in
+// the allocation and at its image offset in the slot -- through the TMA ring.
+// A unit is a page (P <= 64 KiB) or the item's 64 KiB slice of a page (P > 64
+// KiB).  (A first version gave each warp 32 CONSECUTIVE items: a 1 %-dirty
+// chunk's ~160 items then ran on 6 warps, 56 GB/s; r2x.)
+__global__ void __launch_bounds__(kTWarps * 32, 1) k_pack_tma(const AllocDev *allocs, const uint32_t *tile_alloc,
+                                                             const uint8_t *cls, uint64_t tb, uint32_t P, uint32_t lg,
+                                                             uint8_t *slot, const StageItem *items, uint32_t n_items,
+                                                             const uint32_t *scan_done, uint32_t epoch,
+                                                             uint32_t *decision, uint32_t pack_ctas) {
+    extern __shared__ __align__(128) uint8_t tsm[];
+    __shared__ uint32_t s_wide;
+    if (threadIdx.x == 0) {  // the launch's one width decision, as in k_pack
+        uint32_t wd = 1u;
+        if (scan_done != nullptr) {
+            const uint32_t tag = (epoch & 0x7FFFFFFFu) << 1;
+            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(decision);
+            if ((cur & ~1u) == tag) {
+                wd = cur & 1u;
+            } else {
+                const uint32_t mine = *reinterpret_cast<const volatile uint32_t *>(scan_done) == epoch ? 1u : 0u;
+                const uint32_t prev = atomicCAS(decision, cur, tag | mine);
+                wd = prev == cur ? mine : (prev & 1u);
+            }
+        }
+        s_wide = wd;
+    }
+    __syncthreads();
+    const uint32_t G = s_wide ? gridDim.x : min(gridDim.x, pack_ctas);
+    if (blockIdx.x >= G) return;
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const TWarpSmem ws = twarp_smem(tsm, w);
+    TRing ring;
+    if (lane == 0) ring.init(ws.buf, ws.bar, ws.sdst, ws.slen);
+    const uint64_t W = (uint64_t)G * kTWarps, me = (uint64_t)blockIdx.x * kTWarps + w;
+    // lane i of warp me takes item (k * 32 + i) * W + me: a chunk's few items
+    // (1 % dirty: ~160) still spread over every working warp
+    for (uint64_t k = 0; me + k * 32 * W < n_items; k++) {
+        const uint64_t i = (k * 32 + lane) * W + me;
+        // desc: PRESENT-unit mask (bits 0-15) | log2 unit (16-23) | index of a short
+        // last unit (24-31, 0xFF: none) | its length (32-63)
+        unsigned long long src = 0, dst = 0, desc = 0xFFull << 24;
+        if (i < n_items) {
+            const uint2 v = __ldcv(reinterpret_cast<const uint2 *>(items + i));  // host-written: never cached
+            const uint64_t t = tb + v.x;
+            const AllocDev *al = allocs + __ldg(tile_alloc + t);
+            const uint64_t base = __ldg(&al->base), page0 = __ldg(&al->page0), lt = t - __ldg(&al->tile0);
+            const uint32_t n_pages = __ldg(&al->n_pages), tail_len = __ldg(&al->tail_len);
+            dst = reinterpret_cast<unsigned long long>(slot) + v.y;
+            if (P <= kTileBytes) {
+                const uint32_t ppt = kTileBytes >> lg;
+                const uint64_t pi0 = lt * ppt;
+                uint32_t mask = 0;
+                for (uint32_t j = 0; j < ppt && pi0 + j < n_pages; j++)
+                    if ((cls[page0 + pi0 + j] & 3u) == kClsPresent) mask |= 1u << j;
+                src = base + (lt << kLog2Tile);
+                desc = mask | (unsigned long long)lg << 16;
+                if (pi0 + ppt >= n_pages)  // the tile holds the allocation's last page
+                    desc |= (unsigned long long)(n_pages - 1 - pi0) << 24 | (unsigned long long)tail_len << 32;
+                else
+                    desc |= 0xFFull << 24;
+            } else {
+                const uint32_t tpp = P >> kLog2Tile;
+                const uint64_t pi = lt / tpp;
+                const uint32_t s = (uint32_t)(lt % tpp);
+                const uint32_t len = pi == (uint64_t)n_pages - 1 ? tail_len : P;
+                const bool present = (cls[page0 + pi] & 3u) == kClsPresent && s * kTileBytes < len;
+                src = base + (pi << lg) + (uint64_t)s * kTileBytes;
+                desc = (present ? 1ull : 0ull) | (unsigned long long)kLog2Tile << 16 |
+                       (unsigned long long)(present ? min(len - s * kTileBytes, kTileBytes) : 0u) << 32;
+            }
+        }
+        ws.item[lane * 3] = src;
+        ws.item[lane * 3 + 1] = dst;
+        ws.item[lane * 3 + 2] = desc;
+        __syncwarp();
+        if (lane == 0) {
+            for (uint32_t q = 0; q < 32; q++) {
+                const uint64_t s0 = ws.item[q * 3], d = ws.item[q * 3 + 2];
+                uint8_t *dp = reinterpret_cast<uint8_t *>(ws.item[q * 3 + 1]);
+                uint32_t mask = (uint32_t)d & 0xFFFFu;
+                const uint32_t ulg = (uint32_t)(d >> 16) & 0xFFu, jt = (uint32_t)(d >> 24) & 0xFFu;
+                const uint32_t short_len = (uint32_t)(d >> 32);
+                while (mask) {  // maximal runs of consecutive PRESENT units: contiguous in memory and in the image
+                    const uint32_t j = __ffs(mask) - 1u;
+                    const uint32_t r = __ffs(~(mask >> j)) - 1u;  // mask < 2^16: a zero bit above the run
+                    uint64_t len = (uint64_t)r << ulg;
+                    if (jt == j + r - 1u) len -= (1ull << ulg) - short_len;  // ends on the short last unit
+                    ring.push_run(reinterpret_cast<const uint8_t *>(s0 + ((uint64_t)j << ulg)), dp, len);
+                    dp += len;
+                    mask &= ~(((1u << r) - 1u) << j);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) ring.drain();
+}
+
+// K6 (TMA): staged image pieces -> allocation pages.  Piece u of the launch is
+// the kTStg-sized piece u mod M of descriptor u / M (M = kScatterDescMax /
+// kTStg; pieces past a short descriptor's end are empty).  Lane i of warp me
+// describes pieces (k * 32 + i) * W + me (W warps in the grid), so adjacent
+// warps take adjacent pieces and a 64 MiB group spreads over every SM; lane 0
+// streams the non-empty ones through the TMA ring.
+constexpr uint64_t kTPiecesPerDesc = kScatterDescMax / kTStg;
+
+__global__ void __launch_bounds__(kTWarps * 32, 1) k_scatter_tma(const ScatterDesc *desc, uint64_t n,
+                                                                const uint8_t *slot) {
+    extern __shared__ __align__(128) uint8_t tsm[];
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const TWarpSmem ws = twarp_smem(tsm, w);
+    TRing ring;
+    if (lane == 0) ring.init(ws.buf, ws.bar, ws.sdst, ws.slen);
+    const uint64_t W = (uint64_t)gridDim.x * kTWarps, me = (uint64_t)blockIdx.x * kTWarps + w;
+    const uint64_t total = n * kTPiecesPerDesc;
+    for (uint64_t k = 0; me + k * 32 * W < total; k++) {
+        const uint64_t u = (k * 32 + lane) * W + me;
+        unsigned long long src = 0, dst = 0, len = 0;
+        if (u < total) {
+            const ScatterDesc *dd = desc + u / kTPiecesPerDesc;
+            const uint64_t p0 = (u % kTPiecesPerDesc) * kTStg, by = __ldg(&dd->bytes);
+            if (p0 < by) {
+                src = reinterpret_cast<unsigned long long>(slot) + __ldg(&dd->src_off) + p0;
+                dst = __ldg(&dd->dst) + p0;
+                len = by - p0 < kTStg ? by - p0 : (uint64_t)kTStg;
+            }
+        }
+        ws.item[lane * 3] = src;
+        ws.item[lane * 3 + 1] = dst;
+        ws.item[lane * 3 + 2] = len;
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t j = 0; j < 32; j++)
+                if (ws.item[j * 3 + 2])
+                    ring.push(reinterpret_cast<const uint8_t *>(ws.item[j * 3]),
+                              reinterpret_cast<uint8_t *>(ws.item[j * 3 + 1]), (uint32_t)ws.item[j * 3 + 2]);
+        __syncwarp();
+    }
+    if (lane == 0) ring.drain();
+}
+
 }  // namespace
 
 size_t scan_smem_bytes() { return kScanSmem; }
@@ -1439,6 +1692,26 @@ uint32_t scan_prefetch_bytes() {
         return e ? (uint32_t)std::strtoul(e, nullptr, 0) & ~15u : kScanPrefetchDefault;
     }();
     return v;
+}
+
+// K4 / K6 through the TMA ring unless GCR_TMA_COPY=0 (the 16-B vector copies:
+// same-box A/B knob)
+static bool tma_copies() {
+    const char *e = std::getenv("GCR_TMA_COPY");  // read per launch (tests flip it)
+    return !(e && e[0] == '0');
+}
+
+// the ring kernels' shared-memory opt-in, once per device and kernel (setting
+// an attribute can serialise with work in flight)
+static bool tma_attr(const void *fn) {
+    static bool done[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int k = fn == reinterpret_cast<const void *>(k_pack_tma) ? 0 : 1;
+    if (dev < 64 && done[dev][k]) return true;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTSmem) != cudaSuccess) return false;
+    if (dev < 64) done[dev][k] = true;
+    return true;
 }
 
 // K1g for 4 KiB / 8 KiB pages unless GCR_SMALL_GROUPS=0
@@ -1501,6 +1774,15 @@ int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_
     if (grid > cap) grid = cap;
     // narrow while the scan runs only if it left room for K2 + >= 1 pack CTA
     if (scan_free < 3 || n_sms <= 4 * scan_free) scan_done = nullptr;
+    if (tma_copies()) {  // one 192 KiB CTA per SM, 3 issuing warps
+        if (!tma_attr(reinterpret_cast<const void *>(k_pack_tma))) return -1;
+        uint64_t g = ((uint64_t)n_items + kTWarps - 1) / kTWarps;
+        if (g > (uint64_t)n_sms) g = (uint64_t)n_sms;
+        if (scan_done != nullptr && g < (uint64_t)(scan_free - 2)) g = (uint64_t)(scan_free - 2);
+        k_pack_tma<<<(unsigned)g, kTWarps * 32, kTSmem, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items,
+                                                              scan_done, epoch, decision, (uint32_t)(scan_free - 2));
+        return launched(1);
+    }
     k_pack<<<(unsigned)grid, kPackThreads, 0, st>>>(allocs, tile_alloc, cls, tb, P, lg, slot, items, n_items,
                                                     scan_done, epoch, decision, (uint32_t)(scan_free - 2));
     return launched(1);
@@ -1529,6 +1811,14 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
+    if (tma_copies()) {
+        if (!tma_attr(reinterpret_cast<const void *>(k_scatter_tma))) return -1;
+        const uint64_t pieces = n * kTPiecesPerDesc;
+        uint64_t g = (pieces + kTWarps - 1) / kTWarps;
+        if (g > (uint64_t)n_sms) g = (uint64_t)n_sms;
+        k_scatter_tma<<<(unsigned)g, kTWarps * 32, kTSmem, st>>>(desc, n, slot);
+        return launched(1);
+    }
     const uint64_t pieces = n * kPiecesPerDesc, cap = (uint64_t)n_sms * 8;
     k_scatter<<<(unsigned)(pieces < cap ? pieces : cap), 256, 0, st>>>(desc, n, slot);
     return launched(1);

@@ -254,3 +254,57 @@ def test_codec_sub_chunks_in_a_subprocess(G):
                         os.path.abspath(__file__) + "::test_compressed_incremental_chain"],
                        capture_output=True, text=True, env=env, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("compress,chunk,ring", [(1, 2 << 20, "1"), (0, 2 << 20, "1"), (1, 128 << 20, "1"),
+                                                (0, 128 << 20, "1"), (1, 2 << 20, "0")])
+def test_restore_region_ring_reuse(G, compress, chunk, ring, monkeypatch):
+    """The restore lands staged groups in a ring of regions carved out of the
+    staging slots (group_max bytes each; 2 MiB chunks: 2 regions, 128 MiB
+    chunks: 2 x 2 regions of 64 MiB) and runs every scatter / decode on one
+    kernel stream: with ~40 groups each region is reused many times, so an H2D
+    that did not wait for the previous reader of its region would corrupt
+    pages.  Restore into poison reproduces every byte, verify included, and a
+    chain (full + incremental) restores too.  ring "0": the GCR_RESTORE_RING=0
+    A/B layout (slot per copy stream, kernel on the copy stream)."""
+    gcr, synth = G
+    monkeypatch.setenv("GCR_RESTORE_RING", ring)
+    P = 65536
+    kinds = [synth.F32_WEIGHT, synth.F32_M, synth.RANDOM, synth.F32_V, synth.BF16_WEIGHT]
+    ts = []
+    for i, kind in enumerate(kinds):
+        n = (16 << 20) + i * 3 * P + 48 * i
+        t = torch.empty(n, dtype=torch.uint8, device="cuda")
+        synth.gpu_fill(t.data_ptr(), n, 31, i, kind, synth.ONE_F32)
+        ts.append(t)
+    ts[1][5 * P:9 * P].zero_()
+    torch.cuda.synchronize()
+    ctx = gcr.Context(0, page_size=P, chunk_bytes=chunk, compress=compress, direct_min_bytes=(1 << 64) - 1)
+    try:
+        for t in ts:
+            ctx.register_tensor(t)
+        cont = host_copies(ts)
+        ctx.lock()
+        full = ctx.checkpoint()
+        ctx.unlock()
+        for t in ts:  # dirty every 3rd page
+            t.view(-1)[: (t.numel() // P) * P].view(-1, P)[::3, :64].add_(1)
+        torch.cuda.synchronize()
+        cont2 = host_copies(ts)
+        ctx.lock()
+        inc = ctx.checkpoint(gcr.GCR_INCREMENTAL)
+        for t in ts:
+            t.fill_(0xA5)
+        ctx.restore([full])
+        assert ctx.stats()["verify_failures"] == 0
+        for t, c in zip(ts, cont):
+            assert np.array_equal(t.cpu().numpy(), c)
+        for t in ts:
+            t.fill_(0x5A)
+        ctx.restore([full, inc])
+        assert ctx.stats()["verify_failures"] == 0
+        for t, c in zip(ts, cont2):
+            assert np.array_equal(t.cpu().numpy(), c)
+        ctx.unlock()
+    finally:
+        ctx.close()

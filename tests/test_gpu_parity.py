@@ -144,6 +144,17 @@ def test_page_sizes_tails_and_zero_pages(G, orc, P, direct_min):
     _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, seed=P + 1, direct_min=direct_min)
 
 
+@pytest.mark.parametrize("P", [4096, 65536, 262144])
+def test_vector_copy_kernels(G, orc, P, monkeypatch):
+    """K4 / K6 default to the TMA bulk-copy ring; GCR_TMA_COPY=0 selects the
+    16-byte vector copies (the A/B knob): every byte still the oracle's."""
+    monkeypatch.setenv("GCR_TMA_COPY", "0")
+    rng = np.random.default_rng(P + 7)
+    sizes = [int(rng.integers(3, 30)) * P + 4096, 5 * P, 2 * P + 48, 16]
+    zp = [(0, 1), (1, 2), (1, 3)]
+    _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, seed=P + 9, direct_min=ALWAYS_STAGED)
+
+
 @pytest.mark.parametrize("direct_min", [0, ALWAYS_STAGED, 256 << 10])
 @pytest.mark.parametrize("chunk,streams", [(65536, 1), (131072, 3), (1 << 20, 2), (4 << 20, 8)])
 def test_chunking_and_copy_streams(G, orc, chunk, streams, direct_min):
