@@ -1694,11 +1694,17 @@ uint32_t scan_prefetch_bytes() {
     return v;
 }
 
-// K4 / K6 through the TMA ring unless GCR_TMA_COPY=0 (the 16-B vector copies:
-// same-box A/B knob)
-static bool tma_copies() {
-    const char *e = std::getenv("GCR_TMA_COPY");  // read per launch (tests flip it)
-    return !(e && e[0] == '0');
+// GCR_TMA_COPY (read per launch; tests flip it): unset / 1 = K6 scatter
+// through the TMA ring, K4 pack as the 16-B vector copy (default); 2 = both
+// through the TMA ring; 0 = both vector copies.  K4 stays a vector copy by
+// default: on C4 1 % the TMA pack made the step 0.1-0.4 ms SLOWER (same box,
+// alternating, r2x / r2y: 9.39-9.76 vs 9.28-9.37 ms, drain 47.7-49.7 vs
+// 49.8-50.2 GB/s) and its wide launch measured 387 vs 361 us per 1 GiB
+// fully staged chunk in ncu; the TMA scatter is 3-4 % faster than the vector
+// one (1.13-1.14 vs 1.17 ms per all-staged C2 restore).
+static int tma_mode() {
+    const char *e = std::getenv("GCR_TMA_COPY");
+    return e ? std::atoi(e) : 1;
 }
 
 // the ring kernels' shared-memory opt-in, once per device and kernel (setting
@@ -1774,7 +1780,7 @@ int launch_pack(const AllocDev *allocs, const uint32_t *tile_alloc, const uint8_
     if (grid > cap) grid = cap;
     // narrow while the scan runs only if it left room for K2 + >= 1 pack CTA
     if (scan_free < 3 || n_sms <= 4 * scan_free) scan_done = nullptr;
-    if (tma_copies()) {  // one 192 KiB CTA per SM, 3 issuing warps
+    if (tma_mode() >= 2) {  // one 192 KiB CTA per SM, 3 issuing warps
         if (!tma_attr(reinterpret_cast<const void *>(k_pack_tma))) return -1;
         uint64_t g = ((uint64_t)n_items + kTWarps - 1) / kTWarps;
         if (g > (uint64_t)n_sms) g = (uint64_t)n_sms;
@@ -1811,7 +1817,7 @@ int launch_pagemap_write(const AllocDev *allocs, const uint32_t *page_alloc, con
 
 int launch_scatter(const ScatterDesc *desc, uint64_t n, const uint8_t *slot, int n_sms, cudaStream_t st) {
     if (n == 0) return 0;
-    if (tma_copies()) {
+    if (tma_mode() >= 1) {
         if (!tma_attr(reinterpret_cast<const void *>(k_scatter_tma))) return -1;
         const uint64_t pieces = n * kTPiecesPerDesc;
         uint64_t g = (pieces + kTWarps - 1) / kTWarps;

@@ -144,11 +144,13 @@ def test_page_sizes_tails_and_zero_pages(G, orc, P, direct_min):
     _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, seed=P + 1, direct_min=direct_min)
 
 
+@pytest.mark.parametrize("mode", ["0", "2"])
 @pytest.mark.parametrize("P", [4096, 65536, 262144])
-def test_vector_copy_kernels(G, orc, P, monkeypatch):
-    """K4 / K6 default to the TMA bulk-copy ring; GCR_TMA_COPY=0 selects the
-    16-byte vector copies (the A/B knob): every byte still the oracle's."""
-    monkeypatch.setenv("GCR_TMA_COPY", "0")
+def test_copy_kernel_variants(G, orc, P, mode, monkeypatch):
+    """Default: K6 through the TMA bulk-copy ring, K4 as the vector copy.
+    GCR_TMA_COPY=0: both vector copies; =2: both through the TMA ring (the
+    A/B knob).  Everything staged: every byte still the oracle's."""
+    monkeypatch.setenv("GCR_TMA_COPY", mode)
     rng = np.random.default_rng(P + 7)
     sizes = [int(rng.integers(3, 30)) * P + 4096, 5 * P, 2 * P + 48, 16]
     zp = [(0, 1), (1, 2), (1, 3)]
