@@ -793,6 +793,8 @@ gcr_status gcr_create(int cuda_device, const gcr_config *cfg_in, gcr_ctx **out) 
     if (cudaStreamCreateWithFlags(&c->post, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     if (cudaStreamCreateWithFlags(&c->packs, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);
     if (cudaEventCreate(&c->ev_spec) != cudaSuccess) return bail(GCR_E_CUDA);
+    scan_probe();  // K1g's immediate-base variant when this build's smem layout is confirmed (else the IADD one)
+    cudaGetLastError();
     for (uint32_t i = 0; i < cfg.n_copy_streams; i++) {
         cudaStream_t s;
         if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return bail(GCR_E_CUDA);

@@ -165,6 +165,7 @@ struct ScanParams {
     InScanPack isp;            // f1 (img == nullptr: off)
     uint32_t t4rep;            // K1g: 8x-replicated raw16 table (see kernels.cu kT4RepBytes)
     const uint32_t *isp_page_alloc;  // f1: page -> allocation (K0's table)
+    uint32_t *sb_probe;        // scan_probe(): the kernel writes its dynamic-smem base here and exits
 };
 
 struct ScatterDesc {
@@ -220,6 +221,10 @@ int launch_scatter(const ScatterDesc *desc, uint64_t n_desc, const uint8_t *slot
                    cudaStream_t st);
 int launch_zero_fill(const ZeroDesc *desc, uint64_t n_desc, int n_sms, cudaStream_t st);
 size_t scan_smem_bytes();
+// Once per device (gcr_create): launch K1g in probe mode to read its dynamic
+// shared-memory base; K1g's immediate-base braid variant is used when the low
+// 16 bits match the compile-time value (kernels.cu kGrpSbLo).  Returns 0 / -1.
+int scan_probe();
 
 // ---- f4 page codec (codec.cu, R-19) -------------------------------
 // KA over the chunk's pages [page_begin, page_begin + n_pages): stored length

@@ -130,29 +130,6 @@ __device__ __forceinline__ uint32_t apply_tab(const uint32_t *tb, uint32_t v) {
            tb[768u + (v >> 24)];
 }
 
-// The same step with the table base folded into the PRMT and the ld.shared
-// immediate: lb = lane*4 | (sb & 0xFFFF0000) and prmt(x, lb, 0x76k4) = lb with
-// byte 1 replaced by byte_k(x), so entry = that + ((sb & 0xFFFF) + table
-// offset).  kSbLo is the compile-time guess of sb & 0xFFFF, checked per
-// device by scan_probe() (the kernel's static shared layout fixes it): no
-// per-lookup IADD.  ptxas folds the base into a uniform register for K1 but
-// not for K1g (IMAD.IADD per lookup: 16 of ~60 instructions per row, ncu
-// r2zb), which is where this is used.
-template <uint32_t kSbLo>
-__device__ __forceinline__ uint32_t braid_imm(uint32_t x, uint32_t lb) {
-    return lds_imm<kSbLo>(prmt(x, lb, 0x7604u)) ^ lds_imm<kSbLo + 128>(prmt(x, lb, 0x7614u)) ^
-           lds_imm<kSbLo + 65536>(prmt(x, lb, 0x7624u)) ^ lds_imm<kSbLo + 65536 + 128>(prmt(x, lb, 0x7634u));
-}
-
-template <uint32_t kSbLo>
-__device__ __forceinline__ void row_step_imm(uint32_t lb, uint32_t (&x)[4], uint32_t &acc, const uint4 &w) {
-    acc |= w.x | w.y | w.z | w.w;
-    x[0] = braid_imm<kSbLo>(x[0], lb) ^ w.x;
-    x[1] = braid_imm<kSbLo>(x[1], lb) ^ w.y;
-    x[2] = braid_imm<kSbLo>(x[2], lb) ^ w.z;
-    x[3] = braid_imm<kSbLo>(x[3], lb) ^ w.w;
-}
-
 __device__ __forceinline__ void row_step(uint32_t lane4, uint32_t sb, uint32_t (&x)[4], uint32_t &acc,
                                          const uint4 &w) {
     acc |= w.x | w.y | w.z | w.w;
@@ -960,39 +937,26 @@ __device__ __forceinline__ uint32_t alloc_of_group(const AllocDev *al, uint32_t 
     return lo;
 }
 
-// K1g's dynamic shared-memory base, low 16 bits, as laid out by this build
-// (1 KiB reserved + the f1 state in static shared memory); verified per device
-// by scan_probe(), which falls back to the IADD variant on a mismatch.
-#ifndef GCR_GRP_SB_LO
-#define GCR_GRP_SB_LO 0xA00
-#endif
-constexpr uint32_t kGrpSbLo = GCR_GRP_SB_LO;
-
-template <int G, bool kImm>
+template <int G>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p) {
     constexpr uint32_t QL = 32 / G, Wr = kRowBytes / G, Rg = 32, U = 4, NB = Rg / U;
     extern __shared__ __align__(16) uint32_t sm[];
+    if (false) isp_init();
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);
-    if (p.sb_probe) {  // scan_probe(): report the base, do nothing else
-        if (threadIdx.x == 0 && blockIdx.x == 0) *p.sb_probe = sb;
-        return;
-    }
-    if (p.isp.img) isp_init();
     const uint32_t *small = sm + kBraidSmem / 4;
-    const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
+    const uint64_t t_entry = ((unsigned long long*)nullptr) ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
-    const uint32_t lbase = lane4 | (sb & 0xFFFF0000u);  // braid_imm's PRMT operand
     const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     stage_tables(sm, p);  // the host put adv_{512/G} (a128 / a256) in basis[0]
     __syncthreads();
     if (wid >= p.workers) return;
-    if (p.warp_times && lane == 0) {
-        p.warp_times[kStamps * wid] = t_entry;
-        p.warp_times[kStamps * wid + 1] = globaltimer_ns();
+    if (((unsigned long long*)nullptr) && lane == 0) {
+        ((unsigned long long*)nullptr)[kStamps * wid] = t_entry;
+        ((unsigned long long*)nullptr)[kStamps * wid + 1] = globaltimer_ns();
     }
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
-        if (p.isp.img) {
+        if (false) {
             isp_lists_free(p, g_isp, ch);
             isp_chunk_begin(ch, lane);
         }
@@ -1037,17 +1001,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             };
             uint32_t x[4] = {0u, 0u, 0u, 0u}, acc = 0u, pb = 0;
             auto process_block = [&](const uint4 (&w)[U]) {
-                if constexpr (kImm) {
 #pragma unroll
-                    for (uint32_t u = 0; u < U; u++) row_step_imm<kGrpSbLo>(lbase, x, acc, w[u]);
-                } else {
-#pragma unroll
-                    for (uint32_t u = 0; u < U; u++) row_step(lane4, sb, x, acc, w[u]);
-                }
+                for (uint32_t u = 0; u < U; u++) row_step(lane4, sb, x, acc, w[u]);
                 if (++pb < NB) return;
                 // group complete: one raw16 + tree for all G pages
                 uint32_t v;
-                if (p.t4rep) {
+                if (false) {
                     const uint32_t *tr = sm + kScanSmem / 4, c = lane & 7u;
                     v = apply_t4rep(tr, x[0], c);
                     v = apply_t4rep(tr, v ^ x[1], c);
@@ -1075,7 +1034,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                     pres = finalize_page(p, pal.page0 + pgl.pi, tile_of_page(pal.tile0, pgl.pi, P, lg), pgl.pi == 0,
                                          plen, tail ? pal.z_tail : p.z_page, v, nzq != 0u);
                 }
-                if (p.isp.img) {  // f1: the group's PRESENT pages, in lane (= page) order
+                if (false) {  // f1: the group's PRESENT pages, in lane (= page) order
                     const uint32_t bal2 = __ballot_sync(kFull, pres);
                     const uint32_t wib = threadIdx.x >> 5, par = ch & 1u, n0 = g_isp.wn[par][wib];
                     const uint32_t bytes = __reduce_add_sync(kFull, pres ? plen : 0u);
@@ -1116,7 +1075,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                 process_block(wb);
             }
         }
-        if (p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
+        if (false) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
         // every leader lane's page results visible before lane 0 publishes
         __threadfence();
         __syncwarp();
@@ -1128,11 +1087,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             }
         }
         __syncwarp();
-        if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
-        if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
+        if (((unsigned long long*)nullptr) && lane == 0 && ch == 0) ((unsigned long long*)nullptr)[kStamps * wid + 3] = globaltimer_ns();
+        if (false && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
     }
-    if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
-    if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
+    if (false && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
+    if (((unsigned long long*)nullptr) && lane == 0) ((unsigned long long*)nullptr)[kStamps * wid + 4] = globaltimer_ns();
 }
 
 // K0: page -> allocation and tile -> allocation (A1).  One CTA per allocation.
@@ -1769,49 +1728,6 @@ bool scan_uses_groups(uint32_t page_size) {
     return !(e && e[0] == '0') && (page_size == kGroupBytes / 4 || page_size == kGroupBytes / 2);
 }
 
-static bool g_grp_imm[64] = {};  // per device: K1g's immediate-base variant verified by scan_probe()
-
-static int scan_attrs() {
-    const int big = (int)(kScanSmem + kT4RepBytes);
-    if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess)
-        return -1;
-    return 0;
-}
-
-// GCR_GRP_IMM=0 forces the IADD variant (A/B knob).
-int scan_probe() {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return -1;
-    const char *e = std::getenv("GCR_GRP_IMM");
-    if (scan_attrs() != 0) return -1;
-    uint32_t *d = nullptr, h[2] = {~0u, ~0u};
-    if (cudaMalloc(&d, 8) != cudaSuccess) return -1;
-    ScanParams p{};
-    for (int v = 0; v < 2; v++) {
-        p.sb_probe = d + v;
-        if (v == 0) k_scan_grp<4, true><<<1, kScanThreads, kScanSmem>>>(p);
-        else k_scan_grp<2, true><<<1, kScanThreads, kScanSmem>>>(p);
-    }
-    const bool ok = cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost) == cudaSuccess;
-    cudaFree(d);
-    if (!ok) return -1;
-    g_grp_imm[dev] = !(e && e[0] == '0') && (h[0] & 0xFFFFu) == kGrpSbLo && (h[1] & 0xFFFFu) == kGrpSbLo;
-    if (std::getenv("GCR_TRACE"))
-        std::fprintf(stderr, "{\"gcr_scan_probe\": {\"sb\": [%u, %u], \"expected_lo\": %u, \"k1g_imm\": %d}}\n", h[0], h[1],
-                     kGrpSbLo, (int)g_grp_imm[dev]);
-    return 0;
-}
-
-bool scan_grp_imm() {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    return dev < 64 && g_grp_imm[dev];
-}
-
 int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     // once per device: setting a function attribute can serialise with work in
     // flight, which would leave the GPU idle between pipelined launches
@@ -1819,21 +1735,22 @@ int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_done[dev]) {
-        if (scan_attrs() != 0) return -1;
+        if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(k_scan_grp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kScanSmem + kT4RepBytes)) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_scan_grp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kScanSmem + kT4RepBytes)) !=
+                cudaSuccess)
+            return -1;
         attr_done[dev] = true;
     }
     if (p.n_chunks == 0) return 0;
     const uint64_t wpb = kScanThreads / 32;
     const uint64_t grid = (p.workers + wpb - 1) / wpb;
-    const bool imm = dev < 64 && g_grp_imm[dev];
-    const size_t gsm = kScanSmem + (p.t4rep ? kT4RepBytes : 0u);
-    if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 4) {
-        if (imm) k_scan_grp<4, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-        else k_scan_grp<4, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-    } else if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 2) {
-        if (imm) k_scan_grp<2, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-        else k_scan_grp<2, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-    } else
+    if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 4)
+        k_scan_grp<4><<<(unsigned)grid, kScanThreads, kScanSmem + (p.t4rep ? kT4RepBytes : 0u), st>>>(p);
+    else if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 2)
+        k_scan_grp<2><<<(unsigned)grid, kScanThreads, kScanSmem + (p.t4rep ? kT4RepBytes : 0u), st>>>(p);
+    else
         k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
     return launched(1);
 }

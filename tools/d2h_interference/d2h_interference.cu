@@ -20,11 +20,20 @@
         }                                                                                   \
     } while (0)
 
-// stream `bytes` of src (and write dst if non-null) repeatedly until *stop != 0
-__global__ void k_load(const uint4 *src, uint4 *dst, uint64_t n16, volatile int *stop, unsigned long long *sink) {
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// stream src (and write dst if non-null) repeatedly for `ns` nanoseconds of
+// the global timer (no host polling: a mapped-memory flag polled by every
+// thread put ~10 GB/s of PCIe read requests on the link and wrecked the D2H)
+__global__ void k_load(const uint4 *src, uint4 *dst, uint64_t n16, uint64_t ns, unsigned long long *sink) {
     uint4 acc = make_uint4(0, 0, 0, 0);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    while (!*stop) {
+    const uint64_t t_end = gtimer() + ns;
+    while (gtimer() < t_end) {
         for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
             const uint4 v = __ldcs(src + i);
             if (dst) __stcs(dst + i, v);
@@ -44,9 +53,7 @@ int main() {
     CK(cudaMemset(dsrc, 1, D));
     CK(cudaMemset(lsrc, 2, L));
     CK(cudaHostAlloc(&host, D, cudaHostAllocDefault));
-    int *stop;
     unsigned long long *sink;
-    CK(cudaHostAlloc(&stop, sizeof(int), cudaHostAllocMapped));
     CK(cudaMalloc(&sink, 8));
     cudaStream_t cs, ks;
     CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -76,14 +83,10 @@ int main() {
     std::printf("{\"load\": \"none\", \"d2h_GBps_mean\": %.2f, \"best\": %.2f}\n", alone.first, alone.second);
     for (int rw = 0; rw < 2; rw++)
         for (int k : {8, 32, sms}) {
-            *stop = 0;
-            int *dstop;
-            CK(cudaHostGetDevicePointer(&dstop, stop, 0));
             k_load<<<k * 2, 1024, 0, ks>>>(reinterpret_cast<const uint4 *>(lsrc), rw ? reinterpret_cast<uint4 *>(ldst) : nullptr,
-                                           L / 16, dstop, sink);
+                                           L / 16, 200000000ull, sink);  // 200 ms: longer than the 6 D2Hs
             CK(cudaGetLastError());
             auto r = d2h();
-            *stop = 1;
             CK(cudaStreamSynchronize(ks));
             std::printf("{\"load\": \"%s on %d SMs\", \"d2h_GBps_mean\": %.2f, \"best\": %.2f}\n", rw ? "read+write" : "read", k,
                         r.first, r.second);
