@@ -419,6 +419,11 @@ def run_ours(args):
                      "what": "the same workload and launch configuration with compress=0 (raw PRESENT pages), "
                              "measured in this run after the headline steps"}
     t_dev = _max_over_ranks(pg, sum(dev))
+    per_step = [_max_over_ranks(pg, d) for d in dev]  # spread of the timed steps
+    step_ms = {"median": round(statistics.median(per_step) * 1e3, 3), "min": round(min(per_step) * 1e3, 3),
+               "max": round(max(per_step) * 1e3, 3),
+               "std": round(statistics.pstdev(per_step) * 1e3, 3) if len(per_step) > 1 else 0.0,
+               "what": "device time of each timed step (CUDA events, max over ranks)"}
     t_host = _max_over_ranks(pg, sum(host))
     t_box = _max_over_ranks(pg, sum(box))
     lock_ms = sum(r[1]["lock_ns"] for r in recs) / len(recs) * 1e-6
@@ -498,6 +503,7 @@ def run_ours(args):
         "steps": K,
         "warmup": args.warmup,
         "ms_per_step": round(t_dev / K * 1e3, 3),
+        "step_ms": step_ms,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
