@@ -491,13 +491,14 @@ gcr_status build_layout(gcr_ctx *c) {
     {
         std::vector<uint64_t> sizes;
         const char *ramp_env = std::getenv("GCR_CHUNK_RAMP");  // read per layout (tests flip it)
-        const bool ramp_on = ramp_env && ramp_env[0] == '1';
-        if (ramp_on && t >= 8 * ct && ct >= 8 * tpp) {
+        const int ramp_mode = ramp_env ? std::atoi(ramp_env) : 0;  // 1: both ends, 2: the end only
+        if (ramp_mode >= 1 && ramp_mode <= 2 && t >= 8 * ct && ct >= 8 * tpp) {
             const uint64_t r[3] = {ct / 8, ct / 4, ct / 2};
             uint64_t ramp = 0;
             for (uint64_t x : r) ramp += x / tpp * tpp;
-            uint64_t mid = t - 2 * ramp;
-            for (uint64_t x : r) sizes.push_back(x / tpp * tpp);
+            uint64_t mid = t - (ramp_mode == 1 ? 2 : 1) * ramp;
+            if (ramp_mode == 1)
+                for (uint64_t x : r) sizes.push_back(x / tpp * tpp);
             for (; mid > 0; mid -= std::min(mid, ct)) sizes.push_back(std::min(mid, ct));
             for (int k = 2; k >= 0; k--) sizes.push_back(r[k] / tpp * tpp);
         } else {

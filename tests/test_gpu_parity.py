@@ -192,15 +192,16 @@ def test_chunking_small_pages_many_chunks(G, orc, P, groups, monkeypatch):
                          zero_pages=[(0, 3), (0, 4), (1, 0), (2, 1), (3, 5)], seed=5)
 
 
+@pytest.mark.parametrize("ramp", ["1", "2"])
 @pytest.mark.parametrize("P,chunk", [(4096, 1 << 20), (1 << 20, 8 << 20)])
-def test_chunk_ramp_parity(G, orc, P, chunk, monkeypatch):
-    """With GCR_CHUNK_RAMP=1 a registry of >= 8 chunks gets ramped chunk sizes (1/8, 1/4, 1/2 chunk at
-    both ends, whole pages): image offsets, pagemap and digests stitched across
+def test_chunk_ramp_parity(G, orc, P, chunk, ramp, monkeypatch):
+    """With GCR_CHUNK_RAMP=1 (2) a registry of >= 8 chunks gets ramped chunk sizes (1/8, 1/4, 1/2 chunk at
+    both ends (at the end only), whole pages): image offsets, pagemap and digests stitched across
     chunks of every size, 4 KiB page groups (K1g) and 16-tile pages."""
     n = 9 * chunk
     sizes = [n // 2 + 16, n // 3 + 4096, n // 6 + P]
     zp = [(0, 1), (0, 2), (1, 3), (2, 0)]
-    monkeypatch.setenv("GCR_CHUNK_RAMP", "1")  # read by the library at each layout build (lock)
+    monkeypatch.setenv("GCR_CHUNK_RAMP", ramp)  # read by the library at each layout build (lock)
     _ckpt_restore_parity(G, orc, sizes, P, zero_pages=zp, chunk=chunk, streams=2, seed=77, direct_min=1 << 20)
 
 
