@@ -148,8 +148,8 @@ def probe_links(torch, ctx=None, nbytes=1 << 30):
     (gcr_probe_link: the pinned pages the next image lands on) and over a
     separate torch pinned buffer, plus an HBM read probe."""
     out = {}
-    if ctx is not None:
-        d2h, h2d = ctx.probe_link(nbytes)
+    if ctx is not None:  # the pool probe stages through a slot: at most one chunk
+        d2h, h2d = ctx.probe_link(min(nbytes, ctx.cfg.chunk_bytes))
         out["pool_d2h_gbs"], out["pool_h2d_gbs"] = round(d2h, 2), round(h2d, 2)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
