@@ -1997,6 +1997,18 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                                  sms[i].second, sms[i].first);
                 std::fprintf(stderr, "]}");
             }
+            {  // mean exit time by warp index within the CTA: is the tail a fixed scheduling order?
+                const uint64_t wpc = scan_warps_per_cta();
+                std::vector<double> sum(wpc, 0.0), cnt(wpc, 0.0);
+                for (uint64_t w = 0; w < sp.workers; w++) {
+                    sum[w % wpc] += (h[SW * w + 4] - t0) * 1e-3;
+                    cnt[w % wpc] += 1;
+                }
+                std::fprintf(stderr, ", \"exit_mean_us_by_warp_in_cta\": [");
+                for (uint64_t i = 0; i < wpc; i++)
+                    std::fprintf(stderr, "%s%.2f", i ? ", " : "", cnt[i] ? sum[i] / cnt[i] : 0.0);
+                std::fprintf(stderr, "]");
+            }
             std::fprintf(stderr, "}\n");
         }
         CUDA_TRY(c, cudaMemcpyAsync(c->misc_h + 1, c->misc_d + 1, 16, cudaMemcpyDeviceToHost, c->compute));

@@ -221,6 +221,7 @@ int launch_scatter(const ScatterDesc *desc, uint64_t n_desc, const uint8_t *slot
                    cudaStream_t st);
 int launch_zero_fill(const ZeroDesc *desc, uint64_t n_desc, int n_sms, cudaStream_t st);
 size_t scan_smem_bytes();
+uint64_t scan_warps_per_cta();  // K1 / K8 warps per CTA (GCR_SCAN_TIMES summaries)
 // Once per device (gcr_create): launch K1g in probe mode to read its dynamic
 // shared-memory base; K1g's immediate-base braid variant is used when the low
 // 16 bits match the compile-time value (kernels.cu kGrpSbLo).  Returns 0 / -1.

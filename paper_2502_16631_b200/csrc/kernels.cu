@@ -1682,6 +1682,7 @@ __global__ void __launch_bounds__(kTWarps * 32, 1) k_scatter_tma(const ScatterDe
 }  // namespace
 
 size_t scan_smem_bytes() { return kScanSmem; }
+uint64_t scan_warps_per_cta() { return kScanThreads / 32; }
 
 static int launched(int n) { return cudaPeekAtLastError() == cudaSuccess ? n : -1; }
 
