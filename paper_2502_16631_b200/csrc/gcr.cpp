@@ -1077,6 +1077,17 @@ static gcr_status checkpoint_impl(gcr_ctx *c, gcr_mode mode, gcr_image *img) {
     set_basis(c, sp);
     // f1: the scan writes PRESENT pages straight into the mapped image
     const bool isp = !coded && (c->cfg.in_scan_pack == 2 || (c->cfg.in_scan_pack == 1 && mode == GCR_INCREMENTAL));
+    // A full checkpoint needs chunk 0 early (the drain starts on it) and the
+    // rest only before the link frees up (~a chunk's drain later, 10-100x the
+    // scan of the rest): K1 splits chunks 1.. as ONE range over its warps and
+    // publishes them together -- one range start per warp instead of one per
+    // chunk.  Incremental checkpoints keep per-chunk publication (their drain
+    // follows the scan chunk by chunk).  GCR_SCAN_MERGE=0: off (A/B).
+    {
+        const char *e = std::getenv("GCR_SCAN_MERGE");
+        const bool merge = !(e && e[0] == '0');
+        sp.merge_from = merge && mode == GCR_FULL && !isp && nch > 2 ? 1u : 0u;
+    }
     if (isp) {
         void *dimg = nullptr;
         CUDA_TRY(c, cudaHostGetDevicePointer(&dimg, img->data, 0));

@@ -166,6 +166,11 @@ struct ScanParams {
     uint32_t t4rep;            // K1g: 8x-replicated raw16 table (see kernels.cu kT4RepBytes)
     const uint32_t *isp_page_alloc;  // f1: page -> allocation (K0's table)
     uint32_t *sb_probe;        // scan_probe(): the kernel writes its dynamic-smem base here and exits
+    // 0, or the first chunk of a tail that K1 splits over its warps as ONE range
+    // and publishes at once (full checkpoints: the drain needs chunk 0 early,
+    // the rest long before the link frees up; one range start per warp instead
+    // of one per chunk).  Never with the f1 in-scan pack (per-chunk lists).
+    uint32_t merge_from;
 };
 
 struct ScatterDesc {

@@ -819,9 +819,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     const uint32_t P = p.page_size, lg = p.log2_page;
     const uint32_t Rp = P >> kLog2Row;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
+        // chunks merge_from .. n_chunks-1 form ONE range split over the warps
+        // (full checkpoints: see ScanParams::merge_from); published together
+        const uint32_t ch_end = p.merge_from && ch == p.merge_from ? p.n_chunks : ch + 1;
         ChunkCtx cc;
         cc.rb = p.chunk_rows[ch];
-        cc.rows = p.chunk_rows[ch + 1] - cc.rb;
+        cc.rows = p.chunk_rows[ch_end] - cc.rb;
         cc.fs = p.fold.s + (uint64_t)ch * p.workers;
         if (p.isp.img) {
             isp_lists_free(p, g_isp, ch);
@@ -895,13 +898,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             }
         }
         if (p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
-        // this warp is done with chunk ch; the last one publishes it for K2
+        // this warp is done with chunk ch (.. ch_end - 1); the last one publishes it for K2
         if (lane == 0) {
             __threadfence();
             if (atomicAdd(p.chunk_arrive + ch, 1u) == (uint32_t)p.workers - 1u) {
                 atomicExch(p.chunk_arrive + ch, 0u);
                 __threadfence();
-                atomicExch(p.chunk_done + ch, p.epoch);
+                for (uint32_t c2 = ch; c2 < ch_end; c2++) atomicExch(p.chunk_done + c2, p.epoch);
             }
         }
         __syncwarp();
@@ -909,6 +912,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         // f1: write the previous chunk's PRESENT pages (every aggregate of it is
         // published by now, normally without waiting)
         if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
+        if (ch_end == p.n_chunks) break;
     }
     if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
@@ -996,7 +1000,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             isp_lists_free(p, g_isp, ch);
             isp_chunk_begin(ch, lane);
         }
-        const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch + 1] - cb;
+        const uint32_t ch_end = p.merge_from && ch == p.merge_from ? p.n_chunks : ch + 1;  // see k_scan
+        const uint64_t cb = p.chunk_groups[ch], n = p.chunk_groups[ch_end] - cb;
         const uint64_t g0 = cb + n * wid / p.workers, g1 = cb + n * (wid + 1) / p.workers;
         if (g0 < g1) {
             // load cursor (group gl_g, block lb) runs one block ahead of the process cursor
@@ -1124,12 +1129,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             if (atomicAdd(p.chunk_arrive + ch, 1u) == (uint32_t)p.workers - 1u) {
                 atomicExch(p.chunk_arrive + ch, 0u);
                 __threadfence();
-                atomicExch(p.chunk_done + ch, p.epoch);
+                for (uint32_t c2 = ch; c2 < ch_end; c2++) atomicExch(p.chunk_done + c2, p.epoch);
             }
         }
         __syncwarp();
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
         if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
+        if (ch_end == p.n_chunks) break;
     }
     if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
