@@ -192,9 +192,9 @@ bool crc_self_test() {
     {
         const uint64_t n = 3 * kCrcSplitMin + 40;
         uint8_t *buf = new uint8_t[n];
-        for (uint64_t i = 0; i < n; i++) buf[i] = (uint8_t)(i * 2654435761u >> 13);
+        for (uint64_t j = 0; j < n; j++) buf[j] = (uint8_t)(j * 2654435761u >> 13);
         uint32_t one = 0xFFFFFFFFu;
-        for (uint64_t i = 0; i < n; i += 4096) one = host_crc32c_update(one, buf + i, std::min<uint64_t>(4096, n - i));
+        for (uint64_t j = 0; j < n; j += 4096) one = host_crc32c_update(one, buf + j, std::min<uint64_t>(4096, n - j));
         const bool split_ok = host_crc32c_update(0xFFFFFFFFu, buf, n) == one;
         delete[] buf;
         if (!split_ok) {

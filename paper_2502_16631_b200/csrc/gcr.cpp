@@ -507,7 +507,7 @@ gcr_status build_layout(gcr_ctx *c) {
         uint64_t tb = 0;
         for (uint64_t n : sizes) {
             if (n == 0) continue;
-            c->chunks.push_back(Chunk{tb, tb + n, 0, 0});
+            c->chunks.push_back(Chunk{tb, tb + n, 0, 0, 0, 0});
             tb += n;
         }
     }
@@ -1969,11 +1969,11 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
             std::vector<unsigned long long> h(SW * sp.workers);
             cudaMemcpy(h.data(), wt, 8 * SW * sp.workers, cudaMemcpyDeviceToHost);
             cudaFree(wt);
-            unsigned long long t0 = ~0ull;
-            for (uint64_t w = 0; w < sp.workers; w++) t0 = std::min(t0, h[SW * w]);
-            auto pct = [](std::vector<double> v, double q) {
+            unsigned long long tw0 = ~0ull;
+            for (uint64_t w = 0; w < sp.workers; w++) tw0 = std::min(tw0, h[SW * w]);
+            auto pct = [](std::vector<double> v, double qq) {
                 std::sort(v.begin(), v.end());
-                return v[(size_t)(q * (v.size() - 1))];
+                return v[(size_t)(qq * (v.size() - 1))];
             };
             float kms = 0;
             cudaEventSynchronize(v1);
@@ -1984,7 +1984,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
             for (uint64_t k = 0; k < 5; k++) {
                 std::vector<double> v;
                 for (uint64_t w = 0; w < sp.workers; w++)
-                    if (h[SW * w + k]) v.push_back((h[SW * w + k] - t0) * 1e-3);
+                    if (h[SW * w + k]) v.push_back((h[SW * w + k] - tw0) * 1e-3);
                 if (v.empty()) continue;
                 std::fprintf(stderr, ", \"%s\": [%.2f, %.2f, %.2f, %.2f, %.2f]", names[k], pct(v, 0), pct(v, 0.1),
                              pct(v, 0.5), pct(v, 0.9), pct(v, 1));
@@ -1994,7 +1994,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                 std::vector<double> sum(256, 0.0), cnt(256, 0.0);
                 for (uint64_t w = 0; w < sp.workers; w++) {
                     const uint64_t sid = h[SW * w + 5] & 255u;
-                    sum[sid] += (h[SW * w + 4] - t0) * 1e-3;
+                    sum[sid] += (h[SW * w + 4] - tw0) * 1e-3;
                     cnt[sid] += 1;
                 }
                 std::vector<std::pair<double, int>> sms;
@@ -2012,7 +2012,7 @@ static gcr_status restore_impl(gcr_ctx *c, gcr_image *const *chain, uint32_t n, 
                 const uint64_t wpc = scan_warps_per_cta();
                 std::vector<double> sum(wpc, 0.0), cnt(wpc, 0.0);
                 for (uint64_t w = 0; w < sp.workers; w++) {
-                    sum[w % wpc] += (h[SW * w + 4] - t0) * 1e-3;
+                    sum[w % wpc] += (h[SW * w + 4] - tw0) * 1e-3;
                     cnt[w % wpc] += 1;
                 }
                 std::fprintf(stderr, ", \"exit_mean_us_by_warp_in_cta\": [");

@@ -1819,7 +1819,7 @@ bool scan_grp_imm() {
     return dev < 64 && g_grp_imm[dev];
 }
 
-int launch_scan(const ScanParams &p, int n_sms, cudaStream_t st) {
+int launch_scan(const ScanParams &p, int /*n_sms: the grid comes from p.workers*/, cudaStream_t st) {
     // once per device: setting a function attribute can serialise with work in
     // flight, which would leave the GPU idle between pipelined launches
     static bool attr_done[64] = {};
