@@ -308,3 +308,42 @@ def test_restore_region_ring_reuse(G, compress, chunk, ring, monkeypatch):
         ctx.unlock()
     finally:
         ctx.close()
+
+
+def test_rejected_coded_image_leaves_memory_untouched(G):
+    """The f4 restore copies the image's first group into a staging region
+    BEFORE the host validates the chain (speculative prefix).  A chain that
+    fails validation (one digest flipped in the pinned image: meta CRC
+    mismatch -> GCR_E_CORRUPT) must still leave every registered byte as it
+    was, keep the phase, and a valid restore right after must work."""
+    import ctypes as C
+    from paper_2502_16631_b200 import gcr as g
+    gcr, synth = G
+    P = 65536
+    ts = _mixed(G, P, seed=21)
+    ctx = gcr.Context(0, page_size=P, compress=1)
+    try:
+        registry_of(ctx, ts)
+        cont = host_copies(ts)
+        ctx.lock()
+        img = ctx.checkpoint()
+        for t in ts:
+            t.fill_(0x3C)
+        torch.cuda.synchronize()
+        poison = host_copies(ts)
+        p = g._P(g._u32)()
+        n = C.c_uint64()
+        ctx._check(g.gcr_image_digests(img.handle, C.byref(p), C.byref(n)))
+        p[0] ^= 0x1
+        st = ctx.try_restore([img])
+        assert st == gcr.GCR_E_CORRUPT
+        for t, x in zip(ts, poison):  # nothing written
+            assert np.array_equal(t.cpu().numpy(), x)
+        p[0] ^= 0x1
+        ctx.restore([img])
+        assert ctx.stats()["verify_failures"] == 0
+        for t, x in zip(ts, cont):
+            assert np.array_equal(t.cpu().numpy(), x)
+        ctx.unlock()
+    finally:
+        ctx.close()
