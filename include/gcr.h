@@ -301,8 +301,11 @@ gcr_status gcr_mem_free(gcr_ctx *ctx, uint64_t dptr);
 gcr_status gcr_release(gcr_ctx *ctx);
 
 /* LOCKED|CHECKPOINTED|RELEASED -> LOCKED: apply images chain[0..n) in order into the
- * registered allocations: PRESENT pages copied H2D and scattered (K6),
- * ZERO pages filled (K7), PARENT pages skipped; entries map to allocations by
+ * registered allocations: PRESENT pages copied H2D and scattered (K6;
+ * f4-coded images: decoded, KD), ZERO pages filled (K7), PARENT pages skipped.
+ * For a coded chain[0] the first staging group (its data prefix) is copied into
+ * the ctx's own staging memory before validation -- never into a registered
+ * allocation -- so it overlaps the host's checks; entries map to allocations by
  * index, so allocations may live at new addresses (R-14).  Then every page's
  * CRC32C is recomputed and compared with chain[n-1]'s digests (K8, R-11).
  * Validation happens before any write, in order: meta CRC (CORRUPT), version
