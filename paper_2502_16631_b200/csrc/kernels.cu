@@ -428,6 +428,7 @@ struct ChunkCtx {
 // 64-bit CAS folds {XOR contribution, + rows, + non-zero} (FoldSlots); the
 // arrival that completes the page's Rp - r0 real rows finalizes it from its
 // own CAS result.
+template <bool kIsp>
 __device__ __forceinline__ void fold_arrive(const ScanParams &p, ChunkCtx &cc, uint64_t g, uint32_t a,
                                             uint32_t pi, uint32_t r0, uint32_t rows, uint32_t contrib, bool nz) {
     const uint32_t P = p.page_size, lg = p.log2_page, Rp = P >> kLog2Row;
@@ -452,7 +453,7 @@ __device__ __forceinline__ void fold_arrive(const ScanParams &p, ChunkCtx &cc, u
     const uint32_t len = tail ? __ldg(&al->tail_len) : P;
     if (finalize_page(p, g, tile_of_page(__ldg(&al->tile0), pi, P, lg), pi == 0, len,
                       tail ? __ldg(&al->z_tail) : p.z_page, (uint32_t)nv, (nv >> 48) != 0ull) &&
-        p.isp.img)
+        (kIsp && p.isp.img))
         isp_note(p, g, len);
 }
 
@@ -692,6 +693,7 @@ __device__ __forceinline__ void pc_set_page(ProcCursor &pc, uint32_t P) {
 }
 
 // Page complete (vr == Rp): digest it (or leave a piece) and move on.
+template <bool kIsp>
 __device__ __forceinline__ void page_end(const ScanParams &p, ChunkCtx &cc, ProcCursor &pc, uint32_t (&x)[4],
                                          uint32_t &acc, const uint32_t *small, uint32_t lane) {
     const uint32_t P = p.page_size, lg = p.log2_page;
@@ -705,10 +707,10 @@ __device__ __forceinline__ void page_end(const ScanParams &p, ChunkCtx &cc, Proc
             const uint32_t len = tail ? pc.al.tail_len : P;
             if (finalize_page(p, g, tile_of_page(pc.al.tile0, pc.pi, P, lg), pc.pi == 0, len,
                               tail ? pc.al.z_tail : p.z_page, raw, nz) &&
-                p.isp.img)
+                (kIsp && p.isp.img))
                 isp_note(p, g, len);
         } else {  // the page's last piece: nothing left to advance over
-            fold_arrive(p, cc, g, pc.a, pc.pi, pc.r0, (P >> kLog2Row) - pc.vstart, raw, nz);
+            fold_arrive<kIsp>(p, cc, g, pc.a, pc.pi, pc.r0, (P >> kLog2Row) - pc.vstart, raw, nz);
         }
     }
     x[0] = x[1] = x[2] = x[3] = 0u;
@@ -721,7 +723,7 @@ __device__ __forceinline__ void page_end(const ScanParams &p, ChunkCtx &cc, Proc
 }
 
 // Digest the next block (the same cnt rows load_rows fetched into w).
-template <int U>
+template <int U, bool kIsp>
 __device__ __forceinline__ void process_rows(const ScanParams &p, ChunkCtx &cc, ProcCursor &pc, const uint4 (&w)[U],
                                              int &left, uint32_t (&x)[4], uint32_t &acc, const uint32_t *small,
                                              uint32_t lane4, uint32_t sb, uint32_t lane) {
@@ -737,7 +739,7 @@ __device__ __forceinline__ void process_rows(const ScanParams &p, ChunkCtx &cc, 
     }
     pc.vr += cnt;
     left -= cnt;
-    if (pc.vr == Rp) page_end(p, cc, pc, x, acc, small, lane);
+    if (pc.vr == Rp) page_end<kIsp>(p, cc, pc, x, acc, small, lane);
 }
 
 // Build the tables in shared memory from the launch's basis vectors
@@ -796,11 +798,15 @@ __device__ __forceinline__ void stage_tables(uint32_t *sm, const ScanParams &p) 
 }
 
 // K1.
+// kIsp = false (K1 scans without the f1 in-scan pack): the f1 hooks compiled
+// out -- same box, alternating (profiles/r2zq_*, r2zr_*): the incremental K1
+// 5.35 -> 5.51 TB/s, the full K1 +1 % with them gone.
+template <bool kIsp>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm);  // braid tables at the dynamic smem base
     const uint32_t *small = sm + kBraidSmem / 4;
-    if (p.isp.img) isp_init();
+    if (kIsp && p.isp.img) isp_init();
 
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u;
@@ -826,7 +832,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         cc.rb = p.chunk_rows[ch];
         cc.rows = p.chunk_rows[ch_end] - cc.rb;
         cc.fs = p.fold.s + (uint64_t)ch * p.workers;
-        if (p.isp.img) {
+        if (kIsp && p.isp.img) {
             isp_lists_free(p, g_isp, ch);
             isp_chunk_begin(ch, lane);
         }
@@ -882,10 +888,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
             }
             while (to_proc > 0) {
                 if (to_load > 0) load_rows<U>(wb, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
-                process_rows<U>(p, cc, pc, wa, to_proc, x, acc, small, lane4, sb, lane);
+                process_rows<U, kIsp>(p, cc, pc, wa, to_proc, x, acc, small, lane4, sb, lane);
                 if (to_proc <= 0) break;
                 if (to_load > 0) load_rows<U>(wa, to_load, lc, p.allocs, P, lg, lane, p.prefetch);
-                process_rows<U>(p, cc, pc, wb, to_proc, x, acc, small, lane4, sb, lane);
+                process_rows<U, kIsp>(p, cc, pc, wb, to_proc, x, acc, small, lane4, sb, lane);
             }
             // the range ended inside a page: advance the piece to the page end
             // (d = Rp - vr rows) and arrive at the page's owner slot
@@ -894,10 +900,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
                 const bool nz = __any_sync(kFull, acc != 0);
                 const uint32_t contrib = warp_mulmod(__ldg(&p.tables->fold_m[Rp - pc.vr]), raw, lane);
                 if (lane == 0)
-                    fold_arrive(p, cc, pc.al.page0 + pc.pi, pc.a, pc.pi, pc.r0, pc.vr - pc.vstart, contrib, nz);
+                    fold_arrive<kIsp>(p, cc, pc.al.page0 + pc.pi, pc.a, pc.pi, pc.r0, pc.vr - pc.vstart, contrib, nz);
             }
         }
-        if (p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
+        if (kIsp && p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
         // this warp is done with chunk ch (.. ch_end - 1); the last one publishes it for K2
         if (lane == 0) {
             __threadfence();
@@ -911,10 +917,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(const ScanParams p) {
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
         // f1: write the previous chunk's PRESENT pages (every aggregate of it is
         // published by now, normally without waiting)
-        if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
+        if (kIsp && p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
         if (ch_end == p.n_chunks) break;
     }
-    if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
+    if (kIsp && p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
@@ -1776,11 +1782,18 @@ bool scan_uses_groups(uint32_t page_size) {
     return !(e && e[0] == '0') && (page_size == kGroupBytes / 4 || page_size == kGroupBytes / 2);
 }
 
-static bool g_grp_imm[64] = {};  // per device: K1g's immediate-base variant verified by scan_probe()
+static bool g_grp_imm[64] = {};
+
+// GCR_K1_HOOKS=1: K1 / K8 always through the instance with the f1 hooks (A/B)
+static bool k1_hooks_always() {
+    const char *e = std::getenv("GCR_K1_HOOKS");
+    return e && e[0] == '1';
+}  // per device: K1g's immediate-base variant verified by scan_probe()
 
 static int scan_attrs() {
     const int big = (int)(kScanSmem + kT4RepBytes);
-    if (cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
+    if (cudaFuncSetAttribute(k_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(k_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
         cudaFuncSetAttribute(k_scan_grp<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
         cudaFuncSetAttribute(k_scan_grp<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
         cudaFuncSetAttribute(k_scan_grp<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
@@ -1840,8 +1853,14 @@ int launch_scan(const ScanParams &p, int /*n_sms: the grid comes from p.workers*
     } else if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 2) {
         if (imm) k_scan_grp<2, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
         else k_scan_grp<2, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-    } else
-        k_scan<<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    } else if (p.isp.img != nullptr || p.mode == kScanVerify || k1_hooks_always()) {
+        // the verify (K8) also measured ~1 % faster through the hooked instance
+        // (hooks inactive: p.isp.img is null), profiles/r2zr_*: 5.24-5.25 vs
+        // 5.18-5.20 TB/s on C2 -- code placement, not work
+        k_scan<true><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    } else {
+        k_scan<false><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
+    }
     return launched(1);
 }
 
