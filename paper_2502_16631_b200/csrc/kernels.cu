@@ -973,12 +973,20 @@ __device__ __forceinline__ uint32_t alloc_of_group(const AllocDev *al, uint32_t 
 // K1g's dynamic shared-memory base, low 16 bits, as laid out by this build
 // (1 KiB reserved + the f1 state in static shared memory); verified per device
 // by scan_probe(), which falls back to the IADD variant on a mismatch.
+// Two immediate-base instances: with the f1 hooks (the f1 state in static
+// shared memory moves the dynamic base to 0xA00) and without them (0x400).
 #ifndef GCR_GRP_SB_LO
 #define GCR_GRP_SB_LO 0xA00
 #endif
-constexpr uint32_t kGrpSbLo = GCR_GRP_SB_LO;
+#ifndef GCR_GRP_SB_LO_PLAIN
+#define GCR_GRP_SB_LO_PLAIN 0x400
+#endif
+constexpr uint32_t kGrpSbLo = GCR_GRP_SB_LO, kGrpSbLoPlain = GCR_GRP_SB_LO_PLAIN;
 
-template <int G, bool kImm>
+// kImm: table base in the PRMT + immediate (else the IADD per lookup);
+// kHooks: the f1 in-scan-pack hooks compiled in (K1 measured 3 % slower with
+// them, profiles/r2zq_*; scans without f1 run a hook-free instance).
+template <int G, bool kImm, bool kHooks>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p) {
     constexpr uint32_t QL = 32 / G, Wr = kRowBytes / G, Rg = 32, U = 4, NB = Rg / U;
     extern __shared__ __align__(16) uint32_t sm[];
@@ -987,7 +995,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
         if (threadIdx.x == 0 && blockIdx.x == 0) *p.sb_probe = sb;
         return;
     }
-    if (p.isp.img) isp_init();
+    if (kHooks && p.isp.img) isp_init();
     const uint32_t *small = sm + kBraidSmem / 4;
     const uint64_t t_entry = p.warp_times ? globaltimer_ns() : 0ull;
     const uint32_t lane = threadIdx.x & 31u, lane4 = lane * 4u, q = lane / QL, m = lane % QL;
@@ -1002,7 +1010,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
     }
     const uint32_t P = p.page_size, lg = p.log2_page;
     for (uint32_t ch = 0; ch < p.n_chunks; ch++) {
-        if (p.isp.img) {
+        if (kHooks && p.isp.img) {
             isp_lists_free(p, g_isp, ch);
             isp_chunk_begin(ch, lane);
         }
@@ -1050,7 +1058,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
             auto process_block = [&](const uint4 (&w)[U]) {
                 if constexpr (kImm) {
 #pragma unroll
-                    for (uint32_t u = 0; u < U; u++) row_step_imm<kGrpSbLo>(lbase, x, acc, w[u]);
+                    for (uint32_t u = 0; u < U; u++) row_step_imm<kHooks ? kGrpSbLo : kGrpSbLoPlain>(lbase, x, acc, w[u]);
                 } else {
 #pragma unroll
                     for (uint32_t u = 0; u < U; u++) row_step(lane4, sb, x, acc, w[u]);
@@ -1086,7 +1094,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                     pres = finalize_page(p, pal.page0 + pgl.pi, tile_of_page(pal.tile0, pgl.pi, P, lg), pgl.pi == 0,
                                          plen, tail ? pal.z_tail : p.z_page, v, nzq != 0u);
                 }
-                if (p.isp.img) {  // f1: the group's PRESENT pages, in lane (= page) order
+                if (kHooks && p.isp.img) {  // f1: the group's PRESENT pages, in lane (= page) order
                     const uint32_t bal2 = __ballot_sync(kFull, pres);
                     const uint32_t wib = threadIdx.x >> 5, par = ch & 1u, n0 = g_isp.wn[par][wib];
                     const uint32_t bytes = __reduce_add_sync(kFull, pres ? plen : 0u);
@@ -1127,7 +1135,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
                 process_block(wb);
             }
         }
-        if (p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
+        if (kHooks && p.isp.img) isp_chunk_end(p, g_isp, ch, lane);  // f1: the warp's aggregate
         // every leader lane's page results visible before lane 0 publishes
         __threadfence();
         __syncwarp();
@@ -1140,10 +1148,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan_grp(const ScanParams p
         }
         __syncwarp();
         if (p.warp_times && lane == 0 && ch == 0) p.warp_times[kStamps * wid + 3] = globaltimer_ns();
-        if (p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
+        if (kHooks && p.isp.img && ch >= 1) isp_write(p, g_isp, ch - 1, wid, lane);
         if (ch_end == p.n_chunks) break;
     }
-    if (p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
+    if (kHooks && p.isp.img && p.n_chunks) isp_write(p, g_isp, p.n_chunks - 1, wid, lane);
     if (p.warp_times && lane == 0) p.warp_times[kStamps * wid + 4] = globaltimer_ns();
 }
 
@@ -1782,7 +1790,8 @@ bool scan_uses_groups(uint32_t page_size) {
     return !(e && e[0] == '0') && (page_size == kGroupBytes / 4 || page_size == kGroupBytes / 2);
 }
 
-static bool g_grp_imm[64] = {};
+static bool g_grp_imm[64] = {};        // per device: K1g immediate-base instance with the f1 hooks verified
+static bool g_grp_imm_plain[64] = {};  // ... and the hook-free one
 
 // GCR_K1_HOOKS=1: K1 / K8 always through the instance with the f1 hooks (A/B)
 static bool k1_hooks_always() {
@@ -1794,10 +1803,12 @@ static int scan_attrs() {
     const int big = (int)(kScanSmem + kT4RepBytes);
     if (cudaFuncSetAttribute(k_scan<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
         cudaFuncSetAttribute(k_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScanSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-        cudaFuncSetAttribute(k_scan_grp<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess)
+        cudaFuncSetAttribute(k_scan_grp<4, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
+        cudaFuncSetAttribute(k_scan_grp<4, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
+        cudaFuncSetAttribute(k_scan_grp<4, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
+        cudaFuncSetAttribute(k_scan_grp<2, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
+        cudaFuncSetAttribute(k_scan_grp<2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
+        cudaFuncSetAttribute(k_scan_grp<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess)
         return -1;
     return 0;
 }
@@ -1808,28 +1819,34 @@ int scan_probe() {
     if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return -1;
     const char *e = std::getenv("GCR_GRP_IMM");
     if (scan_attrs() != 0) return -1;
-    uint32_t *d = nullptr, h[2] = {~0u, ~0u};
-    if (cudaMalloc(&d, 8) != cudaSuccess) return -1;
+    uint32_t *d = nullptr, h[4] = {~0u, ~0u, ~0u, ~0u};
+    if (cudaMalloc(&d, 16) != cudaSuccess) return -1;
     ScanParams p{};
-    for (int v = 0; v < 2; v++) {
+    for (int v = 0; v < 4; v++) {
         p.sb_probe = d + v;
-        if (v == 0) k_scan_grp<4, true><<<1, kScanThreads, kScanSmem>>>(p);
-        else k_scan_grp<2, true><<<1, kScanThreads, kScanSmem>>>(p);
+        if (v == 0) k_scan_grp<4, true, true><<<1, kScanThreads, kScanSmem>>>(p);
+        else if (v == 1) k_scan_grp<2, true, true><<<1, kScanThreads, kScanSmem>>>(p);
+        else if (v == 2) k_scan_grp<4, true, false><<<1, kScanThreads, kScanSmem>>>(p);
+        else k_scan_grp<2, true, false><<<1, kScanThreads, kScanSmem>>>(p);
     }
-    const bool ok = cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost) == cudaSuccess;
+    const bool ok = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost) == cudaSuccess;
     cudaFree(d);
     if (!ok) return -1;
-    g_grp_imm[dev] = !(e && e[0] == '0') && (h[0] & 0xFFFFu) == kGrpSbLo && (h[1] & 0xFFFFu) == kGrpSbLo;
+    const bool allow = !(e && e[0] == '0');
+    g_grp_imm[dev] = allow && (h[0] & 0xFFFFu) == kGrpSbLo && (h[1] & 0xFFFFu) == kGrpSbLo;
+    g_grp_imm_plain[dev] = allow && (h[2] & 0xFFFFu) == kGrpSbLoPlain && (h[3] & 0xFFFFu) == kGrpSbLoPlain;
     if (std::getenv("GCR_TRACE"))
-        std::fprintf(stderr, "{\"gcr_scan_probe\": {\"sb\": [%u, %u], \"expected_lo\": %u, \"k1g_imm\": %d}}\n", h[0], h[1],
-                     kGrpSbLo, (int)g_grp_imm[dev]);
+        std::fprintf(stderr,
+                     "{\"gcr_scan_probe\": {\"sb_hooks\": [%u, %u], \"sb_plain\": [%u, %u], \"expected_lo\": [%u, %u], "
+                     "\"k1g_imm\": [%d, %d]}}\n",
+                     h[0], h[1], h[2], h[3], kGrpSbLo, kGrpSbLoPlain, (int)g_grp_imm[dev], (int)g_grp_imm_plain[dev]);
     return 0;
 }
 
 bool scan_grp_imm() {
     int dev = 0;
     cudaGetDevice(&dev);
-    return dev < 64 && g_grp_imm[dev];
+    return dev < 64 && (g_grp_imm[dev] || g_grp_imm_plain[dev]);
 }
 
 int launch_scan(const ScanParams &p, int /*n_sms: the grid comes from p.workers*/, cudaStream_t st) {
@@ -1845,14 +1862,19 @@ int launch_scan(const ScanParams &p, int /*n_sms: the grid comes from p.workers*
     if (p.n_chunks == 0) return 0;
     const uint64_t wpb = kScanThreads / 32;
     const uint64_t grid = (p.workers + wpb - 1) / wpb;
-    const bool imm = dev < 64 && g_grp_imm[dev];
+    // K1g instance: hook-free immediate base unless f1 is on (or GCR_K1_HOOKS=1),
+    // else the hooked immediate base, else (a probe mismatched) the IADD one
+    const bool hooks = p.isp.img != nullptr || k1_hooks_always();
+    const int v = dev >= 64 ? 2 : (!hooks && g_grp_imm_plain[dev]) ? 0 : g_grp_imm[dev] ? 1 : 2;
     const size_t gsm = kScanSmem + (p.t4rep ? kT4RepBytes : 0u);
     if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 4) {
-        if (imm) k_scan_grp<4, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-        else k_scan_grp<4, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
+        if (v == 0) k_scan_grp<4, true, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
+        else if (v == 1) k_scan_grp<4, true, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
+        else k_scan_grp<4, false, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
     } else if (p.chunk_groups != nullptr && p.page_size == kGroupBytes / 2) {
-        if (imm) k_scan_grp<2, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-        else k_scan_grp<2, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
+        if (v == 0) k_scan_grp<2, true, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
+        else if (v == 1) k_scan_grp<2, true, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
+        else k_scan_grp<2, false, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
     } else if (p.isp.img != nullptr || p.mode == kScanVerify || k1_hooks_always()) {
         // the verify (K8) also measured ~1 % faster through the hooked instance
         // (hooks inactive: p.isp.img is null), profiles/r2zr_*: 5.24-5.25 vs
