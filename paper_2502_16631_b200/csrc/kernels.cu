@@ -1875,10 +1875,14 @@ int launch_scan(const ScanParams &p, int /*n_sms: the grid comes from p.workers*
         if (v == 0) k_scan_grp<2, true, false><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
         else if (v == 1) k_scan_grp<2, true, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
         else k_scan_grp<2, false, true><<<(unsigned)grid, kScanThreads, gsm, st>>>(p);
-    } else if (p.isp.img != nullptr || p.mode == kScanVerify || k1_hooks_always()) {
-        // the verify (K8) also measured ~1 % faster through the hooked instance
-        // (hooks inactive: p.isp.img is null), profiles/r2zr_*: 5.24-5.25 vs
-        // 5.18-5.20 TB/s on C2 -- code placement, not work
+    } else if (p.isp.img != nullptr || p.mode == kScanVerify || p.page_size > kTileBytes || k1_hooks_always()) {
+        // The hook-free instance wins only for scans at <= 64 KiB pages
+        // (profiles/r2zr_*: incremental 5.35 -> 5.51, full +1 %).  The verify
+        // (K8) measured ~1 % faster through the hooked instance (5.24-5.25 vs
+        // 5.18-5.20 TB/s on C2) and so did scans of > 64 KiB pages, where
+        // every warp range ends in a cut-page fold (C5 16 GiB at 2 MiB: 6.01-6.03
+        // vs 5.49-5.50, profiles/r2zv_*) -- code placement, not work: the hooks
+        // are inactive there (p.isp.img is null).
         k_scan<true><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
     } else {
         k_scan<false><<<(unsigned)grid, kScanThreads, kScanSmem, st>>>(p);
